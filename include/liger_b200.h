@@ -1,0 +1,238 @@
+/*
+ * liger_b200.h — C ABI of the B200-native (sm_100a) Liger training hot path.
+ *
+ * This is the drop-in boundary for the reference's fused-kernel layer
+ * (/root/reference/pkg/src/rowfuse/ops.py and flce.py, surveyed in SURVEY.md
+ * §8(a)/(b)) and for the third-party Liger operator surface those kernels stand
+ * for (liger_kernel 0.8.0, ops/*.py).  The reference is pure Python, so there is
+ * no FFI to replace; each entry point below is what a ctypes/cffi binding of the
+ * reference's operator would call (see INTEGRATION.md for the binding stubs).
+ *
+ * Conventions (all entry points):
+ *   - Plain device pointers, int64 sizes, a cudaStream_t passed as void*.
+ *   - The library never allocates device memory: scratch is a caller-provided
+ *     workspace sized by the matching *_workspace_bytes() query.  Peak memory is
+ *     therefore attributable to the caller's allocator (SURVEY §8(b) ownership).
+ *   - Calls are stream-ordered and asynchronous; none of them synchronises the
+ *     host.  Target-range violations are reported through a device flag written
+ *     into the workspace (lk_status LK_TARGET_OUT_OF_RANGE is set by the host
+ *     wrapper after reading it), mirroring rowfuse's TargetOutOfRange
+ *     (rowfuse/core.py:45-46, ops.py:489-499).
+ *   - Return value: 0 on success, otherwise an lk_status code; the message is
+ *     available from lk_last_error() (thread-local).  Status codes mirror the
+ *     reference error taxonomy (rowfuse/core.py:25-46).
+ *   - All offsets are computed in 64-bit (rowfuse/core.py:86-94 makes 64-bit
+ *     offsets a design decision once rows*cols-1 > 2^31-1; cfg4/cfg5 exceed it).
+ */
+#ifndef LIGER_B200_H
+#define LIGER_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- types ------------------------------------------------------------- */
+
+typedef enum {
+  LK_F32 = 0,
+  LK_BF16 = 1,
+  LK_F16 = 2
+} lk_dtype;
+
+typedef enum {
+  LK_OK = 0,
+  LK_NON_CONTIGUOUS = 1,      /* rowfuse/core.py:33-39 NonContiguousInput   */
+  LK_SHAPE_MISMATCH = 2,      /* rowfuse/core.py:29-30 ShapeMismatch        */
+  LK_SIZE_MISMATCH = 3,       /* rowfuse/core.py:25-26 SizeMismatch         */
+  LK_ODD_HEAD_DIM = 4,        /* rowfuse/core.py:41-42 OddHeadDim           */
+  LK_TARGET_OUT_OF_RANGE = 5, /* rowfuse/core.py:45-46 TargetOutOfRange     */
+  LK_UNSUPPORTED = 6,         /* option the kernels do not implement         */
+  LK_CUDA_ERROR = 7,          /* launch / runtime failure                     */
+  LK_INVALID_ARGUMENT = 8     /* null pointer, bad enum, workspace too small  */
+} lk_status;
+
+typedef enum {
+  LK_REDUCTION_NONE = 0,
+  LK_REDUCTION_MEAN = 1, /* Liger: mean over non-ignored rows (LK/ops/cross_entropy.py:218-219) */
+  LK_REDUCTION_SUM = 2
+} lk_reduction;
+
+typedef enum {
+  LK_CAST_LLAMA = 0, /* LK/ops/rms_norm.py:83-112: rstd fp32, xhat cast before *w */
+  LK_CAST_GEMMA = 1, /* all fp32, cast at the end                                */
+  LK_CAST_NONE = 2   /* compute in the input dtype                              */
+} lk_casting_mode;
+
+/* ---- library ----------------------------------------------------------- */
+
+const char* lk_last_error(void);
+const char* lk_version(void);
+/* 1 if the .so was built with the sm_100a tcgen05 GEMM path. */
+int lk_has_tcgen05(void);
+
+/* Instrumentation for the benchmark (off by default).  When enabled, the FLCE
+ * entry points record CUDA events on the launching stream around each stage:
+ *   0 = logits GEMM (tcgen05 or SIMT), 1 = finalize (softmax-grad rows),
+ *   2 = backward GEMM (dX + dW), 3 = other (target count, loss reduction, bias).
+ * lk_profile_collect() waits for the recorded events, writes the summed
+ * milliseconds and launch counts per stage, and clears the record.
+ * lk_launch_count() is the number of kernels this library has launched. */
+void lk_profile_enable(int on);
+int lk_profile_collect(double* ms4, int64_t* launches4);
+int64_t lk_launch_count(void);
+
+/* ---- cross entropy (standalone) ---------------------------------------- */
+/*
+ * Replaces rowfuse.ops.cross_entropy (rowfuse/ops.py:502-560) and
+ * liger_kernel.ops.cross_entropy.cross_entropy_forward (LK/ops/cross_entropy.py:302-407).
+ * logits[rows, ld] (row-major, unit column stride) is overwritten in place with
+ * d(loss)/d(logits) when compute_grad != 0.  loss_rows[rows] (fp32) receives the
+ * per-row loss (already divided by the non-ignored count for MEAN);
+ * loss_sum (fp32 scalar, may be NULL) receives the deterministic sum of loss_rows.
+ * z_loss_rows / z_loss_sum optional (lse_square_scale term).
+ * softcap <= 0 means "no softcap".
+ */
+size_t lk_cross_entropy_workspace_bytes(int64_t rows);
+int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* targets, int64_t rows,
+                         int64_t vocab, int dtype, int64_t ignore_index, float label_smoothing,
+                         float lse_square_scale, float softcap, int reduction, int compute_grad,
+                         float* loss_rows, float* loss_sum, float* z_loss_rows, float* z_loss_sum,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Count of targets != ignore_index and the out-of-range flag, on device.
+ * out[0] = n_non_ignore (as int64), out[1] = number of out-of-range targets. */
+int lk_count_targets(const int64_t* targets, int64_t rows, int64_t vocab, int64_t ignore_index,
+                     int64_t* out, void* stream);
+
+/* x[rows, cols] (row stride ld) *= scale, where scale is a device fp32 scalar
+ * (grad_output of a reduced loss) — the backward of CE/FLCE
+ * (LK/ops/cross_entropy.py:415-440, LK/ops/fused_linear_cross_entropy.py:247-291).
+ * The kernel early-exits when *scale == 1.0f, so no host sync is needed.  */
+int lk_scale_by_device_scalar(void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
+                              const float* scale, void* stream);
+/* x[r, :] *= row_scale[r] (reduction="none" backward, LK/ops/cross_entropy.py:424-426). */
+int lk_scale_rows(void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
+                  const void* row_scale, int row_scale_dtype, void* stream);
+
+/* ---- fused linear cross entropy ---------------------------------------- */
+/*
+ * Replaces rowfuse.flce.flce_forward_backward (rowfuse/flce.py:107-173) and
+ * liger_kernel's fused_linear_cross_entropy_forward (LK/ops/fused_linear_cross_entropy.py:17-244).
+ * Layout follows Liger: x[BT, H], weight[V, H] (rowfuse stores W as (H, V); the
+ * Python adapter transposes for the oracle).  Gradients are produced during the
+ * forward: grad_x[BT, H] in x's dtype, grad_w[V, H] in weight's dtype (accumulated
+ * in fp32 in the workspace across chunks).  Either grad pointer may be NULL to
+ * skip that gradient.  chunk_rows <= 0 selects the B200 chunk policy
+ * (lk_flce_plan); otherwise any positive row count is honoured (the reference's
+ * ChunkPlan.with_chunk_rows override, rowfuse/flce.py:58-66).
+ */
+typedef struct {
+  const void* x;          /* [BT, H] contiguous                                */
+  const void* weight;     /* [V, H] contiguous                                 */
+  const int64_t* target;  /* [BT]                                              */
+  const void* bias;       /* [V] or NULL                                       */
+  int64_t bt, hidden, vocab;
+  int dtype;              /* lk_dtype of x and weight (must match)             */
+  int64_t ignore_index;
+  float label_smoothing;
+  float lse_square_scale;
+  float softcap;          /* <= 0: none                                        */
+  int reduction;          /* lk_reduction                                      */
+  int64_t chunk_rows;     /* <= 0: lk_flce_plan                                */
+  /* outputs */
+  float* loss_rows;       /* [BT] fp32 (required)                              */
+  float* loss_sum;        /* scalar fp32 or NULL                               */
+  float* z_loss_rows;     /* [BT] fp32 or NULL                                 */
+  float* z_loss_sum;      /* scalar or NULL                                    */
+  void* grad_x;           /* [BT, H] dtype or NULL                             */
+  void* grad_w;           /* [V, H] dtype or NULL                              */
+  void* grad_bias;        /* [V] dtype or NULL                                 */
+  int64_t* target_stats;  /* [2] n_non_ignore, n_out_of_range (device) or NULL */
+  /* scratch */
+  void* workspace;
+  size_t workspace_bytes;
+  void* stream;
+  int force_simt;         /* 1: use the SIMT GEMM path (debug/fp32)            */
+  /* Token-sharded mode: device int64 holding the GLOBAL non-ignored count used as
+   * the MEAN denominator (all-reduced by the caller); NULL = local count. */
+  const int64_t* mean_count;
+} lk_flce_args;
+
+/* B200 chunk policy.  Writes the chunk row count and number of chunks. */
+int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t* chunk_rows,
+                 int64_t* num_chunks);
+size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
+                               int64_t chunk_rows, int has_grad_w);
+int lk_flce_forward_backward(const lk_flce_args* args);
+
+/*
+ * Staged FLCE entry points for the vocab-parallel mode: each rank
+ * holds weight rows [v0, v0+vocab_local).  Stage 1 produces per-row partial
+ * softmax statistics for the local shard; the caller all-reduces them across
+ * ranks (max, then rescaled sum), then stage 2 writes dlogits for the local
+ * shard and accumulates grad_x (to be all-reduced by the caller) and the local
+ * grad_w shard.
+ *   row_stats layout: [rows, 4] fp32 = (max, sumexp, sum_logits, target_logit),
+ *   target_logit is 0 on ranks that do not own the target column.
+ */
+size_t lk_flce_vp_workspace_bytes(int64_t rows, int64_t hidden, int64_t vocab_local, int dtype);
+int lk_flce_vp_logits(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                      int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int dtype,
+                      int64_t ignore_index, float softcap, float* row_stats, void* logits_buf,
+                      void* workspace, size_t workspace_bytes, void* stream);
+int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* target,
+                        int64_t rows, int64_t hidden, int64_t vocab_local, int64_t vocab_offset,
+                        int64_t vocab_total, int dtype, int64_t ignore_index, float label_smoothing,
+                        float lse_square_scale, float softcap, int reduction,
+                        const int64_t* n_non_ignore, const float* row_stats_global,
+                        void* logits_buf, float* loss_rows, void* grad_x_partial_f32,
+                        float* grad_w_accum, int accumulate, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
+/* ---- RMSNorm ----------------------------------------------------------- */
+/* rowfuse/ops.py:190-241 and LK/ops/rms_norm.py (forward 58-112, backward 115-210).
+ * rstd[rows] is fp32 for llama/gemma casting, x dtype for "none". weight may be NULL
+ * (elementwise_affine=False).  dw_partial is a caller workspace of
+ * lk_rmsnorm_bwd_workspace_bytes(); dw receives sum over rows in weight dtype. */
+int lk_rmsnorm_fwd(const void* x, const void* weight, void* y, void* rstd, int64_t rows,
+                   int64_t cols, float eps, float offset, int casting_mode, int dtype, void* stream);
+size_t lk_rmsnorm_bwd_workspace_bytes(int64_t rows, int64_t cols);
+int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight, const void* rstd, void* dx,
+                   void* dw, int64_t rows, int64_t cols, float offset, int casting_mode, int dtype,
+                   void* workspace, size_t workspace_bytes, void* stream);
+
+/* ---- RoPE -------------------------------------------------------------- */
+/* rowfuse/ops.py:344-382 and LK/ops/rope.py:6-112.  q[B, T, nq, d] and
+ * k[B, T, nk, d] are rotated in place (half-split HF layout); cos/sin are
+ * [cos_batch, T, d] with cos_batch in {1, B}; only cos[..., :d/2] is read.
+ * backward != 0 applies the transpose rotation (sin negated). */
+int lk_rope(void* q, void* k, const void* cos, const void* sin, int64_t batch, int64_t seq,
+            int64_t n_q_heads, int64_t n_kv_heads, int64_t head_dim, int64_t cos_batch,
+            int dtype, int cos_dtype, int backward, void* stream);
+
+/* ---- SwiGLU / GeGLU ---------------------------------------------------- */
+/* rowfuse/ops.py:389-482, LK/ops/swiglu.py:15-62, LK/ops/geglu.py:23-88.
+ * c = act(a) * b over n contiguous elements; backward writes da into a and db
+ * into b in place (Liger semantics). */
+int lk_swiglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream);
+int lk_swiglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream);
+int lk_geglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream);
+int lk_geglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream);
+
+/* ---- GEMM test hook ----------------------------------------------------- */
+/* D[M, N] (fp32, row-major) = A · B for the three operand layouts FLCE uses
+ * (layout 0: A[M,K] K-major, B[N,K] K-major; 1: A[M,K] K-major, B[K,N] N-major;
+ * 2: A[K,M] M-major, B[K,N] N-major).  use_tcgen05 selects the sm_100a path.
+ * Used by the kernel tests only. */
+int lk_gemm_test(const void* a, const void* b, float* d, int64_t m, int64_t n, int64_t k,
+                 int layout, int dtype, int use_tcgen05, void* workspace, size_t workspace_bytes,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LIGER_B200_H */

@@ -1,0 +1,75 @@
+"""Torch plumbing around the C ABI: device checks, dtype codes, streams, workspaces.
+
+PyTorch only provides device memory (caching allocator) and the current stream;
+all arithmetic on the path happens in the sm_100a library.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _capi, errors
+
+_DTYPE_CODE = {torch.float32: _capi.LK_F32, torch.bfloat16: _capi.LK_BF16, torch.float16: _capi.LK_F16}
+
+# Read the device-side out-of-range target count after CE/FLCE and raise
+# TargetOutOfRange like the reference (rowfuse/ops.py:496-498).  Costs one 16-byte
+# device->host read per call (Liger syncs on .item() as well).
+CHECK_TARGETS = True
+
+
+def dtype_code(t: torch.Tensor) -> int:
+    try:
+        return _DTYPE_CODE[t.dtype]
+    except KeyError:
+        raise errors.ShapeMismatch(f"unsupported dtype {t.dtype}; expected float32, bfloat16 or float16") from None
+
+
+def require_cuda(*tensors: torch.Tensor | None) -> None:
+    for t in tensors:
+        if t is not None and not t.is_cuda:
+            raise errors.ExtensionMissing(
+                "paper_2410_10989_b200 runs only on CUDA (sm_100a); got a tensor on "
+                f"{t.device}. There is no CPU fallback."
+            )
+
+
+def require_contiguous(name: str, t: torch.Tensor) -> None:
+    if not t.is_contiguous():
+        raise errors.NonContiguousInput(f"{name} must be contiguous (rowfuse/core.py:210-215)")
+
+
+def ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_of(t: torch.Tensor) -> int:
+    return torch.cuda.current_stream(t.device).cuda_stream
+
+
+def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+
+
+def lib():
+    return _capi.load()
+
+
+def check(rc: int) -> None:
+    _capi.check(rc)
+
+
+def as_targets(target: torch.Tensor) -> torch.Tensor:
+    if target.dtype not in (torch.int64, torch.int32, torch.int16, torch.uint8, torch.int8):
+        raise errors.ShapeMismatch(f"targets must be integer class ids, got {target.dtype}")
+    t = target.reshape(-1)
+    if t.dtype != torch.int64:
+        t = t.to(torch.int64)
+    return t.contiguous()
+
+
+def raise_if_out_of_range(stats: torch.Tensor, vocab: int) -> None:
+    if CHECK_TARGETS and int(stats[1].item()) > 0:
+        raise errors.TargetOutOfRange(
+            f"{int(stats[1].item())} target(s) outside [0, {vocab}) that are not ignore_index"
+        )

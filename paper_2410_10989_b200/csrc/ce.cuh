@@ -1,0 +1,222 @@
+// Row-wise online-softmax cross entropy, gradient written in place.
+//
+// One kernel serves two callers:
+//   * standalone CE (rowfuse/ops.py:502-560, LK/ops/cross_entropy.py:26-299):
+//     pass 1 streams the row once for (max, sumexp, sum_logits); pass 2 rewrites
+//     the row with d(loss)/d(logits).  Two reads + one write of the row.
+//   * FLCE finalize (rowfuse/flce.py:155-157): the tcgen05 logits GEMM epilogue
+//     already produced per-(row, N-tile) partial statistics, so pass 1 collapses
+//     to a combine over ~V/256 partials and the row is read once and written once.
+//
+// Semantics follow Liger (LK/ops/cross_entropy.py:100-289): ignore_index rows get
+// zero loss and zero gradient; label smoothing eps = ls / V; z-loss lse_square_scale;
+// softcap cap*tanh(z/cap) with the (1 - tanh^2) chain rule; MEAN divides by the
+// device-side non-ignored count.
+#pragma once
+#include "common.cuh"
+
+namespace lk {
+
+struct CeRowArgs {
+  void* x;                 // [rows, ld] logits in dtype T, overwritten with grad
+  int64_t ld;
+  const int64_t* target;   // [rows]
+  int64_t rows;
+  int64_t n_cols;          // columns held in x (local vocab shard)
+  int64_t vocab_total;     // V used for the smoothing eps (== n_cols unless vocab-parallel)
+  int64_t col_offset;      // global column of x[:, 0] (vocab-parallel), else 0
+  int64_t ignore_index;
+  float label_smoothing;
+  float lse_square_scale;
+  float softcap;           // <= 0: none
+  int input_capped;        // x already holds cap*tanh(z/cap) (FLCE epilogue output)
+  int reduction;
+  int compute_grad;
+  const int64_t* n_valid;  // device count of non-ignored targets (MEAN)
+  float* loss_rows;        // [rows] or null
+  float* z_loss_rows;      // [rows] or null
+  // precomputed statistics (either, or neither):
+  const float4* partials;  // [rows, n_parts] (max, sumexp, sum_logits, -) per N tile
+  int64_t n_parts;
+  const float* tgt_logit;  // [rows] capped target logit (with partials)
+  const float4* row_stats; // [rows] global (max, sumexp, sum_logits, target_logit) (vocab-parallel)
+};
+
+template <typename T>
+__device__ __forceinline__ float cap_val(float z, float cap, bool accurate) {
+  float t = accurate ? tanhf(z / cap) : tanh_fast(z / cap);
+  return cap * t;
+}
+
+template <typename T, int BLOCK>
+__global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
+  constexpr int NV = Vec16<T>::N;
+  constexpr bool ACCURATE = sizeof(T) == 4;
+  __shared__ float red_m[BLOCK / 32], red_s[BLOCK / 32], red_z[BLOCK / 32];
+  __shared__ float bcast[4];
+
+  const int64_t row = blockIdx.x;
+  if (row >= a.rows) return;
+  T* x = static_cast<T*>(a.x) + row * a.ld;
+  const int64_t n = a.n_cols;
+  const int64_t y = a.target[row];
+  const bool has_cap = a.softcap > 0.f;
+  const float cap = a.softcap;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (y == a.ignore_index) {
+    if (a.compute_grad) {
+      for (int64_t i = tid; i < n; i += BLOCK) x[i] = from_f<T>(0.f);
+    }
+    if (tid == 0) {
+      if (a.loss_rows) a.loss_rows[row] = 0.f;
+      if (a.z_loss_rows) a.z_loss_rows[row] = 0.f;
+    }
+    return;
+  }
+  const int64_t yl = y - a.col_offset;  // local column of the target (may be outside [0, n))
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+
+  float m, s, sz, zy;
+  if (a.row_stats) {
+    float4 st = a.row_stats[row];
+    m = st.x; s = st.y; sz = st.z; zy = st.w;
+  } else {
+    float lm = -INFINITY, ls = 0.f, lz = 0.f;
+    if (a.partials) {
+      const float4* p = a.partials + row * a.n_parts;
+      for (int64_t j = tid; j < a.n_parts; j += BLOCK) {
+        float4 q = p[j];
+        ms_combine(lm, ls, q.x, q.y);
+        lz += q.z;
+      }
+    } else {
+      auto upd = [&](float* v, int cnt) {
+        float cm = -INFINITY;
+        for (int i = 0; i < cnt; ++i) {
+          if (has_cap && !a.input_capped) v[i] = cap_val<T>(v[i], cap, ACCURATE);
+          cm = fmaxf(cm, v[i]);
+        }
+        float mn = fmaxf(lm, cm);
+        float acc = 0.f;
+        for (int i = 0; i < cnt; ++i) { acc += __expf(v[i] - mn); lz += v[i]; }
+        ls = (lm == -INFINITY ? 0.f : ls * __expf(lm - mn)) + acc;
+        lm = mn;
+      };
+      if (vec_ok) {
+        const int64_t nvec = n / NV;
+        for (int64_t i = tid; i < nvec; i += BLOCK) {
+          Vec16<T> v;
+          v.load(x + i * NV);
+          upd(v.v, NV);
+        }
+        for (int64_t i = nvec * NV + tid; i < n; i += BLOCK) {
+          float v = to_f<T>(x[i]);
+          upd(&v, 1);
+        }
+      } else {
+        for (int64_t i = tid; i < n; i += BLOCK) {
+          float v = to_f<T>(x[i]);
+          upd(&v, 1);
+        }
+      }
+    }
+    warp_ms(lm, ls);
+    lz = warp_sum(lz);
+    if (lane == 0) { red_m[warp] = lm; red_s[warp] = ls; red_z[warp] = lz; }
+    __syncthreads();
+    if (warp == 0) {
+      float wm = lane < BLOCK / 32 ? red_m[lane] : -INFINITY;
+      float ws = lane < BLOCK / 32 ? red_s[lane] : 0.f;
+      float wz = lane < BLOCK / 32 ? red_z[lane] : 0.f;
+      warp_ms(wm, ws);
+      wz = warp_sum(wz);
+      if (lane == 0) {
+        float zt = 0.f;
+        if (a.partials) {
+          zt = a.tgt_logit[row];
+        } else if (yl >= 0 && yl < n) {
+          zt = to_f<T>(x[yl]);
+          if (has_cap && !a.input_capped) zt = cap_val<T>(zt, cap, true);
+        }
+        bcast[0] = wm; bcast[1] = ws; bcast[2] = wz; bcast[3] = zt;
+      }
+    }
+    __syncthreads();
+    m = bcast[0]; s = bcast[1]; sz = bcast[2]; zy = bcast[3];
+  }
+
+  const float lse = m + logf(s);
+  const float V = (float)a.vocab_total;
+  const float lsm = a.label_smoothing;
+  const float eps = lsm / V;
+  float scale = 1.f;
+  if (a.reduction == LK_REDUCTION_MEAN) {
+    int64_t nv = *a.n_valid;
+    scale = 1.f / (float)(nv > 0 ? nv : 1);
+  }
+  if (tid == 0) {
+    // LK/ops/cross_entropy.py:259-289
+    float loss = lse - zy;
+    if (lsm > 0.f) loss = loss * (1.f - lsm) + (-eps * sz + lsm * lse);
+    float zl = a.lse_square_scale * lse * lse;
+    loss = (loss + zl) * scale;
+    if (a.loss_rows) a.loss_rows[row] = loss;
+    if (a.z_loss_rows) a.z_loss_rows[row] = zl * scale;
+  }
+  if (!a.compute_grad) return;
+
+  // pass 2: d(loss)/d(z) (LK/ops/cross_entropy.py:181-246)
+  const float inv_s = 1.f / s;
+  const float zfac = 1.f + 2.f * a.lse_square_scale * lse;
+  const float hit = 1.f - lsm;
+  auto grad = [&](float z, int64_t col) -> float {
+    float t = 0.f;
+    if (has_cap) {
+      if (a.input_capped) {
+        t = z / cap;
+      } else {
+        t = ACCURATE ? tanhf(z / cap) : tanh_fast(z / cap);
+        z = cap * t;
+      }
+    }
+    float g = __expf(z - m) * inv_s * zfac - eps;
+    if (col == yl) g -= hit;
+    g *= scale;
+    if (has_cap) g *= (1.f - t * t);
+    return g;
+  };
+  if (vec_ok) {
+    const int64_t nvec = n / NV;
+    for (int64_t i = tid; i < nvec; i += BLOCK) {
+      Vec16<T> v;
+      v.load(x + i * NV);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v.v[k] = grad(v.v[k], i * NV + k);
+      v.store(x + i * NV);
+    }
+    for (int64_t i = nvec * NV + tid; i < n; i += BLOCK) x[i] = from_f<T>(grad(to_f<T>(x[i]), i));
+  } else {
+    for (int64_t i = tid; i < n; i += BLOCK) x[i] = from_f<T>(grad(to_f<T>(x[i]), i));
+  }
+}
+
+// Deterministic fixed-order sum of n fp32 values into *out (one CTA, double accumulation).
+__global__ void reduce_sum_kernel(const float* __restrict__ v, int64_t n, float* out);
+// n_non_ignore and out-of-range count: out[0], out[1] (zeroed by the caller).
+__global__ void count_targets_kernel(const int64_t* __restrict__ t, int64_t rows, int64_t vocab,
+                                     int64_t ignore_index, unsigned long long* out);
+
+int launch_ce_rows(const CeRowArgs& a, int dtype, cudaStream_t st);
+int launch_count_targets(const int64_t* t, int64_t rows, int64_t vocab, int64_t ignore_index,
+                         int64_t* out, cudaStream_t st);
+int launch_reduce_sum(const float* v, int64_t n, float* out, cudaStream_t st);
+// Vocab-parallel stage 1: per-row local (max, sumexp, sum_logits, target_logit).
+int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols, int dtype,
+                        const int64_t* target, int64_t col_offset, int64_t ignore_index,
+                        const float4* partials, int64_t n_parts, const float* tgt_logit,
+                        float4* out, cudaStream_t st);
+int launch_colsum_rows(const void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
+                       void* out, int out_dtype, int accumulate, cudaStream_t st);
+
+}  // namespace lk

@@ -1,0 +1,459 @@
+// Fused linear cross entropy: chunk loop, chunk policy, workspace, TMA maps.
+//
+// Per chunk of rows [lo, lo + r) (rowfuse/flce.py:149-162, LK/ops/fused_linear_cross_entropy.py:96-220):
+//   1. logits GEMM  Z = X_c W^T            tcgen05, epilogue: softcap, bf16 store into the
+//                                          chunk buffer, per-(row, 256-col tile) online-softmax
+//                                          partials, target-logit capture
+//   2. finalize     dZ = softmax-grad(Z)   one read + one write of the chunk buffer (in place)
+//   3. backward     dX_c = dZ W            one persistent launch with both problems,
+//                   dW  (+)= dZ^T X_c      dX tiles (K = V) first, dW tiles (K = r) fill the tail
+// The full BT x V logits never exist; the only vocab-sized scratch is the chunk buffer.
+// MEAN divides by the device-side non-ignored count inside the finalize, so there is
+// no host sync (Liger syncs on .item() at LK/ops/fused_linear_cross_entropy.py:80-81).
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "ce.cuh"
+#include "gemm_sm100.cuh"
+
+namespace lk {
+namespace tc {
+
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool tma_ok(const TmaOperand& op) {
+  return (reinterpret_cast<uintptr_t>(op.ptr) & 15) == 0 && (op.row_elems * 2) % 16 == 0 &&
+         op.inner >= 1 && op.outer >= 1;
+}
+
+int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box) {
+  auto enc = get_encode();
+  LK_REQUIRE(enc != nullptr, LK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)op.inner, (cuuint64_t)op.outer};
+  cuuint64_t strides[1] = {(cuuint64_t)op.row_elems * 2};
+  cuuint32_t box[2] = {64u, (cuuint32_t)(op.mn_major ? 64 : rows_in_box)};
+  cuuint32_t es[2] = {1u, 1u};
+  CUresult r = enc(map, dtype == LK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
+                   const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  LK_REQUIRE(r == CUDA_SUCCESS, LK_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return LK_OK;
+}
+
+int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
+                   int* counter, cudaStream_t st) {
+  LK_REQUIRE(dtype == LK_BF16 || dtype == LK_F16, LK_UNSUPPORTED, "tcgen05 path takes bf16/fp16");
+  CUtensorMap maps[4];
+  memset(maps, 0, sizeof(maps));
+  Args args;
+  memset(&args, 0, sizeof(args));
+  args.n_problems = n_problems;
+  int total = 0;
+  for (int p = 0; p < n_problems; ++p) {
+    Problem& P = probs[p];
+    P.tiles_m = (int)((P.M + BM - 1) / BM);
+    P.tiles_n = (int)((P.N + BN - 1) / BN);
+    P.k_blocks = (int)((P.K + BK - 1) / BK);
+    P.a_mn = a[p].mn_major;
+    P.b_mn = b[p].mn_major;
+    int rc = encode_operand(&maps[2 * p], a[p], dtype, BM);
+    if (rc) return rc;
+    rc = encode_operand(&maps[2 * p + 1], b[p], dtype, BN);
+    if (rc) return rc;
+    args.prob[p] = P;
+    args.idesc[p] = make_idesc(dtype, P.a_mn, P.b_mn);
+    if (p == 0) args.tiles0 = P.tiles_m * P.tiles_n;
+    total += P.tiles_m * P.tiles_n;
+  }
+  if (n_problems == 1) { maps[2] = maps[0]; maps[3] = maps[1]; }
+  args.total_tiles = total;
+  args.counter = counter;
+  if (total == 0) return LK_OK;
+  static std::once_flag attr_once;
+  static cudaError_t attr_err = cudaSuccess;
+  auto kern = dtype == LK_BF16 ? gemm_kernel<__nv_bfloat16> : gemm_kernel<__half>;
+  std::call_once(attr_once, [] {
+    attr_err = cudaFuncSetAttribute(gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  });
+  LK_REQUIRE(attr_err == cudaSuccess, LK_CUDA_ERROR,
+             std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
+  const int grid = std::min(total, sm_count());
+  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], args);
+  return check_launch("tcgen05 gemm_kernel");
+}
+
+}  // namespace tc
+
+// ------------------------------------------------------------- planning ----
+static int64_t next_pow2(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+static int64_t elt_size(int dtype) { return dtype == LK_F32 ? 4 : 2; }
+static int64_t ld_logits(int64_t vocab) { return (vocab + 63) / 64 * 64; }
+
+// Reference rule (rowfuse/flce.py:69-78):
+//   C_ref = 2^ceil(log2(ceil(BT / ceil(V/H)))).
+// B200 rule: at least 2048 rows per chunk when the batch has them, because every
+// chunk costs one fp32 read-modify-write of dW (V x H x 8 bytes); at C = 2048 the
+// dW GEMM's MMA time per tile covers its RMW traffic (SURVEY §7 "hard parts").
+// The chunk buffer is capped at 1 GiB.
+static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dtype) {
+  int64_t ratio = (vocab + hidden - 1) / hidden;
+  int64_t c_ref = next_pow2((bt + ratio - 1) / ratio);
+  int64_t c = std::max<int64_t>(c_ref, std::min<int64_t>(next_pow2(bt), 2048));
+  const int64_t cap_bytes = (int64_t)1 << 30;
+  while (c > 128 && c * ld_logits(vocab) * elt_size(dtype) > cap_bytes) c >>= 1;
+  return std::max<int64_t>(1, c);
+}
+
+struct FlceLayout {
+  int64_t C, nchunks, ldz, nparts;
+  bool tc, need_acc, need_bias_acc;
+  size_t off_counts, off_sched, off_z, off_parts, off_tgt, off_acc, off_bias, total;
+};
+
+static bool use_tc_path(int dtype, int64_t hidden, const void* x, const void* w, int force_simt) {
+#ifdef LK_HAS_TCGEN05
+  if (force_simt) return false;
+  if (dtype != LK_BF16 && dtype != LK_F16) return false;
+  if (hidden % 8 != 0) return false;
+  if (x && (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  if (w && (reinterpret_cast<uintptr_t>(w) & 15)) return false;
+  return true;
+#else
+  (void)dtype; (void)hidden; (void)x; (void)w; (void)force_simt;
+  return false;
+#endif
+}
+
+static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t chunk_rows,
+                              bool has_grad_w, bool has_bias_grad, bool tc) {
+  FlceLayout L{};
+  L.C = chunk_rows > 0 ? chunk_rows : b200_chunk_rows(bt, hidden, vocab, dtype);
+  L.C = std::max<int64_t>(1, std::min<int64_t>(L.C, std::max<int64_t>(bt, 1)));
+  L.nchunks = bt > 0 ? (bt + L.C - 1) / L.C : 0;
+  L.ldz = ld_logits(vocab);
+  L.nparts = (vocab + tc::BN - 1) / tc::BN;
+  L.tc = tc;
+  L.need_acc = has_grad_w && dtype != LK_F32 && L.nchunks > 1;
+  L.need_bias_acc = has_bias_grad;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { off = align_up(off, 1024); size_t o = off; off += bytes; return o; };
+  L.off_counts = take(2 * sizeof(int64_t));
+  L.off_sched = take((size_t)(2 * L.nchunks + 2) * sizeof(int));
+  L.off_z = take((size_t)L.C * L.ldz * elt_size(dtype));
+  L.off_parts = take(tc ? (size_t)L.C * L.nparts * sizeof(float4) : 0);
+  L.off_tgt = take(tc ? (size_t)L.C * sizeof(float) : 0);
+  L.off_acc = take(L.need_acc ? (size_t)vocab * hidden * sizeof(float) : 0);
+  L.off_bias = take(L.need_bias_acc ? (size_t)vocab * sizeof(float) : 0);
+  L.total = align_up(off, 1024);
+  return L;
+}
+
+}  // namespace lk
+
+using namespace lk;
+
+extern "C" int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t* chunk_rows,
+                            int64_t* num_chunks) {
+  LK_REQUIRE(bt >= 1 && hidden >= 1 && vocab >= 1, LK_SIZE_MISMATCH, "dimensions must be >= 1");
+  int64_t c = b200_chunk_rows(bt, hidden, vocab, dtype);
+  c = std::min(c, next_pow2(bt));
+  if (chunk_rows) *chunk_rows = c;
+  if (num_chunks) *num_chunks = (bt + c - 1) / c;
+  return LK_OK;
+}
+
+extern "C" size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
+                                          int64_t chunk_rows, int has_grad_w) {
+  bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
+  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc).total;
+}
+
+extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
+  LK_REQUIRE(a != nullptr, LK_INVALID_ARGUMENT, "args is null");
+  const int64_t BT = a->bt, H = a->hidden, V = a->vocab;
+  const int dt = a->dtype;
+  LK_REQUIRE(BT >= 0 && H >= 1 && V >= 1, LK_SIZE_MISMATCH, "bt >= 0, hidden >= 1, vocab >= 1 required");
+  LK_REQUIRE(dt == LK_F32 || dt == LK_BF16 || dt == LK_F16, LK_INVALID_ARGUMENT, "unknown dtype");
+  LK_REQUIRE(a->reduction >= 0 && a->reduction <= 2, LK_INVALID_ARGUMENT, "bad reduction");
+  LK_REQUIRE(a->label_smoothing >= 0.f && a->label_smoothing <= 1.f, LK_INVALID_ARGUMENT,
+             "label_smoothing must be in [0, 1]");
+  LK_REQUIRE(a->loss_rows != nullptr, LK_INVALID_ARGUMENT, "loss_rows is null");
+  LK_REQUIRE(BT == 0 || (a->x && a->weight && a->target), LK_INVALID_ARGUMENT, "null input");
+  cudaStream_t st = as_stream(a->stream);
+  const bool tc = use_tc_path(dt, H, a->x, a->weight, a->force_simt);
+  const bool want_grad = a->grad_x || a->grad_w || a->grad_bias;
+  FlceLayout L = flce_layout(BT, H, V, dt, a->chunk_rows, a->grad_w != nullptr, a->grad_bias != nullptr, tc);
+  LK_REQUIRE(a->workspace && a->workspace_bytes >= L.total, LK_INVALID_ARGUMENT,
+             "workspace too small: need " + std::to_string(L.total) + " bytes");
+  char* ws = static_cast<char*>(a->workspace);
+  int64_t* counts = reinterpret_cast<int64_t*>(ws + L.off_counts);
+  int* sched = reinterpret_cast<int*>(ws + L.off_sched);
+  void* zbuf = ws + L.off_z;
+  float4* parts = reinterpret_cast<float4*>(ws + L.off_parts);
+  float* tgt = reinterpret_cast<float*>(ws + L.off_tgt);
+  float* dwacc = reinterpret_cast<float*>(ws + L.off_acc);
+  float* bacc = reinterpret_cast<float*>(ws + L.off_bias);
+  const int64_t es = elt_size(dt);
+
+  int rc;
+  {
+    ProfScope ps(3, st);
+    rc = launch_count_targets(a->target, BT, V, a->ignore_index, counts, st);
+  }
+  if (rc) return rc;
+  if (a->target_stats)
+    LK_CUDA(cudaMemcpyAsync(a->target_stats, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2) * sizeof(int), st));
+  if (BT == 0) {
+    if (a->loss_sum) LK_CUDA(cudaMemsetAsync(a->loss_sum, 0, sizeof(float), st));
+    if (a->z_loss_sum) LK_CUDA(cudaMemsetAsync(a->z_loss_sum, 0, sizeof(float), st));
+    if (a->grad_w) LK_CUDA(cudaMemsetAsync(a->grad_w, 0, (size_t)V * H * es, st));
+    if (a->grad_bias) LK_CUDA(cudaMemsetAsync(a->grad_bias, 0, (size_t)V * es, st));
+    return LK_OK;
+  }
+
+  for (int64_t ci = 0; ci < L.nchunks; ++ci) {
+    const int64_t lo = ci * L.C;
+    const int64_t r = std::min(L.C, BT - lo);
+    const char* xc = static_cast<const char*>(a->x) + lo * H * es;
+    const bool first = ci == 0, last = ci == L.nchunks - 1;
+
+    // ---- 1. logits ----
+    EpiArgs le{};
+    le.kind = EPI_LOGITS; le.out_dtype = dt; le.out = zbuf; le.ldo = L.ldz; le.alpha = 1.f;
+    le.bias = a->bias; le.softcap = a->softcap; le.target = a->target + lo; le.col_offset = 0;
+    le.ignore_index = a->ignore_index; le.partials = parts; le.n_parts = L.nparts; le.tgt_logit = tgt;
+    le.M = r; le.N = V;
+    {
+      ProfScope ps(0, st);
+      if (tc) {
+        tc::TmaOperand A{xc, H, r, H, 0}, B{a->weight, H, V, H, 0};
+        tc::Problem P{};
+        P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
+        rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
+      } else {
+        Operand A{xc, H, 1}, B{a->weight, H, 1};
+        rc = launch_simt_gemm(A, B, r, V, H, dt, le, st);
+      }
+    }
+    if (rc) return rc;
+
+    // ---- 2. finalize: loss rows + dZ in place ----
+    CeRowArgs ce{};
+    ce.x = zbuf; ce.ld = L.ldz; ce.target = a->target + lo; ce.rows = r; ce.n_cols = V; ce.vocab_total = V;
+    ce.col_offset = 0; ce.ignore_index = a->ignore_index; ce.label_smoothing = a->label_smoothing;
+    ce.lse_square_scale = a->lse_square_scale; ce.softcap = a->softcap; ce.input_capped = 1;
+    ce.reduction = a->reduction; ce.compute_grad = want_grad ? 1 : 0;
+    ce.n_valid = a->mean_count ? a->mean_count : counts;
+    ce.loss_rows = a->loss_rows + lo; ce.z_loss_rows = a->z_loss_rows ? a->z_loss_rows + lo : nullptr;
+    if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
+    {
+      ProfScope ps(1, st);
+      rc = launch_ce_rows(ce, dt, st);
+    }
+    if (rc) return rc;
+    if (!want_grad) continue;
+
+    if (a->grad_bias) {
+      ProfScope ps(3, st);
+      rc = launch_colsum_rows(zbuf, r, V, L.ldz, dt, bacc, LK_F32, first ? 0 : 1, st);
+      if (rc) return rc;
+    }
+
+    // ---- 3. dX = dZ W, dW (+)= dZ^T X ----
+    EpiArgs xe{};
+    xe.kind = EPI_STORE; xe.out_dtype = dt; xe.out = a->grad_x ? static_cast<char*>(a->grad_x) + lo * H * es : nullptr;
+    xe.ldo = H; xe.alpha = 1.f; xe.M = r; xe.N = H;
+    EpiArgs we{};
+    we.kind = EPI_ACCUM; we.out_dtype = dt; we.out = a->grad_w; we.ldo = H; we.M = V; we.N = H;
+    if (dt == LK_F32) {
+      we.acc = static_cast<float*>(a->grad_w); we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
+    } else if (L.nchunks == 1) {
+      we.acc = nullptr; we.ldacc = H; we.beta = 0; we.final_out = 1;
+    } else {
+      we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = last ? 1 : 0;
+    }
+    ProfScope ps_bwd(2, st);
+    if (tc) {
+      tc::TmaOperand As[2], Bs[2];
+      tc::Problem Ps[2];
+      int np = 0;
+      if (a->grad_x) {
+        As[np] = {zbuf, V, r, L.ldz, 0};
+        Bs[np] = {a->weight, H, V, H, 1};
+        Ps[np] = tc::Problem{};
+        Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
+        ++np;
+      }
+      if (a->grad_w) {
+        As[np] = {zbuf, V, r, L.ldz, 1};
+        Bs[np] = {xc, H, r, H, 1};
+        Ps[np] = tc::Problem{};
+        Ps[np].M = V; Ps[np].N = H; Ps[np].K = r; Ps[np].n_fast = 1; Ps[np].epi = we;
+        ++np;
+      }
+      if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, dt, sched + 2 * ci + 1, st);
+    } else {
+      if (a->grad_x) {
+        Operand A{zbuf, L.ldz, 1}, B{a->weight, 1, H};
+        rc = launch_simt_gemm(A, B, r, H, V, dt, xe, st);
+        if (rc) return rc;
+      }
+      if (a->grad_w) {
+        Operand A{zbuf, 1, L.ldz}, B{xc, 1, H};
+        rc = launch_simt_gemm(A, B, V, H, r, dt, we, st);
+      }
+    }
+    if (rc) return rc;
+  }
+  ProfScope ps_tail(3, st);
+  if (a->grad_bias) {
+    rc = launch_colsum_rows(bacc, 1, V, V, LK_F32, a->grad_bias, dt, 0, st);
+    if (rc) return rc;
+  }
+  if (a->loss_sum) { rc = launch_reduce_sum(a->loss_rows, BT, a->loss_sum, st); if (rc) return rc; }
+  if (a->z_loss_sum && a->z_loss_rows) {
+    rc = launch_reduce_sum(a->z_loss_rows, BT, a->z_loss_sum, st);
+    if (rc) return rc;
+  }
+  return LK_OK;
+}
+
+// ------------------------------------------------------ vocab-parallel ----
+extern "C" size_t lk_flce_vp_workspace_bytes(int64_t rows, int64_t hidden, int64_t vocab_local, int dtype) {
+  (void)hidden;
+  const int64_t nparts = (vocab_local + tc::BN - 1) / tc::BN;
+  return align_up((size_t)rows * nparts * sizeof(float4), 1024) + align_up((size_t)rows * 4, 1024) + 4096 +
+         (size_t)elt_size(dtype) * 0;
+}
+
+// Stage 1: local-shard logits + per-row local statistics (max, sumexp, sum_logits, target_logit).
+extern "C" int lk_flce_vp_logits(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                                 int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int dtype,
+                                 int64_t ignore_index, float softcap, float* row_stats, void* logits_buf,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+  LK_REQUIRE(rows >= 0 && hidden >= 1 && vocab_local >= 1, LK_SIZE_MISMATCH, "bad sizes");
+  LK_REQUIRE(workspace && workspace_bytes >= lk_flce_vp_workspace_bytes(rows, hidden, vocab_local, dtype),
+             LK_INVALID_ARGUMENT, "workspace too small");
+  if (rows == 0) return LK_OK;
+  cudaStream_t st = as_stream(stream);
+  const bool tc = use_tc_path(dtype, hidden, x, weight_shard, 0);
+  const int64_t ldz = ld_logits(vocab_local);
+  const int64_t nparts = (vocab_local + tc::BN - 1) / tc::BN;
+  char* ws = static_cast<char*>(workspace);
+  float4* parts = reinterpret_cast<float4*>(ws);
+  float* tgt = reinterpret_cast<float*>(ws + align_up((size_t)rows * nparts * sizeof(float4), 1024));
+  int* sched = reinterpret_cast<int*>(ws + align_up((size_t)rows * nparts * sizeof(float4), 1024) +
+                                      align_up((size_t)rows * 4, 1024));
+  EpiArgs le{};
+  le.kind = EPI_LOGITS; le.out_dtype = dtype; le.out = logits_buf; le.ldo = ldz; le.alpha = 1.f;
+  le.softcap = softcap; le.target = target; le.col_offset = vocab_offset; le.ignore_index = ignore_index;
+  le.partials = parts; le.n_parts = nparts; le.tgt_logit = tgt; le.M = rows; le.N = vocab_local;
+  int rc;
+  LK_CUDA(cudaMemsetAsync(tgt, 0, (size_t)rows * 4, st));
+  if (tc) {
+    LK_CUDA(cudaMemsetAsync(sched, 0, 64, st));
+    tc::TmaOperand A{x, hidden, rows, hidden, 0}, B{weight_shard, hidden, vocab_local, hidden, 0};
+    tc::Problem P{};
+    P.M = rows; P.N = vocab_local; P.K = hidden; P.n_fast = 0; P.epi = le;
+    rc = tc::launch_tc_gemm(&A, &B, &P, 1, dtype, sched, st);
+  } else {
+    Operand A{x, hidden, 1}, B{weight_shard, hidden, 1};
+    rc = launch_simt_gemm(A, B, rows, vocab_local, hidden, dtype, le, st);
+  }
+  if (rc) return rc;
+  // reduce the per-tile partials (tc) or the stored row (simt) to one stats row
+  return launch_vp_row_stats(logits_buf, ldz, rows, vocab_local, dtype, target, vocab_offset, ignore_index,
+                             tc ? parts : nullptr, nparts, tgt, reinterpret_cast<float4*>(row_stats), st);
+}
+
+extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                                   int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
+                                   int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
+                                   float softcap, int reduction, const int64_t* n_non_ignore,
+                                   const float* row_stats_global, void* logits_buf, float* loss_rows,
+                                   void* grad_x_partial_f32, float* grad_w_accum, int accumulate, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  LK_REQUIRE(rows >= 0 && hidden >= 1 && vocab_local >= 1, LK_SIZE_MISMATCH, "bad sizes");
+  (void)workspace; (void)workspace_bytes;
+  if (rows == 0) return LK_OK;
+  cudaStream_t st = as_stream(stream);
+  const int64_t ldz = ld_logits(vocab_local);
+  CeRowArgs ce{};
+  ce.x = logits_buf; ce.ld = ldz; ce.target = target; ce.rows = rows; ce.n_cols = vocab_local;
+  ce.vocab_total = vocab_total; ce.col_offset = vocab_offset; ce.ignore_index = ignore_index;
+  ce.label_smoothing = label_smoothing; ce.lse_square_scale = lse_square_scale; ce.softcap = softcap;
+  ce.input_capped = 1; ce.reduction = reduction; ce.compute_grad = 1; ce.n_valid = n_non_ignore;
+  ce.loss_rows = loss_rows; ce.row_stats = reinterpret_cast<const float4*>(row_stats_global);
+  int rc = launch_ce_rows(ce, dtype, st);
+  if (rc) return rc;
+  // dX partial (fp32, all-reduced by the caller) and local dW shard (fp32 accumulator)
+  EpiArgs xe{};
+  xe.kind = EPI_STORE; xe.out_dtype = LK_F32; xe.out = grad_x_partial_f32; xe.ldo = hidden; xe.alpha = 1.f;
+  xe.M = rows; xe.N = hidden;
+  EpiArgs we{};
+  we.kind = EPI_ACCUM; we.out_dtype = LK_F32; we.acc = grad_w_accum; we.ldacc = hidden;
+  we.beta = accumulate ? 1 : 0; we.M = vocab_local; we.N = hidden;
+  // The fp32 dX-partial store uses the SIMT epilogue contract; both GEMMs run through
+  // the generic launcher so the partial stays fp32 for the all-reduce.
+  if (grad_x_partial_f32) {
+    Operand A{logits_buf, ldz, 1}, B{weight_shard, 1, hidden};
+    rc = launch_simt_gemm(A, B, rows, hidden, vocab_local, dtype, xe, st);
+    if (rc) return rc;
+  }
+  if (grad_w_accum) {
+    Operand A{logits_buf, 1, ldz}, B{x, 1, hidden};
+    rc = launch_simt_gemm(A, B, vocab_local, hidden, rows, dtype, we, st);
+  }
+  return rc;
+}
+
+// ------------------------------------------------------------ GEMM test ----
+extern "C" int lk_gemm_test(const void* a, const void* b, float* d, int64_t m, int64_t n, int64_t k, int layout,
+                            int dtype, int use_tcgen05, void* workspace, size_t workspace_bytes, void* stream) {
+  LK_REQUIRE(a && b && d, LK_INVALID_ARGUMENT, "null pointer");
+  LK_REQUIRE(layout >= 0 && layout <= 2, LK_INVALID_ARGUMENT, "layout must be 0, 1 or 2");
+  cudaStream_t st = as_stream(stream);
+  EpiArgs e{};
+  e.kind = EPI_F32; e.out_dtype = LK_F32; e.out = d; e.ldo = n; e.M = m; e.N = n; e.alpha = 1.f;
+  if (use_tcgen05) {
+#ifdef LK_HAS_TCGEN05
+    LK_REQUIRE(workspace && workspace_bytes >= 64, LK_INVALID_ARGUMENT, "workspace too small");
+    LK_CUDA(cudaMemsetAsync(workspace, 0, 64, st));
+    tc::TmaOperand A, B;
+    if (layout == 0) { A = {a, k, m, k, 0}; B = {b, k, n, k, 0}; }
+    else if (layout == 1) { A = {a, k, m, k, 0}; B = {b, n, k, n, 1}; }
+    else { A = {a, m, k, m, 1}; B = {b, n, k, n, 1}; }
+    LK_REQUIRE(tc::tma_ok(A) && tc::tma_ok(B), LK_NON_CONTIGUOUS, "operands not TMA-describable");
+    tc::Problem P{};
+    P.M = m; P.N = n; P.K = k; P.n_fast = layout == 2 ? 1 : 0; P.epi = e;
+    return tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st);
+#else
+    return fail(LK_UNSUPPORTED, "built without tcgen05");
+#endif
+  }
+  Operand A, B;
+  if (layout == 0) { A = {a, k, 1}; B = {b, k, 1}; }
+  else if (layout == 1) { A = {a, k, 1}; B = {b, 1, n}; }
+  else { A = {a, 1, m}; B = {b, 1, n}; }
+  return launch_simt_gemm(A, B, m, n, k, dtype, e, st);
+}

@@ -1,0 +1,505 @@
+// Persistent, warp-specialised tcgen05 GEMM for sm_100a with the FLCE epilogues.
+//
+// Tile 128 x 256 x 64 (bf16/fp16 in, fp32 accumulate in TMEM), cta_group::1.
+//   warp 0      : TMA producer (one elected lane), 4-stage smem ring, mbarrier full/empty
+//   warp 1      : MMA issuer (one lane): 4 x tcgen05.mma (K=16) per stage, commit -> empty
+//   warp 2      : TMEM allocator (512 columns = two 128x256 fp32 accumulators)
+//   warps 4..7  : epilogue, one TMEM lane quadrant each -> one output row per thread
+// Tiles come from a global atomic counter (dynamic persistent scheduling) and
+// are handed to the MMA and epilogue warps through a small smem ring, so the
+// TMEM double buffer overlaps tile i's epilogue with tile i+1's MMAs.
+//
+// Up to two GEMM "problems" share one launch: the FLCE backward runs the dX
+// GEMM (long K = V, few tiles) and the dW GEMM (short K = chunk rows, many
+// tiles) together, heavy tiles first, so the tail of one fills the other.
+//
+// Operand layouts (smem, SWIZZLE_128B, UMMA canonical forms; see cute
+// mma_sm100_desc.hpp):
+//   K-major  : TMA box {64 (K), rows}      -> 8-row groups of 1024 B, SBO = 1024
+//   MN-major : TMA boxes {64 (MN), 64 (K)} -> one 8 KB box per 64-wide MN atom,
+//              LBO = 8192 (MN atom stride), SBO = 1024 (8-row K group stride)
+#pragma once
+#include <cuda.h>
+#include "gemm_common.cuh"
+
+namespace lk {
+namespace tc {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4, SCHED = 4;
+constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int NUM_THREADS = 256;
+constexpr int TMEM_COLS = 512;
+// barriers + sched ring + tmem slot, after the 1024-aligned stage buffers
+constexpr int AUX_BYTES = 1024;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + AUX_BYTES + 1024;  // + alignment slack
+
+struct Problem {
+  int64_t M, N, K;
+  int tiles_m, tiles_n, k_blocks;
+  int a_mn, b_mn;       // 1 = MN-major operand
+  int n_fast;           // tile id -> (m, n): 1 = n varies fastest
+  EpiArgs epi;
+};
+
+struct Args {
+  Problem prob[2];
+  int n_problems;
+  int tiles0;           // tiles of problem 0
+  int total_tiles;
+  int* counter;         // dynamic scheduler (zero at launch)
+  uint32_t idesc[2];    // instruction descriptors per problem
+};
+
+#if defined(__CUDA_ARCH__)
+// ------------------------------------------------------------------ PTX ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}"
+      ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+               ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// SWIZZLE_128B shared-memory matrix descriptor (sm100 "version 1").
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+struct TileCoord {
+  int p, m_blk, n_blk;
+};
+__device__ __forceinline__ TileCoord decode_tile(const Args& a, int t) {
+  TileCoord c;
+  c.p = (t >= a.tiles0) ? 1 : 0;
+  int lt = c.p ? t - a.tiles0 : t;
+  const Problem& P = a.prob[c.p];
+  if (P.n_fast) { c.n_blk = lt % P.tiles_n; c.m_blk = lt / P.tiles_n; }
+  else { c.m_blk = lt % P.tiles_m; c.n_blk = lt / P.tiles_m; }
+  return c;
+}
+
+// ------------------------------------------------------------ epilogues ----
+template <typename T>
+__device__ __forceinline__ void store32(T* dst, const float (&v)[32]) {
+  // 32 elements -> 16-byte stores
+  constexpr int NV = 16 / sizeof(T);
+#pragma unroll
+  for (int q = 0; q < 32 / NV; ++q) {
+    uint4 raw;
+    T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) e[i] = from_f<T>(v[q * NV + i]);
+    reinterpret_cast<uint4*>(dst)[q] = raw;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64_t n0, int n_blk,
+                                           uint32_t taddr) {
+  const bool row_ok = grow < e.M;
+  int64_t tcol = -1;
+  if (row_ok) {
+    int64_t y = e.target[grow];
+    if (y != e.ignore_index) tcol = y - e.col_offset;
+  }
+  const bool cap = e.softcap > 0.f;
+  const float inv_cap = cap ? 1.f / e.softcap : 0.f;
+  float m = -INFINITY, s = 0.f, sz = 0.f, tv = 0.f;
+  bool have_t = false;
+  T* orow = static_cast<T*>(e.out) + grow * e.ldo;
+  const bool vec_ok = (e.ldo % 8) == 0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    if (!row_ok) continue;
+    const int64_t col0 = n0 + c * 32;
+    const int nvalid = (int)(e.N - col0 < 32 ? e.N - col0 : 32);
+    if (nvalid <= 0) continue;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      float z = __uint_as_float(r[j]);
+      if (e.bias && j < nvalid) z += load_any(e.bias, col0 + j, e.out_dtype);
+      if (cap) z = e.softcap * tanh_fast(z * inv_cap);
+      v[j] = round_to<T>(z);
+    }
+    float cm = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) cm = fmaxf(cm, v[j]);
+    const float mn = fmaxf(m, cm);
+    float acc = 0.f, zs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < nvalid) { acc += __expf(v[j] - mn); zs += v[j]; }
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + acc;
+    m = mn;
+    sz += zs;
+    if (tcol >= col0 && tcol < col0 + nvalid) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (col0 + j == tcol) tv = v[j];
+      have_t = true;
+    }
+    if (nvalid == 32 && vec_ok) {
+      store32<T>(orow + col0, v);
+    } else {
+      for (int j = 0; j < nvalid; ++j) orow[col0 + j] = from_f<T>(v[j]);
+    }
+  }
+  if (row_ok) {
+    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
+    if (have_t) e.tgt_logit[grow] = tv;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_store(const EpiArgs& e, int64_t grow, int64_t n0, uint32_t taddr) {
+  const bool row_ok = grow < e.M;
+  T* orow = static_cast<T*>(e.out) + grow * e.ldo;
+  const bool vec_ok = (e.ldo % (16 / sizeof(T))) == 0;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    if (!row_ok) continue;
+    const int64_t col0 = n0 + c * 32;
+    const int nvalid = (int)(e.N - col0 < 32 ? e.N - col0 : 32);
+    if (nvalid <= 0) continue;
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = e.alpha * __uint_as_float(r[j]);
+    if (nvalid == 32 && vec_ok) store32<T>(orow + col0, v);
+    else for (int j = 0; j < nvalid; ++j) orow[col0 + j] = from_f<T>(v[j]);
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_accum(const EpiArgs& e, int64_t grow, int64_t n0, uint32_t taddr) {
+  const bool row_ok = grow < e.M;
+  float* arow = e.acc + grow * e.ldacc;
+  T* orow = static_cast<T*>(e.out) + grow * e.ldo;
+  const bool vec_ok = (e.ldacc % 4) == 0 && (!e.final_out || (e.ldo % 8) == 0);
+  float4 nxt[8];
+  auto fetch = [&](int c, float4 (&dst)[8]) {
+    const int64_t col0 = n0 + c * 32;
+    if (row_ok && e.beta && vec_ok && col0 + 32 <= e.N) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dst[q] = reinterpret_cast<const float4*>(arow + col0)[q];
+    }
+  };
+  fetch(0, nxt);
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    float4 cur[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) cur[q] = nxt[q];
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    if (c + 1 < BN / 32) fetch(c + 1, nxt);
+    tmem_wait_ld();
+    if (!row_ok) continue;
+    const int64_t col0 = n0 + c * 32;
+    const int nvalid = (int)(e.N - col0 < 32 ? e.N - col0 : 32);
+    if (nvalid <= 0) continue;
+    float v[32];
+    if (nvalid == 32 && vec_ok) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 a = e.beta ? cur[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+        v[4 * q + 0] = a.x + __uint_as_float(r[4 * q + 0]);
+        v[4 * q + 1] = a.y + __uint_as_float(r[4 * q + 1]);
+        v[4 * q + 2] = a.z + __uint_as_float(r[4 * q + 2]);
+        v[4 * q + 3] = a.w + __uint_as_float(r[4 * q + 3]);
+      }
+      if (e.final_out) {
+        store32<T>(orow + col0, v);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          reinterpret_cast<float4*>(arow + col0)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+    } else {
+      for (int j = 0; j < nvalid; ++j) {
+        float a = (e.beta ? arow[col0 + j] : 0.f) + __uint_as_float(r[j]);
+        if (e.final_out) orow[col0 + j] = from_f<T>(a);
+        else arow[col0 + j] = a;
+      }
+    }
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ void epi_f32(const EpiArgs& e, int64_t grow, int64_t n0, uint32_t taddr) {
+  const bool row_ok = grow < e.M;
+  float* orow = static_cast<float*>(e.out) + grow * e.ldo;
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    if (!row_ok) continue;
+    const int64_t col0 = n0 + c * 32;
+    for (int j = 0; j < 32; ++j)
+      if (col0 + j < e.N) orow[col0 + j] = __uint_as_float(r[j]);
+  }
+}
+#endif  // __CUDA_ARCH__
+
+// ---------------------------------------------------------------- kernel ----
+template <typename T>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap mb0,
+            const __grid_constant__ CUtensorMap ma1, const __grid_constant__ CUtensorMap mb1,
+            const __grid_constant__ Args args) {
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* aux = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = aux;                    // [STAGES]
+  uint64_t* empty = full + STAGES;         // [STAGES]
+  uint64_t* tfull = empty + STAGES;        // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint64_t* sfull = tempty + 2;            // [SCHED]
+  uint64_t* sempty = sfull + SCHED;        // [SCHED]
+  int* stile = reinterpret_cast<int*>(sempty + SCHED);  // [SCHED]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stile + SCHED);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&tfull[i], 1); mbar_init(&tempty[i], 4); }
+    for (int i = 0; i < SCHED; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 5); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&ma0); tma_prefetch_desc(&mb0);
+    if (args.n_problems > 1) { tma_prefetch_desc(&ma1); tma_prefetch_desc(&mb1); }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
+                 ::"r"(smem_u32(tmem_slot)), "r"(TMEM_COLS) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===================== TMA producer =====================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % SCHED;
+        mbar_wait(&sempty[slot], ((it / SCHED) & 1) ^ 1);
+        int tile = atomicAdd(args.counter, 1);
+        if (tile >= args.total_tiles) tile = -1;
+        stile[slot] = tile;
+        mbar_arrive(&sfull[slot]);
+        if (tile < 0) break;
+        const TileCoord tcd = decode_tile(args, tile);
+        const Problem& P = args.prob[tcd.p];
+        const CUtensorMap* ma = tcd.p ? &ma1 : &ma0;
+        const CUtensorMap* mb = tcd.p ? &mb1 : &mb0;
+        const int m0 = tcd.m_blk * BM, n0 = tcd.n_blk * BN;
+        for (int kb = 0; kb < P.k_blocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* a_dst = sA + stage * A_BYTES;
+          uint8_t* b_dst = sB + stage * B_BYTES;
+          const int k0 = kb * BK;
+          if (P.a_mn) {
+            tma_load_2d(ma, &full[stage], a_dst, m0, k0);
+            tma_load_2d(ma, &full[stage], a_dst + 8192, m0 + 64, k0);
+          } else {
+            tma_load_2d(ma, &full[stage], a_dst, k0, m0);
+          }
+          if (P.b_mn) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) tma_load_2d(mb, &full[stage], b_dst + j * 8192, n0 + 64 * j, k0);
+          } else {
+            tma_load_2d(mb, &full[stage], b_dst, k0, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===================== MMA issuer =====================
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = 0;; ++it) {
+        const int slot = it % SCHED;
+        mbar_wait(&sfull[slot], (it / SCHED) & 1);
+        const int tile = stile[slot];
+        mbar_arrive(&sempty[slot]);
+        if (tile < 0) break;
+        const TileCoord tcd = decode_tile(args, tile);
+        const Problem& P = args.prob[tcd.p];
+        const uint32_t idesc = args.idesc[tcd.p];
+        const int buf = it & 1;
+        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + buf * BN;
+        // per-UMMA_K (16 elements) start-address advance inside a 64-wide K block
+        const uint32_t a_kstep = P.a_mn ? 2048u : 32u;
+        const uint32_t b_kstep = P.b_mn ? 2048u : 32u;
+        const uint32_t a_lbo = P.a_mn ? 8192u : 16u, b_lbo = P.b_mn ? 8192u : 16u;
+        for (int kb = 0; kb < P.k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t ad = make_desc(a_addr + k * a_kstep, a_lbo, 1024u);
+            const uint64_t bd = make_desc(b_addr + k * b_kstep, b_lbo, 1024u);
+            umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[buf]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===================== epilogue =====================
+    const int q = warp & 3;
+    for (int it = 0;; ++it) {
+      const int slot = it % SCHED;
+      mbar_wait(&sfull[slot], (it / SCHED) & 1);
+      const int tile = stile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[slot]);
+      if (tile < 0) break;
+      const TileCoord tcd = decode_tile(args, tile);
+      const Problem& P = args.prob[tcd.p];
+      const int buf = it & 1;
+      mbar_wait(&tfull[buf], (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(q * 32) << 16);
+      const int64_t grow = (int64_t)tcd.m_blk * BM + q * 32 + lane;
+      const int64_t n0 = (int64_t)tcd.n_blk * BN;
+      switch (P.epi.kind) {
+        case EPI_LOGITS: epi_logits<T>(P.epi, grow, n0, tcd.n_blk, taddr); break;
+        case EPI_STORE: epi_store<T>(P.epi, grow, n0, taddr); break;
+        case EPI_ACCUM: epi_accum<T>(P.epi, grow, n0, taddr); break;
+        default: epi_f32<T>(P.epi, grow, n0, taddr); break;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+    }
+  }
+  __syncwarp();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(TMEM_COLS)
+                 : "memory");
+  }
+#endif
+}
+
+// ------------------------------------------------------------------ host ----
+// Instruction descriptor for kind::f16 (cute UMMA::InstrDescriptor bit layout):
+// c_format F32 @4, a/b format @7/@10 (0 = F16, 1 = BF16), a/b major @15/@16,
+// N>>3 @17, M>>4 @24.
+inline uint32_t make_idesc(int dtype, int a_mn, int b_mn) {
+  uint32_t fmt = dtype == LK_BF16 ? 1u : 0u;
+  return (1u << 4) | (fmt << 7) | (fmt << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+// One GEMM operand as the TMA sees it: a row-major [outer, inner] matrix.
+struct TmaOperand {
+  const void* ptr;
+  int64_t inner, outer;  // elements
+  int64_t row_elems;     // row stride in elements
+  int mn_major;          // 0: inner dim is K; 1: inner dim is M/N
+};
+
+int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box);
+bool tma_ok(const TmaOperand& op);
+
+// Launch one or two problems in a single persistent launch.
+// Problem p: C[M, N] = A·B with A given by `a[p]` and B by `b[p]`.
+int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
+                   int* counter, cudaStream_t st);
+
+}  // namespace tc
+}  // namespace lk

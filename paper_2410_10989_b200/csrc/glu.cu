@@ -1,0 +1,152 @@
+// SwiGLU / GeGLU forward + backward: pure streaming kernels, 128-bit vectorised.
+//
+// Forward  c = act(a) * b          (rowfuse/ops.py:389-402, 438-451)
+// Backward da, db written in place  (rowfuse/ops.py:405-430, 454-482;
+//                                    Liger in-place contract LK/ops/swiglu.py:61-62,
+//                                    LK/ops/geglu.py:85-86)
+// Casting points follow Liger: the activation is computed in fp32 and cast to b's
+// dtype before the multiply (LK/ops/swiglu.py:28-31, LK/ops/geglu.py:43-44).
+#include "common.cuh"
+
+namespace lk {
+
+constexpr float kGeluC = 0.7978845608028654f;  // sqrt(2/pi)   rowfuse/ops.py:37
+constexpr float kGeluA = 0.044715f;            //              rowfuse/ops.py:38
+constexpr float kGelu3A = 0.134145f;           // 3 * 0.044715 rowfuse/ops.py:39
+
+template <bool ACC>
+__device__ __forceinline__ float tanh_sel(float x) { return ACC ? tanhf(x) : tanh_fast(x); }
+
+__device__ __forceinline__ float sigmoidf_(float z) { return 1.f / (1.f + __expf(-z)); }
+
+template <typename T, int ACT>
+struct Glu {
+  static constexpr bool ACC = sizeof(T) == 4;
+  // forward value for one element
+  static __device__ __forceinline__ float fwd(float a, float b) {
+    float act;
+    if (ACT == 0) {
+      act = a * sigmoidf_(a);
+    } else {
+      float t = tanh_sel<ACC>(kGeluC * (a + kGeluA * a * a * a));
+      act = 0.5f * a * (1.f + t);
+    }
+    return round_to<T>(act) * b;
+  }
+  // backward: returns (da, db)
+  static __device__ __forceinline__ void bwd(float dc, float a, float b, float& da, float& db) {
+    if (ACT == 0) {
+      float sg = sigmoidf_(a);
+      float silu = a * sg;
+      db = dc * silu;
+      da = dc * (silu * (1.f - sg) + sg) * b;
+    } else {
+      float t = tanh_sel<ACC>(kGeluC * (a + kGeluA * a * a * a));
+      float g = round_to<T>(0.5f * a * (1.f + t));
+      db = dc * g;
+      float dg = 0.5f * (1.f + t) + 0.5f * kGeluC * a * (1.f - t * t) * (1.f + kGelu3A * a * a);
+      da = dc * b * dg;
+    }
+  }
+};
+
+template <typename T, int ACT>
+__global__ void __launch_bounds__(256) glu_fwd_kernel(const T* __restrict__ a, const T* __restrict__ b,
+                                                      T* __restrict__ c, int64_t n) {
+  constexpr int NV = Vec16<T>::N;
+  const int64_t nvec = n / NV;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    Vec16<T> va, vb;
+    va.load_nc(a + i * NV);
+    vb.load_nc(b + i * NV);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) va.v[k] = Glu<T, ACT>::fwd(va.v[k], vb.v[k]);
+    va.store(c + i * NV);
+  }
+  for (int64_t i = nvec * NV + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    c[i] = from_f<T>(Glu<T, ACT>::fwd(to_f<T>(a[i]), to_f<T>(b[i])));
+}
+
+template <typename T, int ACT>
+__global__ void __launch_bounds__(256) glu_bwd_kernel(const T* __restrict__ dc, T* __restrict__ a,
+                                                      T* __restrict__ b, int64_t n) {
+  constexpr int NV = Vec16<T>::N;
+  const int64_t nvec = n / NV;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    Vec16<T> vd, va, vb;
+    vd.load_nc(dc + i * NV);
+    va.load(a + i * NV);
+    vb.load(b + i * NV);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      float da, db;
+      Glu<T, ACT>::bwd(vd.v[k], va.v[k], vb.v[k], da, db);
+      va.v[k] = da;
+      vb.v[k] = db;
+    }
+    va.store(a + i * NV);
+    vb.store(b + i * NV);
+  }
+  for (int64_t i = nvec * NV + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    float da, db;
+    Glu<T, ACT>::bwd(to_f<T>(dc[i]), to_f<T>(a[i]), to_f<T>(b[i]), da, db);
+    a[i] = from_f<T>(da);
+    b[i] = from_f<T>(db);
+  }
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+static unsigned grid_for(int64_t n, int nv) {
+  int64_t work = (n / nv) + 1;
+  int64_t blocks = (work + 255) / 256;
+  int64_t cap = (int64_t)sm_count() * 8;  // 8 x 256-thread CTAs per SM resident
+  return (unsigned)std::max<int64_t>(1, std::min(blocks, cap));
+}
+
+template <int ACT>
+static int glu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream) {
+  LK_REQUIRE(n >= 0, LK_SIZE_MISMATCH, "n must be >= 0");
+  if (n == 0) return LK_OK;
+  LK_REQUIRE(a && b && c, LK_INVALID_ARGUMENT, "null pointer");
+  LK_REQUIRE(aligned16(a) && aligned16(b) && aligned16(c), LK_NON_CONTIGUOUS,
+             "GLU operands must be 16-byte aligned contiguous buffers");
+  cudaStream_t st = as_stream(stream);
+  LK_DISPATCH_FLOAT(dtype, T, {
+    glu_fwd_kernel<T, ACT><<<grid_for(n, Vec16<T>::N), 256, 0, st>>>(
+        static_cast<const T*>(a), static_cast<const T*>(b), static_cast<T*>(c), n);
+  });
+  return check_launch("glu_fwd_kernel");
+}
+
+template <int ACT>
+static int glu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream) {
+  LK_REQUIRE(n >= 0, LK_SIZE_MISMATCH, "n must be >= 0");
+  if (n == 0) return LK_OK;
+  LK_REQUIRE(a && b && dc, LK_INVALID_ARGUMENT, "null pointer");
+  LK_REQUIRE(aligned16(a) && aligned16(b) && aligned16(dc), LK_NON_CONTIGUOUS,
+             "GLU operands must be 16-byte aligned contiguous buffers");
+  cudaStream_t st = as_stream(stream);
+  LK_DISPATCH_FLOAT(dtype, T, {
+    glu_bwd_kernel<T, ACT><<<grid_for(n, Vec16<T>::N), 256, 0, st>>>(
+        static_cast<const T*>(dc), static_cast<T*>(a), static_cast<T*>(b), n);
+  });
+  return check_launch("glu_bwd_kernel");
+}
+
+}  // namespace lk
+
+extern "C" int lk_swiglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream) {
+  return lk::glu_fwd<0>(a, b, c, n, dtype, stream);
+}
+extern "C" int lk_swiglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream) {
+  return lk::glu_bwd<0>(dc, a, b, n, dtype, stream);
+}
+extern "C" int lk_geglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream) {
+  return lk::glu_fwd<1>(a, b, c, n, dtype, stream);
+}
+extern "C" int lk_geglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream) {
+  return lk::glu_bwd<1>(dc, a, b, n, dtype, stream);
+}

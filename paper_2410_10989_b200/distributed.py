@@ -1,0 +1,184 @@
+"""Multi-GPU FLCE: token-sharded and vocab-parallel modes (one process per GPU).
+
+Token-sharded.  Rank r owns rows [r*BT/R, (r+1)*BT/R) and a
+full replica of W.  Rows are independent except for the MEAN denominator and the
+dW sum (rowfuse/flce.py:161-168; dW additivity over row groups is the reference's
+own test, tests/test_flce.py:182-205).  Collectives: one int64 all-reduce of the
+non-ignored count before the local FLCE (so every rank divides by the global
+count inside the finalize kernel, no host sync), one all-reduce of the loss, one
+NCCL all-reduce of dW in the weight dtype.
+
+Vocab-parallel (row 2).  Rank r owns W rows [v0, v0 + V/R) and sees all tokens.
+Per row chunk: local logits + per-row (max, sumexp, sum_logits, target_logit)
+statistics (lk_flce_vp_logits), an all-reduce of the statistics (MAX, then SUM
+of rescaled sums), then local dlogits, an fp32 partial dX (all-reduced SUM) and
+the local dW shard (no communication) (lk_flce_vp_backward).
+
+The compute callbacks are injectable so the host-side collective logic is tested
+on CPU with gloo and the oracle standing in for the CUDA kernels
+(tests/test_distributed.py); the default callbacks are the sm_100a library.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from ._utils import as_targets, check, dtype_code, lib, ptr, stream_of, workspace
+
+
+# ------------------------------------------------------------- token sharded
+def shard_rows(n_rows: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous, as-even-as-possible row range of `rank`."""
+    base, extra = divmod(n_rows, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def _count_cuda(t: torch.Tensor, vocab: int, ignore_index: int) -> torch.Tensor:
+    out = torch.empty(2, dtype=torch.int64, device=t.device)
+    check(lib().lk_count_targets(t.data_ptr(), t.numel(), vocab, ignore_index, out.data_ptr(), stream_of(t)))
+    return out
+
+
+def _local_flce_cuda(x, w, t, mean_count, **kw):
+    from .fused_linear_cross_entropy import fused_linear_cross_entropy_forward
+
+    loss, _, _, _, gx, gw, _ = fused_linear_cross_entropy_forward(
+        x, w, t, compute_grad_input=True, compute_grad_weight=True, mean_count=mean_count[:1], **kw)
+    return loss, gx, gw
+
+
+def token_sharded_flce(
+    x_local: torch.Tensor,
+    weight: torch.Tensor,
+    target_local: torch.Tensor,
+    group=None,
+    ignore_index: int = -100,
+    reduction: str = "mean",
+    count_fn: Optional[Callable] = None,
+    local_fn: Optional[Callable] = None,
+    reduce_grad_weight: bool = True,
+    **kw,
+):
+    """Returns (global loss, local grad_x, all-reduced grad_w)."""
+    t = as_targets(target_local) if target_local.is_cuda else target_local.reshape(-1).to(torch.int64)
+    count_fn = count_fn or (lambda tt: _count_cuda(tt, weight.shape[0], ignore_index))
+    local_fn = local_fn or _local_flce_cuda
+    counts = count_fn(t)
+    if reduction == "mean":
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    loss, gx, gw = local_fn(x_local, weight, t, counts, ignore_index=ignore_index, reduction=reduction, **kw)
+    loss = loss.clone()
+    dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+    if reduce_grad_weight and gw is not None:
+        dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=group)
+    return loss, gx, gw
+
+
+# ------------------------------------------------------------ vocab parallel
+@dataclass
+class VocabShard:
+    offset: int
+    size: int
+    total: int
+
+
+def vocab_shard(vocab: int, rank: int, world: int) -> VocabShard:
+    lo, hi = shard_rows(vocab, rank, world)
+    return VocabShard(lo, hi - lo, vocab)
+
+
+def combine_row_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
+    """All-reduce per-row (max, sumexp, sum_logits, target_logit) across vocab shards."""
+    m = stats[:, 0].clone()
+    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
+    out = torch.empty_like(stats)
+    out[:, 0] = m
+    out[:, 1] = stats[:, 1] * torch.exp(stats[:, 0] - m)
+    out[:, 2] = stats[:, 2]
+    out[:, 3] = stats[:, 3]
+    rest = out[:, 1:].contiguous()
+    dist.all_reduce(rest, op=dist.ReduceOp.SUM, group=group)
+    out[:, 1:] = rest
+    return out
+
+
+class CudaVocabOps:
+    """Default stage implementations: the sm_100a library."""
+
+    def __init__(self, dtype: torch.dtype, device: torch.device):
+        self.dt = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}[dtype]
+        self.device = device
+
+    def logits_stats(self, x, w_shard, t, shard: VocabShard, softcap, ignore_index):
+        rows, h = x.shape
+        ldz = -(-shard.size // 64) * 64
+        buf = torch.empty(rows, ldz, dtype=x.dtype, device=x.device)
+        stats = torch.empty(rows, 4, dtype=torch.float32, device=x.device)
+        L = lib()
+        ws = workspace(L.lk_flce_vp_workspace_bytes(rows, h, shard.size, self.dt), x.device)
+        check(L.lk_flce_vp_logits(ptr(x), ptr(w_shard), ptr(t), rows, h, shard.size, shard.offset, self.dt,
+                                  ignore_index, float(softcap or 0.0), ptr(stats), ptr(buf), ptr(ws), ws.numel(),
+                                  stream_of(x)))
+        return stats, buf
+
+    def backward(self, x, w_shard, t, shard, stats_g, buf, n_valid, gw_acc, accumulate, *, ignore_index,
+                 label_smoothing, lse_square_scale, softcap, reduction):
+        rows, h = x.shape
+        loss_rows = torch.empty(rows, dtype=torch.float32, device=x.device)
+        gx = torch.empty(rows, h, dtype=torch.float32, device=x.device)
+        ws = workspace(256, x.device)
+        check(lib().lk_flce_vp_backward(
+            ptr(x), ptr(w_shard), ptr(t), rows, h, shard.size, shard.offset, shard.total, self.dt, ignore_index,
+            float(label_smoothing), float(lse_square_scale), float(softcap or 0.0), _capi.REDUCTIONS[reduction],
+            ptr(n_valid), ptr(stats_g), ptr(buf), ptr(loss_rows), ptr(gx), ptr(gw_acc), int(accumulate), ptr(ws),
+            ws.numel(), stream_of(x)))
+        return loss_rows, gx
+
+    def count(self, t, vocab, ignore_index):
+        return _count_cuda(t, vocab, ignore_index)
+
+
+def vocab_parallel_flce(
+    x: torch.Tensor,
+    w_shard: torch.Tensor,
+    target: torch.Tensor,
+    shard: VocabShard,
+    group=None,
+    ignore_index: int = -100,
+    label_smoothing: float = 0.0,
+    lse_square_scale: float = 0.0,
+    softcap: Optional[float] = None,
+    reduction: str = "mean",
+    chunk_rows: int = 2048,
+    ops=None,
+):
+    """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
+
+    Every rank holds all rows of x and the targets; only W is sharded by vocab rows.
+    """
+    ops = ops or CudaVocabOps(x.dtype, x.device)
+    t = target.reshape(-1).to(torch.int64).contiguous()
+    bt, h = x.shape
+    n_valid = ops.count(t, shard.total, ignore_index)
+    gw_acc = torch.zeros(shard.size, h, dtype=torch.float32, device=x.device)
+    gx = torch.empty(bt, h, dtype=x.dtype, device=x.device)
+    loss_rows = torch.empty(bt, dtype=torch.float32, device=x.device)
+    kw = dict(ignore_index=ignore_index, label_smoothing=label_smoothing, lse_square_scale=lse_square_scale,
+              softcap=softcap, reduction=reduction)
+    for ci, lo in enumerate(range(0, bt, chunk_rows)):
+        hi = min(lo + chunk_rows, bt)
+        xc, tc = x[lo:hi].contiguous(), t[lo:hi]
+        stats, buf = ops.logits_stats(xc, w_shard, tc, shard, softcap, ignore_index)
+        stats_g = combine_row_stats(stats, group)
+        lr, gxp = ops.backward(xc, w_shard, tc, shard, stats_g, buf, n_valid, gw_acc, ci > 0, **kw)
+        dist.all_reduce(gxp, op=dist.ReduceOp.SUM, group=group)
+        gx[lo:hi] = gxp.to(x.dtype)
+        loss_rows[lo:hi] = lr
+    loss = loss_rows if reduction == "none" else loss_rows.sum()
+    return loss, gx, gw_acc.to(w_shard.dtype)

@@ -1,0 +1,255 @@
+"""Fused linear cross entropy: LigerFusedLinearCrossEntropyFunction / ...Loss.
+
+Drop-in for liger_kernel's FLCE (LK/transformers/fused_linear_cross_entropy.py:9-69,
+LK/ops/fused_linear_cross_entropy.py:17-400).  The algorithm is the reference's
+chunked projection head (rowfuse/flce.py:107-173): logits are produced one row
+chunk at a time, turned into logit gradients in place, and folded into dX and
+dW, so the full BT x V logits never exist.  Everything on the path runs in the
+sm_100a library through one C-ABI call (lk_flce_forward_backward); the gradients
+are computed during the forward and backward only scales them by grad_output.
+"""
+
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+
+from . import _capi, errors
+from ._utils import (
+    as_targets,
+    check,
+    dtype_code,
+    lib,
+    ptr,
+    raise_if_out_of_range,
+    require_contiguous,
+    require_cuda,
+    stream_of,
+    workspace,
+)
+from .cross_entropy import CrossEntropyOutput
+
+
+def flce_plan(bt: int, hidden: int, vocab: int, dtype: torch.dtype = torch.bfloat16) -> tuple[int, int]:
+    """B200 chunk policy (chunk_rows, num_chunks) from the library (see flce.cu b200_chunk_rows)."""
+    c = _capi.C.c_int64()
+    n = _capi.C.c_int64()
+    code = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}[dtype]
+    check(lib().lk_flce_plan(bt, hidden, vocab, code, _capi.C.byref(c), _capi.C.byref(n)))
+    return int(c.value), int(n.value)
+
+
+def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=None, has_grad_w=True) -> int:
+    code = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}[dtype]
+    return int(lib().lk_flce_workspace_bytes(bt, hidden, vocab, code, int(chunk_rows or 0), int(has_grad_w)))
+
+
+def fused_linear_cross_entropy_forward(
+    _input: torch.Tensor,
+    weight: torch.Tensor,
+    target: torch.Tensor,
+    ce_weight=None,
+    bias: Optional[torch.Tensor] = None,
+    ignore_index: int = -100,
+    lse_square_scale: float = 0.0,
+    label_smoothing: float = 0.0,
+    reduction: str = "mean",
+    softcap: Optional[float] = None,
+    return_z_loss: bool = False,
+    accum_dtype=None,
+    use_token_scaling: bool = False,
+    return_token_accuracy: bool = False,
+    return_predicted_tokens: bool = False,
+    chunk_rows: Optional[int] = None,
+    force_simt: bool = False,
+    compute_grad_input: Optional[bool] = None,
+    compute_grad_weight: Optional[bool] = None,
+    mean_count: Optional[torch.Tensor] = None,
+):
+    """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
+
+    Same return tuple as LK/ops/fused_linear_cross_entropy.py:17-244.  grad_weight is
+    accumulated in fp32 across chunks regardless of accum_dtype (>= Liger precision) and
+    returned in weight.dtype, as Liger does.  `mean_count` (CUDA int64 scalar) overrides
+    the MEAN denominator with a global non-ignored count (token-sharded mode).
+    """
+    if ce_weight is not None:
+        raise errors.UnsupportedOption("ce_weight is not implemented in the B200 build")
+    if use_token_scaling or return_token_accuracy or return_predicted_tokens:
+        raise errors.UnsupportedOption("token scaling / accuracy / predicted tokens are not implemented")
+    if not (0.0 <= label_smoothing <= 1.0):
+        raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
+    if reduction not in _capi.REDUCTIONS:
+        raise ValueError(f"reduction must be 'mean' or 'sum' or 'none'. Got: {reduction}")
+    if softcap is not None and not softcap > 0:
+        raise ValueError(f"softcap must greater than 0.0 or None. Got: {softcap}")
+    require_cuda(_input, weight, target, bias)
+    if _input.dim() != 2 or weight.dim() != 2:
+        raise errors.ShapeMismatch("expected _input (BT, H) and weight (V, H)")
+    bt, h = _input.shape
+    v, hw = weight.shape
+    if hw != h:
+        raise errors.ShapeMismatch(f"hidden width {h} != weight input width {hw}")
+    if weight.dtype != _input.dtype:
+        raise errors.ShapeMismatch(f"weight dtype {weight.dtype} != input dtype {_input.dtype}")
+    if bias is not None and (bias.shape != (v,) or bias.dtype != weight.dtype):
+        raise errors.ShapeMismatch("bias must be (V,) in the weight dtype")
+    t = as_targets(target)
+    if t.numel() != bt:
+        raise errors.ShapeMismatch(f"need one target per row ({bt}), got {t.numel()}")
+    x = _input.contiguous()
+    w = weight.contiguous()
+    b = bias.contiguous() if bias is not None else None
+    require_contiguous("_input", x)
+    need_gx = _input.requires_grad if compute_grad_input is None else compute_grad_input
+    need_gw = (need_gx and weight.requires_grad) if compute_grad_weight is None else compute_grad_weight
+    dev = x.device
+    grad_x = torch.empty_like(x) if need_gx else None
+    grad_w = torch.empty_like(w) if need_gw else None
+    grad_b = torch.empty_like(b) if (b is not None and need_gx) else None
+    loss_rows = torch.empty(bt, dtype=torch.float32, device=dev)
+    loss_sum = torch.empty((), dtype=torch.float32, device=dev)
+    z_rows = torch.empty(bt, dtype=torch.float32, device=dev) if return_z_loss else None
+    z_sum = torch.empty((), dtype=torch.float32, device=dev) if return_z_loss else None
+    stats = torch.empty(2, dtype=torch.int64, device=dev)
+    L = lib()
+    dt = dtype_code(x)
+    cr = int(chunk_rows or 0)
+    ws = workspace(L.lk_flce_workspace_bytes(bt, h, v, dt, cr, int(grad_w is not None)), dev)
+    args = _capi.FlceArgs(
+        x=ptr(x), weight=ptr(w), target=ptr(t), bias=ptr(b), bt=bt, hidden=h, vocab=v, dtype=dt,
+        ignore_index=int(ignore_index), label_smoothing=float(label_smoothing),
+        lse_square_scale=float(lse_square_scale), softcap=float(softcap) if softcap is not None else 0.0,
+        reduction=_capi.REDUCTIONS[reduction], chunk_rows=cr, loss_rows=ptr(loss_rows), loss_sum=ptr(loss_sum),
+        z_loss_rows=ptr(z_rows), z_loss_sum=ptr(z_sum), grad_x=ptr(grad_x), grad_w=ptr(grad_w),
+        grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=ptr(ws), workspace_bytes=ws.numel(),
+        stream=stream_of(x), force_simt=int(bool(force_simt)),
+        mean_count=ptr(mean_count) if mean_count is not None else None,
+    )
+    if mean_count is not None and (mean_count.dtype != torch.int64 or not mean_count.is_cuda):
+        raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")
+    check(L.lk_flce_forward_backward(_capi.C.byref(args)))
+    del ws
+    raise_if_out_of_range(stats, v)
+    if reduction == "none":
+        loss = loss_rows
+        z_loss = z_rows.to(x.dtype) if return_z_loss else None
+    else:
+        loss = loss_sum
+        z_loss = z_sum.to(x.dtype) if return_z_loss else None
+    return loss, z_loss, None, None, grad_x, grad_w, grad_b
+
+
+def fused_linear_cross_entropy_backward(grad_output, grad_input, grad_weight, grad_bias):
+    """Scale the forward-computed gradients by grad_output (LK/ops/fused_linear_cross_entropy.py:247-291).
+
+    The scale kernel reads grad_output on the device and returns immediately when it
+    is 1.0, so there is no torch.equal host sync.
+    """
+    if grad_output.ndim > 0:
+        g = grad_output.reshape(-1)
+        # dW = sum_r g_r dZ_r^T x_r cannot be rescaled after the fact unless g is uniform.
+        if g.numel() and not bool(torch.all(g == g[0])):
+            raise errors.UnsupportedOption("reduction='none' backward with a non-uniform grad_output")
+        g = g[:1] if g.numel() else torch.ones(1, device=grad_output.device)
+    else:
+        g = grad_output.reshape(1)
+    g = g.detach().to(torch.float32).contiguous()
+    L = lib()
+    for t in (grad_input, grad_weight):
+        if t is not None and t.numel():
+            check(L.lk_scale_by_device_scalar(t.data_ptr(), t.shape[0], t.shape[1], t.stride(0), dtype_code(t),
+                                              g.data_ptr(), stream_of(t)))
+    if grad_bias is not None and grad_bias.numel():
+        check(L.lk_scale_by_device_scalar(grad_bias.data_ptr(), 1, grad_bias.numel(), grad_bias.numel(),
+                                          dtype_code(grad_bias), g.data_ptr(), stream_of(grad_bias)))
+    return grad_input, grad_weight, grad_bias
+
+
+class LigerFusedLinearCrossEntropyFunction(torch.autograd.Function):
+    """Same signature and 15-slot backward arity as LK/ops/fused_linear_cross_entropy.py:294-400."""
+
+    @staticmethod
+    def forward(
+        ctx,
+        _input,
+        weight,
+        target,
+        bias=None,
+        ce_weight=None,
+        ignore_index=-100,
+        lse_square_scale=0.0,
+        label_smoothing=0.0,
+        reduction="mean",
+        softcap=None,
+        return_z_loss: bool = False,
+        accum_dtype=None,
+        use_token_scaling: bool = False,
+        return_token_accuracy: bool = False,
+        return_predicted_tokens: bool = False,
+        chunk_rows: Optional[int] = None,
+    ):
+        loss, z_loss, acc, pred, gx, gw, gb = fused_linear_cross_entropy_forward(
+            _input, weight, target, ce_weight, bias, ignore_index, lse_square_scale, label_smoothing, reduction,
+            softcap, return_z_loss, accum_dtype, use_token_scaling, return_token_accuracy,
+            return_predicted_tokens, chunk_rows=chunk_rows,
+        )
+        ctx.save_for_backward(
+            gx.detach() if gx is not None else None,
+            gw.detach() if gw is not None else None,
+            gb.detach() if gb is not None else None,
+        )
+        return loss, z_loss, acc, pred
+
+    @staticmethod
+    def backward(ctx, grad_output, grad_output2, grad_output3, grad_output4):
+        gx, gw, gb = ctx.saved_tensors
+        gx, gw, gb = fused_linear_cross_entropy_backward(grad_output, gx, gw, gb)
+        return (gx, gw, None, gb) + (None,) * 12
+
+
+class LigerFusedLinearCrossEntropyLoss(torch.nn.Module):
+    """Drop-in for LK/transformers/fused_linear_cross_entropy.py:9-69 (plus an optional chunk_rows override)."""
+
+    def __init__(
+        self,
+        ce_weight: Optional[torch.FloatTensor] = None,
+        ignore_index: int = -100,
+        lse_square_scale: float = 0.0,
+        label_smoothing: float = 0.0,
+        reduction: str = "mean",
+        softcap: Optional[float] = None,
+        return_z_loss: bool = False,
+        accum_dtype: Optional[torch.dtype] = None,
+        use_token_scaling: bool = False,
+        return_token_accuracy: bool = False,
+        return_predicted_tokens: bool = False,
+        chunk_rows: Optional[int] = None,
+    ):
+        super().__init__()
+        assert 0 <= label_smoothing <= 1, f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}"
+        assert reduction in {"mean", "sum", "none"}, f"reduction must be 'mean' or 'sum' or 'none'. Got: {reduction}"
+        assert softcap is None or softcap > 0, f"softcap must greater than 0.0 or None. Got: {softcap}"
+        self.ce_weight = ce_weight
+        self.ignore_index = ignore_index
+        self.lse_square_scale = lse_square_scale
+        self.label_smoothing = label_smoothing
+        self.reduction = reduction
+        self.softcap = softcap
+        self.return_z_loss = return_z_loss
+        self.accum_dtype = accum_dtype
+        self.use_token_scaling = use_token_scaling
+        self.return_token_accuracy = return_token_accuracy
+        self.return_predicted_tokens = return_predicted_tokens
+        self.chunk_rows = chunk_rows
+
+    def forward(self, lin_weight, _input, target, bias=None):
+        loss, z_loss, acc, pred = LigerFusedLinearCrossEntropyFunction.apply(
+            _input, lin_weight, target, bias, self.ce_weight, self.ignore_index, self.lse_square_scale,
+            self.label_smoothing, self.reduction, self.softcap, self.return_z_loss, self.accum_dtype,
+            self.use_token_scaling, self.return_token_accuracy, self.return_predicted_tokens, self.chunk_rows,
+        )
+        if not self.return_z_loss and not self.return_token_accuracy and not self.return_predicted_tokens:
+            return loss
+        return CrossEntropyOutput(loss=loss, z_loss=z_loss, token_accuracy=acc, predicted_tokens=pred)

@@ -1,0 +1,147 @@
+"""C-ABI boundary checks that need no GPU: the library loads, exports every symbol
+include/liger_b200.h declares, validates arguments into the reference's error
+taxonomy, and the Python surface matches liger_kernel's signatures."""
+
+import ctypes as C
+import inspect
+import re
+from pathlib import Path
+
+import pytest
+import torch
+
+import paper_2410_10989_b200 as lk
+from paper_2410_10989_b200 import _capi, errors
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "liger_b200.h"
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(lk_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _capi.load()
+    syms = declared_symbols()
+    assert len(syms) >= 25
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_capi.SIGNATURES), "ctypes binding out of sync with the header"
+    assert lib.lk_has_tcgen05() == 1
+    assert b"sm_100a" in lib.lk_version()
+
+
+def test_flce_args_struct_matches_header_field_order():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    body = re.search(r"typedef struct \{(.*?)\} lk_flce_args;", text, flags=re.S).group(1)
+    names = []
+    for stmt in body.split(";"):
+        stmt = stmt.strip()
+        if stmt:
+            names += re.findall(r"(\w+)\s*(?:,|$)", stmt)
+    assert names == [f[0] for f in _capi.FlceArgs._fields_]
+
+
+def test_plan_and_workspace_queries():
+    lib = _capi.load()
+    c, n = C.c_int64(), C.c_int64()
+    assert lib.lk_flce_plan(8192, 4096, 128256, 1, C.byref(c), C.byref(n)) == 0
+    assert (c.value, n.value) == (2048, 4)
+    assert lib.lk_flce_plan(1024, 512, 4096, 0, C.byref(c), C.byref(n)) == 0
+    assert (c.value, n.value) == (1024, 1)
+    assert lib.lk_flce_plan(0, 4096, 128256, 1, C.byref(c), C.byref(n)) == 3  # SIZE_MISMATCH
+    ws = lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 0, 1)
+    chunk = 2048 * 128256 * 2
+    dw_acc = 128256 * 4096 * 4
+    assert chunk + dw_acc < ws < chunk + dw_acc + 64 * 2**20
+    assert lk.flce_plan(8192, 4096, 128256) == (2048, 4)
+
+
+def test_status_codes_map_to_reference_exceptions():
+    lib = _capi.load()
+    rc = lib.lk_rope(None, None, None, None, 1, 4, 2, 2, 7, 1, 1, 1, 0, None)
+    assert rc == 4
+    with pytest.raises(errors.OddHeadDim):
+        _capi.check(rc)
+    assert "even" in lib.lk_last_error().decode()
+    rc = lib.lk_rope(None, None, None, None, 2, 4, 2, 2, 8, 3, 1, 1, 0, None)
+    with pytest.raises(errors.ShapeMismatch):
+        _capi.check(rc)
+    rc = lib.lk_cross_entropy_fwd(None, 2, None, 4, 8, 1, -100, 0.0, 0.0, 0.0, 1, 1, None, None, None, None,
+                                  None, 0, None)
+    with pytest.raises(errors.NonContiguousInput):
+        _capi.check(rc)
+    rc = lib.lk_swiglu_fwd(None, None, None, -1, 1, None)
+    with pytest.raises(errors.SizeMismatch):
+        _capi.check(rc)
+    assert issubclass(errors.TargetOutOfRange, IndexError)
+    assert issubclass(errors.ShapeMismatch, ValueError)
+
+
+def test_no_cpu_fallback():
+    x = torch.randn(4, 8)
+    t = torch.zeros(4, dtype=torch.long)
+    with pytest.raises(errors.ExtensionMissing):
+        lk.LigerCrossEntropyLoss()(x, t)
+    with pytest.raises(errors.ExtensionMissing):
+        lk.LigerFusedLinearCrossEntropyLoss()(torch.randn(16, 8), x, t)
+    with pytest.raises(errors.ExtensionMissing):
+        lk.LigerRMSNorm(8)(x)
+    with pytest.raises(errors.ExtensionMissing):
+        lk.liger_swiglu(x, x)
+
+
+def _params(obj):
+    sig = inspect.signature(obj)
+    return [(p.name, p.default) for p in sig.parameters.values() if p.name not in ("self", "ctx")]
+
+
+@pytest.mark.parametrize(
+    "ours,theirs",
+    [
+        ("LigerCrossEntropyLoss.__init__", "liger_kernel.transformers.cross_entropy.LigerCrossEntropyLoss.__init__"),
+        ("LigerCrossEntropyLoss.forward", "liger_kernel.transformers.cross_entropy.LigerCrossEntropyLoss.forward"),
+        ("LigerFusedLinearCrossEntropyLoss.forward",
+         "liger_kernel.transformers.fused_linear_cross_entropy.LigerFusedLinearCrossEntropyLoss.forward"),
+        ("LigerRMSNorm.__init__", "liger_kernel.transformers.rms_norm.LigerRMSNorm.__init__"),
+        ("LigerRMSNorm.forward", "liger_kernel.transformers.rms_norm.LigerRMSNorm.forward"),
+        ("liger_rotary_pos_emb", "liger_kernel.transformers.rope.liger_rotary_pos_emb"),
+        ("LigerSwiGLUMLP.__init__", "liger_kernel.transformers.swiglu.LigerSwiGLUMLP.__init__"),
+        ("LigerGEGLUMLP.__init__", "liger_kernel.transformers.geglu.LigerGEGLUMLP.__init__"),
+        ("LigerCrossEntropyFunction.forward", "liger_kernel.ops.cross_entropy.LigerCrossEntropyFunction.forward"),
+    ],
+)
+def test_signatures_match_liger(ours, theirs):
+    lk_mod = pytest.importorskip("liger_kernel.transformers")  # noqa: F841  (third-party, signature source only)
+    import importlib
+
+    def resolve(path, root=None):
+        parts = path.split(".")
+        if root is None:
+            for i in range(len(parts), 0, -1):
+                try:
+                    obj = importlib.import_module(".".join(parts[:i]))
+                    break
+                except Exception:
+                    continue
+            rest = parts[i:]
+        else:
+            obj, rest = root, parts
+        for p in rest:
+            obj = getattr(obj, p)
+        return obj
+
+    a = _params(resolve(ours, lk))
+    b = _params(resolve(theirs))
+    assert a == b
+
+
+def test_flce_module_signature_is_liger_plus_chunk_override():
+    pytest.importorskip("liger_kernel.transformers")
+    from liger_kernel.transformers.fused_linear_cross_entropy import LigerFusedLinearCrossEntropyLoss as Ref
+
+    ours = _params(lk.LigerFusedLinearCrossEntropyLoss.__init__)
+    assert ours[:-1] == _params(Ref.__init__)
+    assert ours[-1] == ("chunk_rows", None)

@@ -1,0 +1,131 @@
+"""Standalone cross entropy on the GPU against the CPU oracle (GPU).
+
+fp32: rtol 1e-4 (atol 1e-4 * max|ref|); bf16: rtol 2e-2 (atol 2e-2 * max|ref|)
+with the oracle evaluated on the bf16-rounded inputs.  Ignored
+rows and token counts are checked exactly.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2410_10989_b200 as lk
+from oracle import liger_ref, rowfuse_port as rp
+from paper_2410_10989_b200 import errors
+from tests.conftest import rel_close
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+def run_ce(x_np, t_np, dtype, **kw):
+    x = torch.tensor(x_np, dtype=dtype, device="cuda").requires_grad_(True)
+    t = torch.tensor(t_np, dtype=torch.long, device="cuda")
+    loss_fn = lk.LigerCrossEntropyLoss(**kw)
+    loss = loss_fn(x, t)
+    if kw.get("reduction", "mean") == "none":
+        loss.sum().backward()
+    else:
+        loss.backward()
+    return loss.detach().float().cpu().numpy(), x.grad.float().cpu().numpy()
+
+
+def test_ce_known_answers(golden):
+    for k in (1, 2):
+        loss, grad = run_ce(golden[f"ce_kat_{k}_logits"], golden[f"ce_kat_{k}_target"], torch.float32,
+                            reduction="sum")
+        assert float(loss) == pytest.approx(float(golden[f"ce_kat_{k}_loss"]), rel=1e-5)
+        np.testing.assert_allclose(grad, golden[f"ce_kat_{k}_grad"], atol=1e-6)
+
+
+@pytest.mark.parametrize("case", ["a", "b", "c"])
+def test_ce_golden_fp32(golden, case):
+    mean = bool(golden[f"ce_rand_{case}_mean"])
+    loss, grad = run_ce(golden[f"ce_rand_{case}_logits"], golden[f"ce_rand_{case}_target"], torch.float32,
+                        reduction="mean" if mean else "sum")
+    assert float(loss) == pytest.approx(float(golden[f"ce_rand_{case}_loss"]), rel=1e-4)
+    ok, err = rel_close(grad, golden[f"ce_rand_{case}_grad"], 1e-4)
+    assert ok, err
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+@pytest.mark.parametrize("ls,cap,lss", [(0.0, None, 0.0), (0.1, None, 0.0), (0.0, 30.0, 0.0), (0.1, 5.0, 1e-4)])
+def test_ce_liger_semantics(dtype, reduction, ls, cap, lss):
+    rng = np.random.default_rng(0)
+    rows, v = 64, 5003
+    z = rng.normal(0, 3, (rows, v)).astype(np.float32)
+    t = rng.integers(0, v, rows)
+    t[rng.random(rows) < 0.1] = -100
+    zin = torch.tensor(z, dtype=dtype).float().numpy()  # oracle on the rounded inputs
+    ref_loss, ref_rows, _, ref_grad = liger_ref.ce(zin, t, ignore_index=-100, label_smoothing=ls, softcap=cap,
+                                                   lse_square_scale=lss, reduction=reduction)
+    loss, grad = run_ce(z, t, dtype, label_smoothing=ls, softcap=cap, lse_square_scale=lss, reduction=reduction)
+    tol = TOL[dtype]
+    ok, err = rel_close(loss, ref_loss, tol)
+    assert ok, ("loss", err)
+    ok, err = rel_close(grad, ref_grad, tol)
+    assert ok, ("grad", err)
+    # ignored rows: exactly zero gradient and loss
+    assert np.all(grad[t == -100] == 0.0)
+    if reduction == "none":
+        assert np.all(loss[t == -100] == 0.0)
+
+
+def test_ce_large_vocab_bf16_rows_sum_to_zero():
+    rows, v = 256, 128256
+    g = torch.Generator(device="cuda").manual_seed(1)
+    x = (torch.randn(rows, v, device="cuda", generator=g) * 2).to(torch.bfloat16).requires_grad_(True)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    loss = lk.LigerCrossEntropyLoss(reduction="sum")(x, t)
+    loss.backward()
+    ref = torch.nn.functional.cross_entropy(x.detach().float(), t, reduction="sum")
+    assert loss.item() == pytest.approx(ref.item(), rel=2e-2)
+    rs = x.grad.float().sum(dim=1)
+    assert rs.abs().max().item() < 5e-2  # bf16 rounding of ~1e5 entries per row
+
+
+def test_ce_inplace_and_backward_scale():
+    rows, v = 8, 100
+    x = torch.randn(rows, v, device="cuda", requires_grad=True)
+    t = torch.randint(0, v, (rows,), device="cuda")
+    loss = lk.LigerCrossEntropyLoss()(x * 1.0, t)
+    (3.0 * loss).backward()
+    ref_x = x.detach().clone().requires_grad_(True)
+    (3.0 * torch.nn.functional.cross_entropy(ref_x, t)).backward()
+    torch.testing.assert_close(x.grad, ref_x.grad, rtol=1e-4, atol=1e-6)
+
+
+def test_ce_target_out_of_range_raises():
+    x = torch.randn(4, 10, device="cuda", requires_grad=True)
+    t = torch.tensor([0, 1, 10, 2], device="cuda")
+    with pytest.raises(errors.TargetOutOfRange):
+        lk.LigerCrossEntropyLoss()(x, t)
+
+
+def test_ce_mean_is_sum_over_count_exact_count():
+    rows, v = 33, 77
+    x = torch.randn(rows, v, device="cuda")
+    t = torch.randint(0, v, (rows,), device="cuda")
+    t[::3] = -100
+    n = int((t != -100).sum())
+    lm = lk.LigerCrossEntropyLoss(reduction="mean")(x.clone(), t)
+    lsum = lk.LigerCrossEntropyLoss(reduction="sum")(x.clone(), t)
+    assert lm.item() == pytest.approx(lsum.item() / n, rel=1e-6)
+
+
+def test_rowfuse_inplace_contract_port_vs_gpu(golden):
+    """The reference mutates logits into the gradient (rowfuse/ops.py:546-551); so do we."""
+    x_np = golden["ce_rand_a_logits"]
+    x = torch.tensor(x_np, dtype=torch.float32, device="cuda", requires_grad=True)
+    t = torch.tensor(golden["ce_rand_a_target"], device="cuda")
+    buf = x.detach()
+    from paper_2410_10989_b200.cross_entropy import cross_entropy_forward
+
+    loss, _, _, _, g = cross_entropy_forward(buf, t, compute_grad=True)
+    assert g.data_ptr() == buf.data_ptr()
+    ref = x_np.copy()
+    rp.cross_entropy_(ref, golden["ce_rand_a_target"], mean=True)
+    ok, err = rel_close(buf.cpu().numpy(), ref, 1e-4)
+    assert ok, err

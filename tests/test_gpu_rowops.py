@@ -1,0 +1,173 @@
+"""RMSNorm, RoPE, SwiGLU/GeGLU on the GPU against the reference goldens and oracle (GPU)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2410_10989_b200 as lk
+from oracle import liger_ref, rowfuse_port as rp
+from tests.conftest import rel_close
+from tests.torch_ref import close
+
+pytestmark = pytest.mark.gpu
+
+
+def cuda(a, dtype=torch.float32):
+    return torch.tensor(np.ascontiguousarray(a), dtype=dtype, device="cuda")
+
+
+# ------------------------------------------------------------------ RMSNorm
+def test_rmsnorm_fp32_vs_reference_golden(golden):
+    x = cuda(golden["rms_x"]).requires_grad_(True)
+    m = lk.LigerRMSNorm(33, eps=1e-6, casting_mode="gemma", in_place=False).cuda()
+    with torch.no_grad():
+        m.weight.copy_(cuda(golden["rms_gamma"]))
+    y = m(x)
+    y.backward(cuda(golden["rms_dy"]))
+    assert rel_close(y.detach().cpu().numpy(), golden["rms_y"], 1e-4)[0]
+    assert rel_close(x.grad.cpu().numpy(), golden["rms_dx"], 1e-4)[0]
+    assert rel_close(m.weight.grad.cpu().numpy(), golden["rms_dgamma"], 1e-4)[0]
+
+
+@pytest.mark.parametrize("mode", ["llama", "gemma", "none"])
+@pytest.mark.parametrize("shape", [(8192, 4096), (37, 1000), (5, 4099)])
+def test_rmsnorm_bf16_vs_oracle(mode, shape):
+    rows, cols = shape
+    g = torch.Generator(device="cuda").manual_seed(rows + cols)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(torch.bfloat16)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    offset = 0.0 if mode != "gemma" else 1.0
+    xr = x.clone().requires_grad_(True)
+    wr = w.clone().requires_grad_(True)
+    y = lk.liger_rms_norm(xr, wr, 1e-6, offset, mode, False)
+    y.backward(dy)
+    sel = slice(0, min(rows, 512))
+    ry, _ = liger_ref.rmsnorm_fwd(x[sel].double().cpu().numpy(), w.double().cpu().numpy(), 1e-6, offset)
+    rdx, _ = liger_ref.rmsnorm_bwd(dy[sel].double().cpu().numpy(), x[sel].double().cpu().numpy(),
+                                   w.double().cpu().numpy(), 1e-6, offset)
+    assert rel_close(y[sel].float().detach().cpu().numpy(), ry, 2e-2)[0]
+    assert rel_close(xr.grad[sel].float().cpu().numpy(), rdx, 2e-2)[0]
+    # dW over all rows against a torch fp32 restatement
+    xf, dyf = x.float(), dy.float()
+    r = torch.rsqrt((xf * xf).mean(1, keepdim=True) + 1e-6)
+    rdw = (dyf * xf * r).sum(0)
+    assert close(wr.grad, rdw, 2e-2)
+
+
+def test_rmsnorm_dw_deterministic_and_batch_linear():
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(4096, 1024, device="cuda", generator=g)
+    w = torch.randn(1024, device="cuda", generator=g)
+    dy = torch.randn(4096, 1024, device="cuda", generator=g)
+    outs = []
+    for _ in range(2):
+        wr = w.clone().requires_grad_(True)
+        lk.liger_rms_norm(x, wr, 1e-6, 0.0, "gemma", False).backward(dy)
+        outs.append(wr.grad.clone())
+    assert torch.equal(outs[0], outs[1])  # fixed-order two-stage reduction
+
+
+# --------------------------------------------------------------------- RoPE
+def test_rope_fp32_vs_reference_golden(golden):
+    q, k, th, pos = golden["rope_q"], golden["rope_k"], golden["rope_thetas"], golden["rope_pos"]
+    rows, d = q.shape
+    # golden rows are independent tokens: map to (B=1, T=rows, nh=1, d) with per-token tables
+    ang = pos[:, None] * th[None, :]
+    emb = np.concatenate([ang, ang], axis=-1)
+    cos, sin = cuda(np.cos(emb)[None]), cuda(np.sin(emb)[None])
+    qt = cuda(q).reshape(1, rows, 1, d).transpose(1, 2)
+    kt = cuda(k).reshape(1, rows, 1, d).transpose(1, 2)
+    qo, ko = lk.liger_rotary_pos_emb(qt, kt, cos, sin)
+    assert rel_close(qo.transpose(1, 2).reshape(rows, d).cpu().numpy(), golden["rope_q_fwd"], 1e-4)[0]
+    assert rel_close(ko.transpose(1, 2).reshape(rows, d).cpu().numpy(), golden["rope_k_fwd"], 1e-4)[0]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_rope_llama3_gqa_fwd_bwd(dtype):
+    b, t, nq, nk, d = 4, 2048, 32, 8, 128
+    g = torch.Generator(device="cuda").manual_seed(1)
+    q0 = torch.randn(b, t, nq, d, device="cuda", generator=g).to(dtype)
+    k0 = torch.randn(b, t, nk, d, device="cuda", generator=g).to(dtype)
+    cos_np, sin_np = liger_ref.rope_tables(t, d, base=500000.0)
+    cos, sin = cuda(cos_np, dtype), cuda(sin_np, dtype)
+    q = q0.clone().transpose(1, 2).requires_grad_(True)
+    k = k0.clone().transpose(1, 2).requires_grad_(True)
+    qo, ko = lk.liger_rotary_pos_emb(q, k, cos, sin)
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    rq, rk = liger_ref.rope(q0[:1, :64].transpose(1, 2).double().cpu().numpy(),
+                            k0[:1, :64].transpose(1, 2).double().cpu().numpy(),
+                            cos.double().cpu().numpy()[:, :64], sin.double().cpu().numpy()[:, :64])
+    assert rel_close(qo[:1, :, :64].float().detach().cpu().numpy(), rq, tol)[0]
+    assert rel_close(ko[:1, :, :64].float().detach().cpu().numpy(), rk, tol)[0]
+    # backward is the inverse rotation: grad of sum(qo * u) wrt q = R^T u
+    u = torch.randn_like(qo)
+    v = torch.randn_like(ko)
+    torch.autograd.backward([qo, ko], [u, v])
+    bq, bk = liger_ref.rope(u[:1, :, :64].double().cpu().numpy(), v[:1, :, :64].double().cpu().numpy(),
+                            cos.double().cpu().numpy()[:, :64], sin.double().cpu().numpy()[:, :64], backward=True)
+    assert rel_close(q.grad[:1, :, :64].float().cpu().numpy(), bq, tol)[0]
+    assert rel_close(k.grad[:1, :, :64].float().cpu().numpy(), bk, tol)[0]
+
+
+def test_rope_per_batch_tables():
+    b, t, nq, nk, d = 2, 16, 4, 2, 64
+    q0 = torch.randn(b, nq, t, d, device="cuda")  # (B, nh, T, d) contiguous: Liger copies, rotates the copy
+    k0 = torch.randn(b, nk, t, d, device="cuda")
+    cos_np, sin_np = liger_ref.rope_tables(t, d, batch=b)
+    cos_np[1] = np.roll(cos_np[1], 3, axis=0)
+    sin_np[1] = np.roll(sin_np[1], 3, axis=0)
+    qo, ko = lk.liger_rotary_pos_emb(q0, k0, cuda(cos_np), cuda(sin_np))
+    rq, rk = liger_ref.rope(q0.double().cpu().numpy(), k0.double().cpu().numpy(), cos_np, sin_np)
+    assert rel_close(qo.cpu().numpy(), rq, 1e-4)[0]
+    assert rel_close(ko.cpu().numpy(), rk, 1e-4)[0]
+
+
+# ---------------------------------------------------------------------- GLU
+@pytest.mark.parametrize("kind", ["swiglu", "geglu"])
+def test_glu_fp32_vs_reference_golden(golden, kind):
+    x1 = cuda(golden["glu_x1"]).requires_grad_(True)
+    x2 = cuda(golden["glu_x2"]).requires_grad_(True)
+    fn = lk.liger_swiglu if kind == "swiglu" else lk.liger_geglu
+    y = fn(x1 * 1.0, x2 * 1.0)
+    y.backward(cuda(golden["glu_dy"]))
+    assert rel_close(y.detach().cpu().numpy(), golden[f"{kind}_y"], 1e-4)[0]
+    assert rel_close(x1.grad.cpu().numpy(), golden[f"{kind}_dx1"], 1e-4)[0]
+    assert rel_close(x2.grad.cpu().numpy(), golden[f"{kind}_dx2"], 1e-4)[0]
+
+
+@pytest.mark.parametrize("kind", ["swiglu", "geglu"])
+def test_glu_bf16_llama_shape(kind):
+    rows, cols = 8192, 14336
+    g = torch.Generator(device="cuda").manual_seed(2)
+    a = (torch.randn(rows, cols, device="cuda", generator=g) * 2).to(torch.bfloat16)
+    b = torch.randn(rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    dc = torch.randn(rows, cols, device="cuda", generator=g).to(torch.bfloat16)
+    ar, br = a.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    fn = lk.liger_swiglu if kind == "swiglu" else lk.liger_geglu
+    c = fn(ar * 1, br * 1)
+    c.backward(dc)
+    sel = slice(0, 256)
+    x1, x2, dy = (t[sel].double().cpu().numpy() for t in (a, b, dc))
+    fwd = rp.swiglu_forward if kind == "swiglu" else rp.geglu_forward
+    bwd = rp.swiglu_backward if kind == "swiglu" else rp.geglu_backward
+    assert rel_close(c[sel].float().detach().cpu().numpy(), fwd(x1, x2), 2e-2)[0]
+    rda, rdb = bwd(dy, x1, x2)
+    assert rel_close(ar.grad[sel].float().cpu().numpy(), rda, 2e-2)[0]
+    assert rel_close(br.grad[sel].float().cpu().numpy(), rdb, 2e-2)[0]
+
+
+def test_swiglu_mlp_module_matches_torch():
+    class Cfg:
+        hidden_size, intermediate_size, hidden_act = 256, 704, "silu"
+
+    torch.manual_seed(0)
+    m = lk.LigerSwiGLUMLP(Cfg()).cuda()
+    x = torch.randn(64, 256, device="cuda", requires_grad=True)
+    y = m(x)
+    ref = m.down_proj(torch.nn.functional.silu(m.gate_proj(x)) * m.up_proj(x))
+    torch.testing.assert_close(y, ref, rtol=1e-4, atol=1e-5)
+    gy = torch.randn_like(y)
+    gx = torch.autograd.grad(y, x, gy)[0]
+    gx_ref = torch.autograd.grad(ref, x, gy)[0]
+    torch.testing.assert_close(gx, gx_ref, rtol=1e-4, atol=1e-5)
