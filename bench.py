@@ -79,7 +79,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([s.strip() for s in line.split(",")])
+            self.rows.append((time.monotonic(), [s.strip() for s in line.split(",")]))
+
+    def mark(self, which):
+        setattr(self, which, time.monotonic())
 
     def __exit__(self, *a):
         if self.proc:
@@ -90,11 +93,15 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        rows = [r for ts, r in self.rows if t0 is None or (t0 - 0.1 <= ts <= t1 + 0.25)]
+        if not rows and self.rows:  # region shorter than the sampling period: nearest sample
+            rows = [min(self.rows, key=lambda tr: abs(tr[0] - (t0 or 0)))[1]]
+        sm = [float(r[0]) for r in rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             if len(r) >= 7:
                 for n, v in zip(names, r[3:7]):
                     if v.strip().lower() == "active":
@@ -203,6 +210,7 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
+    clk = ClockSampler(local).__enter__()  # started early: nvidia-smi needs ~0.5 s to emit samples
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -225,12 +233,14 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record()
-        for _ in range(args.steps):
-            step()
-        ev1.record()
-        torch.cuda.synchronize()
+    clk.mark("t0")
+    ev0.record()
+    for _ in range(args.steps):
+        step()
+    ev1.record()
+    torch.cuda.synchronize()
+    clk.mark("t1")
+    clk.__exit__()
     barrier()
     launches = (L.lk_launch_count() - n0) / args.steps
     L.lk_profile_enable(0)
@@ -340,7 +350,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--bt", type=int, default=BT)

@@ -1,0 +1,144 @@
+#!/usr/bin/env python
+"""Bandwidth-kernel benchmark at BASELINE cfg3 (Llama-3-8B decoder block, BT=8192, bf16).
+
+Each kernel runs through the C ABI on device-resident inputs; a 512 MiB buffer is
+written between timed launches so every launch starts with a cold L2 (several cfg3
+operands fit the 126 MB L2).  achieved = algorithmic bytes / CUDA-event time,
+frac = achieved / measured HBM copy bandwidth (MEASURED_PEAKS.json hbm_gbs).
+Prints one JSON line per kernel, and a summary line.
+
+    python bench_kernels.py [--reps 20]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import statistics
+import sys
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from bench import measured_peaks  # noqa: E402
+from paper_2410_10989_b200 import _capi  # noqa: E402
+
+BT, H, I, NQ, NK, D, V = 8192, 4096, 14336, 32, 8, 128, 128256
+
+
+def timed(fn, reps, flush):
+    fn()
+    torch.cuda.synchronize()
+    times = []
+    for _ in range(reps):
+        # evict L2 by READING 512 MiB (a write-based flush would leave dirty lines whose
+        # write-back would be charged to the timed kernel)
+        flush_sink.copy_(flush.view(torch.int64).sum())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return statistics.median(times)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--only", default="")
+    args = ap.parse_args()
+    dev = torch.device("cuda")
+    L = _capi.load()
+    st = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731
+    global flush_sink
+    flush = torch.ones(512 * 2**20, dtype=torch.uint8, device=dev)
+    flush_sink = torch.zeros((), dtype=torch.int64, device=dev)
+    peaks, src = measured_peaks()
+    hbm = float(peaks["hbm_gbs"])
+    bf = torch.bfloat16
+    g = torch.Generator(device=dev).manual_seed(0)
+    out = []
+
+    def report(name, bytes_, ms, extra=None):
+        gbs = bytes_ / (ms / 1e3) / 1e9
+        line = {"kernel": name, "bytes": bytes_, "ms": ms, "achieved_gbs": gbs, "peak_gbs": hbm,
+                "frac": gbs / hbm, "peak_source": f"{src} hbm_gbs", "bound": "hbm"}
+        if extra:
+            line.update(extra)
+        out.append(line)
+        print(json.dumps(line), flush=True)
+
+    want = lambda n: (not args.only) or any(k in n for k in args.only.split(","))  # noqa: E731
+
+    # ---- RMSNorm (x: 8192 x 4096) ----
+    if want("rmsnorm"):
+        x = torch.randn(BT, H, device=dev, generator=g).to(bf)
+        w = (torch.rand(H, device=dev, generator=g) + 0.5).to(bf)
+        y = torch.empty_like(x)
+        rstd = torch.empty(BT, device=dev)
+        dy = torch.randn(BT, H, device=dev, generator=g).to(bf)
+        dx = torch.empty_like(x)
+        dw = torch.empty_like(w)
+        ws = torch.empty(L.lk_rmsnorm_bwd_workspace_bytes(BT, H), dtype=torch.uint8, device=dev)
+        f = lambda: _capi.check(L.lk_rmsnorm_fwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), rstd.data_ptr(), BT, H,  # noqa: E731
+                                                 1e-6, 0.0, 0, 1, st()))
+        b = lambda: _capi.check(L.lk_rmsnorm_bwd(dy.data_ptr(), x.data_ptr(), w.data_ptr(), rstd.data_ptr(),  # noqa: E731
+                                                 dx.data_ptr(), dw.data_ptr(), BT, H, 0.0, 0, 1, ws.data_ptr(),
+                                                 ws.numel(), st()))
+        report("rmsnorm_fwd", 2 * BT * H * 2 + H * 2 + BT * 4, timed(f, args.reps, flush))
+        report("rmsnorm_bwd", 3 * BT * H * 2 + H * 2 * 2 + BT * 4, timed(b, args.reps, flush))
+        del x, y, dy, dx
+
+    # ---- RoPE (q: 4 x 2048 x 32 x 128, k: 4 x 2048 x 8 x 128) ----
+    if want("rope"):
+        B, T = 4, 2048
+        q = torch.randn(B, T, NQ, D, device=dev, generator=g).to(bf)
+        k = torch.randn(B, T, NK, D, device=dev, generator=g).to(bf)
+        cos = torch.randn(1, T, D, device=dev, generator=g).to(bf)
+        sin = torch.randn(1, T, D, device=dev, generator=g).to(bf)
+        for bwd in (0, 1):
+            f = lambda: _capi.check(L.lk_rope(q.data_ptr(), k.data_ptr(), cos.data_ptr(), sin.data_ptr(), B, T, NQ,  # noqa: E731
+                                              NK, D, 1, 1, 1, bwd, st()))
+            nbytes = 2 * (q.numel() + k.numel()) * 2 + 2 * T * (D // 2) * 2
+            report("rope_bwd" if bwd else "rope_fwd", nbytes, timed(f, args.reps, flush))
+        del q, k
+
+    # ---- SwiGLU / GeGLU (8192 x 14336) ----
+    for kind in ("swiglu", "geglu"):
+        if not want(kind):
+            continue
+        a = torch.randn(BT, I, device=dev, generator=g).to(bf)
+        b_ = torch.randn(BT, I, device=dev, generator=g).to(bf)
+        c = torch.empty_like(a)
+        dc = torch.randn(BT, I, device=dev, generator=g).to(bf)
+        n = a.numel()
+        ffn, bfn = getattr(L, f"lk_{kind}_fwd"), getattr(L, f"lk_{kind}_bwd")
+        f = lambda: _capi.check(ffn(a.data_ptr(), b_.data_ptr(), c.data_ptr(), n, 1, st()))  # noqa: E731
+        report(f"{kind}_fwd", 3 * n * 2, timed(f, args.reps, flush))
+        bb = lambda: _capi.check(bfn(dc.data_ptr(), a.data_ptr(), b_.data_ptr(), n, 1, st()))  # noqa: E731
+        report(f"{kind}_bwd", 5 * n * 2, timed(bb, args.reps, flush))
+        del a, b_, c, dc
+
+    # ---- standalone cross entropy (8192 x 128256 bf16, in place) ----
+    if want("cross_entropy"):
+        rows = BT
+        x = torch.randn(rows, V, device=dev, generator=g).to(bf)
+        t = torch.randint(0, V, (rows,), device=dev, generator=g)
+        lr = torch.empty(rows, device=dev)
+        ls = torch.empty((), device=dev)
+        ws = torch.empty(256, dtype=torch.uint8, device=dev)
+        f = lambda: _capi.check(L.lk_cross_entropy_fwd(x.data_ptr(), V, t.data_ptr(), rows, V, 1, -100, 0.0, 0.0,  # noqa: E731
+                                                       0.0, 1, 1, lr.data_ptr(), ls.data_ptr(), None, None,
+                                                       ws.data_ptr(), ws.numel(), st()))
+        ms = timed(f, args.reps, flush)
+        report("cross_entropy_fwd_bwd", 2 * rows * V * 2, ms,
+               {"note": "algorithmic bytes = 1 read + 1 write of the logits (the in-place minimum)"})
+    print(json.dumps({"summary": {o["kernel"]: round(o["frac"], 3) for o in out}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -38,18 +38,35 @@ bool tma_ok(const TmaOperand& op) {
          op.inner >= 1 && op.outer >= 1;
 }
 
-int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box) {
+static bool g_allow_3d = true;  // cleared if the driver rejects the 3D MN-major map
+
+int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box, int* mode) {
   auto enc = get_encode();
   LK_REQUIRE(enc != nullptr, LK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+  const CUtensorMapDataType dt =
+      dtype == LK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+  cuuint32_t es[3] = {1u, 1u, 1u};
+  if (op.mn_major && g_allow_3d && op.inner % 64 == 0) {
+    // [K rows][MN] viewed as {64 (MN within atom), K, MN/64 atoms}: one box {64, 64, atoms}
+    // lands as `atoms` contiguous 8 KB SWIZZLE_128B atoms, the UMMA MN-major canonical layout.
+    cuuint64_t dims[3] = {64u, (cuuint64_t)op.outer, (cuuint64_t)(op.inner / 64)};
+    cuuint64_t strides[2] = {(cuuint64_t)op.row_elems * 2, 128u};
+    cuuint32_t box[3] = {64u, 64u, (cuuint32_t)(rows_in_box / 64)};
+    CUresult r = enc(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      *mode = 1;
+      return LK_OK;
+    }
+    g_allow_3d = false;
+  }
   cuuint64_t dims[2] = {(cuuint64_t)op.inner, (cuuint64_t)op.outer};
   cuuint64_t strides[1] = {(cuuint64_t)op.row_elems * 2};
   cuuint32_t box[2] = {64u, (cuuint32_t)(op.mn_major ? 64 : rows_in_box)};
-  cuuint32_t es[2] = {1u, 1u};
-  CUresult r = enc(map, dtype == LK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2,
-                   const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = enc(map, dt, 2, const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   LK_REQUIRE(r == CUDA_SUCCESS, LK_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  *mode = op.mn_major ? 2 : 0;
   return LK_OK;
 }
 
@@ -67,14 +84,12 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     P.tiles_m = (int)((P.M + BM - 1) / BM);
     P.tiles_n = (int)((P.N + BN - 1) / BN);
     P.k_blocks = (int)((P.K + BK - 1) / BK);
-    P.a_mn = a[p].mn_major;
-    P.b_mn = b[p].mn_major;
-    int rc = encode_operand(&maps[2 * p], a[p], dtype, BM);
+    int rc = encode_operand(&maps[2 * p], a[p], dtype, BM, &P.a_mode);
     if (rc) return rc;
-    rc = encode_operand(&maps[2 * p + 1], b[p], dtype, BN);
+    rc = encode_operand(&maps[2 * p + 1], b[p], dtype, BN, &P.b_mode);
     if (rc) return rc;
     args.prob[p] = P;
-    args.idesc[p] = make_idesc(dtype, P.a_mn, P.b_mn);
+    args.idesc[p] = make_idesc(dtype, a[p].mn_major, b[p].mn_major);
     if (p == 0) args.tiles0 = P.tiles_m * P.tiles_n;
     total += P.tiles_m * P.tiles_n;
   }

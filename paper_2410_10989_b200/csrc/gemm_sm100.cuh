@@ -38,7 +38,9 @@ constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + AUX_BYTES + 1024;  // + alignm
 struct Problem {
   int64_t M, N, K;
   int tiles_m, tiles_n, k_blocks;
-  int a_mn, b_mn;       // 1 = MN-major operand
+  // operand load mode: 0 = K-major (one 2D box), 1 = MN-major via one 3D box
+  // {64, 64 K, atoms}, 2 = MN-major via one 2D box per 64-wide atom
+  int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
   EpiArgs epi;
 };
@@ -85,6 +87,45 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
       ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
       : "memory");
+}
+__device__ __forceinline__ void mbar_wait_addr(uint32_t a, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_expect_tx_addr(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_2d(uint64_t map, uint32_t bar, uint32_t dst, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y)
+      : "memory");
+}
+__device__ __forceinline__ void tma_3d(uint64_t map, uint32_t bar, uint32_t dst, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+      ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "elect.sync _|P1, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P1;\n\t}"
+      : "=r"(pred));
+  return pred;
+}
+__device__ __forceinline__ void umma_commit_addr(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -357,83 +398,102 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // ===================== TMA producer =====================
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int it = 0;; ++it) {
-        const int slot = it % SCHED;
+    // ===================== TMA producer (warp-converged, one elected issuer) =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB), full0 = smem_u32(full), empty0 = smem_u32(empty);
+    for (int it = 0;; ++it) {
+      const int slot = it % SCHED;
+      int tile = 0;
+      if (lane == 0) {
         mbar_wait(&sempty[slot], ((it / SCHED) & 1) ^ 1);
-        int tile = atomicAdd(args.counter, 1);
+        tile = atomicAdd(args.counter, 1);
         if (tile >= args.total_tiles) tile = -1;
         stile[slot] = tile;
         mbar_arrive(&sfull[slot]);
-        if (tile < 0) break;
-        const TileCoord tcd = decode_tile(args, tile);
-        const Problem& P = args.prob[tcd.p];
-        const CUtensorMap* ma = tcd.p ? &ma1 : &ma0;
-        const CUtensorMap* mb = tcd.p ? &mb1 : &mb0;
-        const int m0 = tcd.m_blk * BM, n0 = tcd.n_blk * BN;
-        for (int kb = 0; kb < P.k_blocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          uint8_t* a_dst = sA + stage * A_BYTES;
-          uint8_t* b_dst = sB + stage * B_BYTES;
+      }
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      if (tile < 0) break;
+      const TileCoord tcd = decode_tile(args, tile);
+      const int p = tcd.p;
+      const int a_mode = p ? args.prob[1].a_mode : args.prob[0].a_mode;
+      const int b_mode = p ? args.prob[1].b_mode : args.prob[0].b_mode;
+      const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
+      const uint64_t ma = reinterpret_cast<uint64_t>(p ? &ma1 : &ma0);
+      const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
+      const int m0 = tcd.m_blk * BM, n0 = tcd.n_blk * BN;
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
+        if (elect_one()) {
+          const uint32_t fb = full0 + stage * 8;
+          mbar_expect_tx_addr(fb, STAGE_BYTES);
+          const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
           const int k0 = kb * BK;
-          if (P.a_mn) {
-            tma_load_2d(ma, &full[stage], a_dst, m0, k0);
-            tma_load_2d(ma, &full[stage], a_dst + 8192, m0 + 64, k0);
+          // mode 0: K-major 2D {64 K, rows}; 1: MN-major 3D {64, 64 K, atoms}; 2: MN-major 2D per atom
+          if (a_mode == 0) {
+            tma_2d(ma, fb, a_dst, k0, m0);
+          } else if (a_mode == 1) {
+            tma_3d(ma, fb, a_dst, 0, k0, m0 >> 6);
           } else {
-            tma_load_2d(ma, &full[stage], a_dst, k0, m0);
+            tma_2d(ma, fb, a_dst, m0, k0);
+            tma_2d(ma, fb, a_dst + 8192, m0 + 64, k0);
           }
-          if (P.b_mn) {
+          if (b_mode == 0) {
+            tma_2d(mb, fb, b_dst, k0, n0);
+          } else if (b_mode == 1) {
+            tma_3d(mb, fb, b_dst, 0, k0, n0 >> 6);
+          } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) tma_load_2d(mb, &full[stage], b_dst + j * 8192, n0 + 64 * j, k0);
-          } else {
-            tma_load_2d(mb, &full[stage], b_dst, k0, n0);
+            for (int j = 0; j < 4; ++j) tma_2d(mb, fb, b_dst + j * 8192, n0 + 64 * j, k0);
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===================== MMA issuer =====================
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int it = 0;; ++it) {
-        const int slot = it % SCHED;
-        mbar_wait(&sfull[slot], (it / SCHED) & 1);
-        const int tile = stile[slot];
-        mbar_arrive(&sempty[slot]);
-        if (tile < 0) break;
-        const TileCoord tcd = decode_tile(args, tile);
-        const Problem& P = args.prob[tcd.p];
-        const uint32_t idesc = args.idesc[tcd.p];
-        const int buf = it & 1;
-        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+    // ===================== MMA issuer (warp-converged, one elected issuer) =====================
+    int stage = 0;
+    uint32_t phase = 0;
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB), full0 = smem_u32(full), empty0 = smem_u32(empty);
+    for (int it = 0;; ++it) {
+      const int slot = it % SCHED;
+      mbar_wait(&sfull[slot], (it / SCHED) & 1);
+      const int tile = stile[slot];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&sempty[slot]);
+      if (tile < 0) break;
+      const TileCoord tcd = decode_tile(args, tile);
+      const int p = tcd.p;
+      const int a_mn = (p ? args.prob[1].a_mode : args.prob[0].a_mode) != 0;
+      const int b_mn = (p ? args.prob[1].b_mode : args.prob[0].b_mode) != 0;
+      const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
+      const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];
+      const int buf = it & 1;
+      mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + buf * BN;
+      // descriptors of stage 0 / k 0; stage and K advances only touch the start-address field
+      const uint64_t a_desc0 = make_desc(sA0, a_mn ? 8192u : 16u, 1024u);
+      const uint64_t b_desc0 = make_desc(sB0, b_mn ? 8192u : 16u, 1024u);
+      const uint32_t a_k16 = a_mn ? (2048u >> 4) : (32u >> 4);   // per UMMA_K=16 step
+      const uint32_t b_k16 = b_mn ? (2048u >> 4) : (32u >> 4);
+      for (int kb = 0; kb < kblocks; ++kb) {
+        mbar_wait_addr(full0 + stage * 8, phase);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * BN;
-        // per-UMMA_K (16 elements) start-address advance inside a 64-wide K block
-        const uint32_t a_kstep = P.a_mn ? 2048u : 32u;
-        const uint32_t b_kstep = P.b_mn ? 2048u : 32u;
-        const uint32_t a_lbo = P.a_mn ? 8192u : 16u, b_lbo = P.b_mn ? 8192u : 16u;
-        for (int kb = 0; kb < P.k_blocks; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+        if (elect_one()) {
+          const uint64_t ad = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t bd = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            const uint64_t ad = make_desc(a_addr + k * a_kstep, a_lbo, 1024u);
-            const uint64_t bd = make_desc(b_addr + k * b_kstep, b_lbo, 1024u);
-            umma_f16(d_tmem, ad, bd, idesc, (kb | k) != 0 ? 1u : 0u);
-          }
-          umma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          for (int k = 0; k < BK / 16; ++k)
+            umma_f16(d_tmem, ad + k * a_k16, bd + k * b_k16, idesc, (kb | k) != 0 ? 1u : 0u);
+          umma_commit_addr(empty0 + stage * 8);
         }
-        umma_commit(&tfull[buf]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (elect_one()) umma_commit(&tfull[buf]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
@@ -493,7 +553,8 @@ struct TmaOperand {
   int mn_major;          // 0: inner dim is K; 1: inner dim is M/N
 };
 
-int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box);
+// Encodes the operand's tensor map and returns its load mode (0/1/2, see Problem).
+int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_in_box, int* mode);
 bool tma_ok(const TmaOperand& op);
 
 // Launch one or two problems in a single persistent launch.

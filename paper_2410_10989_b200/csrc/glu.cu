@@ -17,7 +17,8 @@ constexpr float kGelu3A = 0.134145f;           // 3 * 0.044715 rowfuse/ops.py:39
 template <bool ACC>
 __device__ __forceinline__ float tanh_sel(float x) { return ACC ? tanhf(x) : tanh_fast(x); }
 
-__device__ __forceinline__ float sigmoidf_(float z) { return 1.f / (1.f + __expf(-z)); }
+// 1 / (1 + e^-z) with the MUFU reciprocal; e^-z -> inf for z << 0 gives exactly 0.
+__device__ __forceinline__ float sigmoidf_(float z) { return __frcp_rn(1.f + __expf(-z)); }
 
 template <typename T, int ACT>
 struct Glu {

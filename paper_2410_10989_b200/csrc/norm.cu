@@ -3,67 +3,69 @@
 // Forward (rowfuse/ops.py:190-214; Liger casting modes LK/ops/rms_norm.py:45-112):
 //   y = x * rstd * (offset + w), rstd = 1/sqrt(mean(x^2) + eps), one rstd per row cached.
 // Backward (rowfuse/ops.py:217-241; LK/ops/rms_norm.py:115-210):
-//   dx = rstd * (m - (rstd^2 / n) * (m . x) * x),  m = dy * (offset + w)
+//   dx = rstd * m - (rstd^3 / n) * (m . x) * x,  m = dy * (offset + w)
 //   dw = sum_rows dy * xhat  -- two-stage: one fp32 partial row per CTA, then a
 //   fixed-order column sum.  The combine order depends only on the row count and
 //   the grid, so the result is bitwise reproducible (the property rowfuse gets from
 //   _tree_sum, ops.py:138-152).
 //
-// One CTA per row in the forward (the row lives in registers between the
-// reduction and the write: one read, one write).  The backward is persistent:
-// grid = a multiple of the SM count, contiguous row ranges per CTA.
+// Register path (16-byte aligned rows, cols <= 4 x 512 vectors): the row lives in
+// registers between the reduction and the write, so the forward is one read + one
+// write and the backward two reads + one write.  Streaming path (any other shape):
+// the row is re-read from L1/L2 for the second pass.  The backward is persistent:
+// grid = 2 x SMs CTAs, contiguous row ranges per CTA.
 #include "common.cuh"
 
 namespace lk {
 
-template <typename T, bool VEC, int KV>
-struct RowIO {
-  static constexpr int NV = VEC ? Vec16<T>::N : 1;
-  // column of element e of vector slot k for thread tid
-  static __device__ __forceinline__ int64_t col(int k, int e, int tid, int bs) {
-    return ((int64_t)k * bs + tid) * NV + e;
-  }
+constexpr int NORM_MAX_THREADS = 512;
+
+template <typename T, int KV>
+struct RowRegs {
+  static constexpr int NV = Vec16<T>::N;
+  static __device__ __forceinline__ int64_t col(int k, int tid, int bs) { return ((int64_t)k * bs + tid) * NV; }
   static __device__ __forceinline__ void load(const T* p, int64_t cols, float (&v)[KV][NV], int tid, int bs) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
-      int64_t c0 = col(k, 0, tid, bs);
-      if (VEC) {
-        if (c0 < cols) {
-          Vec16<T> t;
-          t.load(p + c0);
+      const int64_t c0 = col(k, tid, bs);
+      if (c0 < cols) {
+        Vec16<T> t;
+        t.load(p + c0);
 #pragma unroll
-          for (int e = 0; e < NV; ++e) v[k][e] = t.v[e];
-        } else {
-#pragma unroll
-          for (int e = 0; e < NV; ++e) v[k][e] = 0.f;
-        }
+        for (int e = 0; e < NV; ++e) v[k][e] = t.v[e];
       } else {
-        v[k][0] = c0 < cols ? to_f<T>(p[c0]) : 0.f;
+#pragma unroll
+        for (int e = 0; e < NV; ++e) v[k][e] = 0.f;
       }
     }
   }
   static __device__ __forceinline__ void store(T* p, int64_t cols, const float (&v)[KV][NV], int tid, int bs) {
 #pragma unroll
     for (int k = 0; k < KV; ++k) {
-      int64_t c0 = col(k, 0, tid, bs);
-      if (c0 >= cols) continue;
-      if (VEC) {
+      const int64_t c0 = col(k, tid, bs);
+      if (c0 < cols) {
         Vec16<T> t;
 #pragma unroll
         for (int e = 0; e < NV; ++e) t.v[e] = v[k][e];
         t.store(p + c0);
-      } else {
-        p[c0] = from_f<T>(v[k][0]);
       }
     }
   }
 };
 
-template <typename T, typename R, bool VEC, int KV>
-__global__ void rmsnorm_fwd_kernel(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y,
-                                   R* __restrict__ rstd, int64_t rows, int64_t cols, float eps,
-                                   float offset, int mode) {
-  using IO = RowIO<T, VEC, KV>;
+template <typename T>
+__device__ __forceinline__ float fwd_val(float x, float r, float w, bool has_w, float offset, int mode) {
+  float xh = x * r;
+  if (mode != LK_CAST_GEMMA) xh = round_to<T>(xh);  // llama: cast xhat to x dtype before *w
+  return has_w ? xh * (offset + w) : xh;
+}
+
+// ------------------------------------------------------------ register path
+template <typename T, typename R, int KV>
+__global__ void __launch_bounds__(NORM_MAX_THREADS)
+rmsnorm_fwd_reg(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y, R* __restrict__ rstd,
+                int64_t rows, int64_t cols, float eps, float offset, int mode) {
+  using IO = RowRegs<T, KV>;
   constexpr int NV = IO::NV;
   __shared__ float scratch[32];
   const int tid = threadIdx.x, bs = blockDim.x;
@@ -78,82 +80,135 @@ __global__ void rmsnorm_fwd_kernel(const T* __restrict__ x, const T* __restrict_
     ss = block_sum(ss, scratch);
     const float r = rsqrtf(ss / (float)cols + eps);
     if (tid == 0) rstd[row] = from_f<R>(r);
-    float wv[KV][NV];
-    if (w) IO::load(w, cols, wv, tid, bs);
+    if (w) {
+      float wv[KV][NV];
+      IO::load(w, cols, wv, tid, bs);
 #pragma unroll
-    for (int k = 0; k < KV; ++k)
+      for (int k = 0; k < KV; ++k)
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {
-        float xh = v[k][e] * r;
-        if (mode != LK_CAST_GEMMA) xh = round_to<T>(xh);  // llama: cast xhat before *w
-        v[k][e] = w ? xh * (offset + wv[k][e]) : xh;
-      }
+        for (int e = 0; e < NV; ++e) v[k][e] = fwd_val<T>(v[k][e], r, wv[k][e], true, offset, mode);
+    } else {
+#pragma unroll
+      for (int k = 0; k < KV; ++k)
+#pragma unroll
+        for (int e = 0; e < NV; ++e) v[k][e] = fwd_val<T>(v[k][e], r, 0.f, false, offset, mode);
+    }
     IO::store(y + row * cols, cols, v, tid, bs);
   }
 }
 
-template <typename T, typename R, bool VEC, int KV>
-__global__ void rmsnorm_bwd_kernel(const T* dy, const T* __restrict__ x,
-                                   const T* __restrict__ w, const R* __restrict__ rstd, T* dx,
-                                   float* __restrict__ dw_part, int64_t rows, int64_t cols,
-                                   float offset, int mode) {
-  using IO = RowIO<T, VEC, KV>;
+template <typename T, typename R, int KV>
+__global__ void __launch_bounds__(NORM_MAX_THREADS)
+rmsnorm_bwd_reg(const T* dy, const T* __restrict__ x, const T* __restrict__ w, const R* __restrict__ rstd, T* dx,
+                float* __restrict__ dw_part, int64_t rows, int64_t cols, float offset, int mode) {
+  using IO = RowRegs<T, KV>;
   constexpr int NV = IO::NV;
   __shared__ float scratch[32];
   const int tid = threadIdx.x, bs = blockDim.x;
   const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
   const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  float wv[KV][NV];
   float acc[KV][NV];
 #pragma unroll
   for (int k = 0; k < KV; ++k)
 #pragma unroll
     for (int e = 0; e < NV; ++e) acc[k][e] = 0.f;
-  if (w) {
-    IO::load(w, cols, wv, tid, bs);
-#pragma unroll
-    for (int k = 0; k < KV; ++k)
-#pragma unroll
-      for (int e = 0; e < NV; ++e) wv[k][e] += offset;
-  }
   for (int64_t row = r0; row < r1; ++row) {
     float g[KV][NV], xv[KV][NV];
     IO::load(dy + row * cols, cols, g, tid, bs);
     IO::load(x + row * cols, cols, xv, tid, bs);
     const float r = to_f<R>(rstd[row]);
     float dot = 0.f;
-    float m[KV][NV];
 #pragma unroll
-    for (int k = 0; k < KV; ++k)
+    for (int k = 0; k < KV; ++k) {
+      Vec16<T> wt;
+      const int64_t c0 = IO::col(k, tid, bs);
+      if (w && c0 < cols) wt.load(w + c0);
 #pragma unroll
       for (int e = 0; e < NV; ++e) {
-        float mm = w ? g[k][e] * wv[k][e] : g[k][e];
+        float mm = w ? g[k][e] * (offset + (c0 < cols ? wt.v[e] : 0.f)) : g[k][e];
         if (mode == LK_CAST_LLAMA) mm = round_to<T>(mm);  // (dY * W) in x dtype, then fp32
-        m[k][e] = mm;
         dot += mm * xv[k][e];
+        float xh = xv[k][e] * r;
+        if (mode == LK_CAST_LLAMA) xh = round_to<T>(xh);
+        acc[k][e] += g[k][e] * xh;
+        g[k][e] = mm;  // g now holds m
       }
+    }
     dot = block_sum(dot, scratch);
     const float c = r * r * r * dot / (float)cols;
 #pragma unroll
     for (int k = 0; k < KV; ++k)
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {
-        float xh = xv[k][e] * r;
-        if (mode == LK_CAST_LLAMA) xh = round_to<T>(xh);
-        acc[k][e] += g[k][e] * xh;
-        m[k][e] = r * m[k][e] - c * xv[k][e];
-      }
-    IO::store(dx + row * cols, cols, m, tid, bs);
+      for (int e = 0; e < NV; ++e) g[k][e] = r * g[k][e] - c * xv[k][e];
+    IO::store(dx + row * cols, cols, g, tid, bs);
   }
   if (dw_part) {
     float* p = dw_part + (int64_t)blockIdx.x * cols;
 #pragma unroll
-    for (int k = 0; k < KV; ++k)
+    for (int k = 0; k < KV; ++k) {
+      const int64_t c0 = IO::col(k, tid, bs);
+      if (c0 < cols) {
 #pragma unroll
-      for (int e = 0; e < NV; ++e) {
-        int64_t cidx = IO::col(k, e, tid, bs);
-        if (cidx < cols) p[cidx] = acc[k][e];
+        for (int e = 0; e < NV; e += 4)
+          *reinterpret_cast<float4*>(p + c0 + e) = make_float4(acc[k][e], acc[k][e + 1], acc[k][e + 2], acc[k][e + 3]);
       }
+    }
+  }
+}
+
+// ----------------------------------------------------------- streaming path
+template <typename T, typename R>
+__global__ void __launch_bounds__(256)
+rmsnorm_fwd_stream(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y, R* __restrict__ rstd,
+                   int64_t rows, int64_t cols, float eps, float offset, int mode) {
+  __shared__ float scratch[32];
+  for (int64_t row = blockIdx.x; row < rows; row += gridDim.x) {
+    const T* xr = x + row * cols;
+    float ss = 0.f;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      float v = to_f<T>(xr[c]);
+      ss += v * v;
+    }
+    ss = block_sum(ss, scratch);
+    const float r = rsqrtf(ss / (float)cols + eps);
+    if (threadIdx.x == 0) rstd[row] = from_f<R>(r);
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
+      y[row * cols + c] = from_f<T>(fwd_val<T>(to_f<T>(xr[c]), r, w ? to_f<T>(w[c]) : 0.f, w != nullptr, offset, mode));
+  }
+}
+
+template <typename T, typename R>
+__global__ void __launch_bounds__(256)
+rmsnorm_bwd_stream(const T* dy, const T* __restrict__ x, const T* __restrict__ w, const R* __restrict__ rstd, T* dx,
+                   float* __restrict__ dw_part, int64_t rows, int64_t cols, float offset, int mode) {
+  __shared__ float scratch[32];
+  const int64_t per = (rows + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float* p = dw_part ? dw_part + (int64_t)blockIdx.x * cols : nullptr;
+  if (p)
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) p[c] = 0.f;
+  auto mval = [&](float g, int64_t c) {
+    float mm = w ? g * (offset + to_f<T>(w[c])) : g;
+    return mode == LK_CAST_LLAMA ? round_to<T>(mm) : mm;
+  };
+  for (int64_t row = r0; row < r1; ++row) {
+    const T* gr = dy + row * cols;
+    const T* xr = x + row * cols;
+    const float r = to_f<R>(rstd[row]);
+    float dot = 0.f;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) dot += mval(to_f<T>(gr[c]), c) * to_f<T>(xr[c]);
+    dot = block_sum(dot, scratch);
+    const float cc = r * r * r * dot / (float)cols;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float g = to_f<T>(gr[c]), xv = to_f<T>(xr[c]);
+      if (p) {
+        float xh = xv * r;
+        if (mode == LK_CAST_LLAMA) xh = round_to<T>(xh);
+        p[c] += g * xh;
+      }
+      dx[row * cols + c] = from_f<T>(r * mval(g, c) - cc * xv);
+    }
+    __syncthreads();  // dx may alias dy: finish the row before the next row's reduction
   }
 }
 
@@ -169,34 +224,61 @@ __global__ void colsum_partials_kernel(const float* __restrict__ part, int64_t g
 }
 
 struct NormCfg {
-  bool vec;
+  bool reg;
   int kv;
   int block;
 };
 
 template <typename T>
-static NormCfg pick_cfg(int64_t cols, const void* p0, const void* p1, const void* p2) {
+static NormCfg pick_cfg(int64_t cols, std::initializer_list<const void*> ptrs) {
   constexpr int NV = Vec16<T>::N;
   bool vec = (cols % NV == 0);
-  for (const void* p : {p0, p1, p2})
+  for (const void* p : ptrs)
     if (p && (reinterpret_cast<uintptr_t>(p) & 15)) vec = false;
-  int64_t units = vec ? cols / NV : cols;
+  const int64_t units = cols / NV;
+  if (!vec || units > 4 * NORM_MAX_THREADS) return {false, 0, 256};
   int kv = 1;
-  while (kv < 8 && (units + kv - 1) / kv > 256) kv *= 2;
+  while (kv < 4 && (units + kv - 1) / kv > 256) kv *= 2;
   int64_t block = (units + kv - 1) / kv;
-  block = std::min<int64_t>(1024, std::max<int64_t>(32, (block + 31) / 32 * 32));
-  return {vec, kv, (int)block};
+  block = std::min<int64_t>(NORM_MAX_THREADS, std::max<int64_t>(32, (block + 31) / 32 * 32));
+  return {true, kv, (int)block};
 }
 
-#define LK_KV_DISPATCH(kv, KV, ...)                  \
-  switch (kv) {                                      \
-    case 1: { constexpr int KV = 1; __VA_ARGS__; break; } \
-    case 2: { constexpr int KV = 2; __VA_ARGS__; break; } \
-    case 4: { constexpr int KV = 4; __VA_ARGS__; break; } \
-    default: { constexpr int KV = 8; __VA_ARGS__; break; } \
+#define LK_KV_DISPATCH(kv, KV, ...)                            \
+  switch (kv) {                                                \
+    case 1: { constexpr int KV = 1; __VA_ARGS__; break; }      \
+    case 2: { constexpr int KV = 2; __VA_ARGS__; break; }      \
+    default: { constexpr int KV = 4; __VA_ARGS__; break; }     \
   }
 
-static int64_t max_cols_for(NormCfg c, int nv) { return (int64_t)c.block * c.kv * (c.vec ? nv : 1); }
+template <typename T, typename R>
+static int rms_fwd_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
+                          float offset, int mode, cudaStream_t st) {
+  NormCfg c = pick_cfg<T>(cols, {x, w, y});
+  unsigned grid = (unsigned)std::min<int64_t>(rows, 1 << 20);
+  if (c.reg) {
+    LK_KV_DISPATCH(c.kv, KV, { rmsnorm_fwd_reg<T, R, KV><<<grid, c.block, 0, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode); });
+  } else {
+    rmsnorm_fwd_stream<T, R><<<grid, 256, 0, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode);
+  }
+  return check_launch("rmsnorm_fwd");
+}
+
+static int64_t rms_bwd_grid(int64_t rows) {
+  return std::max<int64_t>(1, std::min<int64_t>(rows, 2 * (int64_t)sm_count()));
+}
+
+template <typename T, typename R>
+static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
+                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st) {
+  NormCfg c = pick_cfg<T>(cols, {dy, x, w, dx});
+  if (c.reg) {
+    LK_KV_DISPATCH(c.kv, KV, { rmsnorm_bwd_reg<T, R, KV><<<(unsigned)g, c.block, 0, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode); });
+  } else {
+    rmsnorm_bwd_stream<T, R><<<(unsigned)g, 256, 0, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode);
+  }
+  return check_launch("rmsnorm_bwd");
+}
 
 }  // namespace lk
 
@@ -210,28 +292,15 @@ extern "C" int lk_rmsnorm_fwd(const void* x, const void* weight, void* y, void* 
   LK_REQUIRE(x && y && rstd, LK_INVALID_ARGUMENT, "null pointer");
   LK_REQUIRE(casting_mode >= 0 && casting_mode <= 2, LK_INVALID_ARGUMENT, "bad casting mode");
   cudaStream_t st = as_stream(stream);
-  unsigned grid = (unsigned)std::min<int64_t>(rows, 1 << 20);
   LK_DISPATCH_FLOAT(dtype, T, {
-    NormCfg c = pick_cfg<T>(cols, x, y, weight);
-    LK_REQUIRE(cols <= max_cols_for(c, Vec16<T>::N), LK_SIZE_MISMATCH, "feature dim too large");
     const T* w = static_cast<const T*>(weight);
-    if (casting_mode == LK_CAST_NONE) {
-      LK_KV_DISPATCH(c.kv, KV, {
-        if (c.vec) rmsnorm_fwd_kernel<T, T, true, KV><<<grid, c.block, 0, st>>>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<T*>(rstd), rows, cols, eps, offset, casting_mode);
-        else rmsnorm_fwd_kernel<T, T, false, KV><<<grid, c.block, 0, st>>>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<T*>(rstd), rows, cols, eps, offset, casting_mode);
-      });
-    } else {
-      LK_KV_DISPATCH(c.kv, KV, {
-        if (c.vec) rmsnorm_fwd_kernel<T, float, true, KV><<<grid, c.block, 0, st>>>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<float*>(rstd), rows, cols, eps, offset, casting_mode);
-        else rmsnorm_fwd_kernel<T, float, false, KV><<<grid, c.block, 0, st>>>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<float*>(rstd), rows, cols, eps, offset, casting_mode);
-      });
-    }
+    if (casting_mode == LK_CAST_NONE)
+      return rms_fwd_launch<T, T>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<T*>(rstd), rows,
+                                  cols, eps, offset, casting_mode, st);
+    return rms_fwd_launch<T, float>(static_cast<const T*>(x), w, static_cast<T*>(y), static_cast<float*>(rstd),
+                                    rows, cols, eps, offset, casting_mode, st);
   });
-  return check_launch("rmsnorm_fwd_kernel");
-}
-
-static int64_t rms_bwd_grid(int64_t rows) {
-  return std::max<int64_t>(1, std::min<int64_t>(rows, 2 * (int64_t)sm_count()));
+  return LK_OK;
 }
 
 extern "C" size_t lk_rmsnorm_bwd_workspace_bytes(int64_t rows, int64_t cols) {
@@ -251,34 +320,25 @@ extern "C" int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight,
     LK_REQUIRE(workspace && workspace_bytes >= (size_t)g * cols * sizeof(float), LK_INVALID_ARGUMENT,
                "workspace too small");
     part = static_cast<float*>(workspace);
-  }
-  if (rows == 0) {
-    if (part) LK_CUDA(cudaMemsetAsync(part, 0, (size_t)g * cols * sizeof(float), st));
+    if (rows == 0) LK_CUDA(cudaMemsetAsync(part, 0, (size_t)g * cols * sizeof(float), st));
   }
   LK_REQUIRE(rows == 0 || (dy && x && rstd && dx), LK_INVALID_ARGUMENT, "null pointer");
   LK_DISPATCH_FLOAT(dtype, T, {
+    const T* w = static_cast<const T*>(weight);
     if (rows > 0) {
-      NormCfg c = pick_cfg<T>(cols, dy, x, dx);
-      if (weight && (reinterpret_cast<uintptr_t>(weight) & 15)) c.vec = false;
-      LK_REQUIRE(cols <= max_cols_for(c, Vec16<T>::N), LK_SIZE_MISMATCH, "feature dim too large");
-      const T* w = static_cast<const T*>(weight);
-      if (casting_mode == LK_CAST_NONE) {
-        LK_KV_DISPATCH(c.kv, KV, {
-          if (c.vec) rmsnorm_bwd_kernel<T, T, true, KV><<<(unsigned)g, c.block, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x), w, static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols, offset, casting_mode);
-          else rmsnorm_bwd_kernel<T, T, false, KV><<<(unsigned)g, c.block, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x), w, static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols, offset, casting_mode);
-        });
-      } else {
-        LK_KV_DISPATCH(c.kv, KV, {
-          if (c.vec) rmsnorm_bwd_kernel<T, float, true, KV><<<(unsigned)g, c.block, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x), w, static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows, cols, offset, casting_mode);
-          else rmsnorm_bwd_kernel<T, float, false, KV><<<(unsigned)g, c.block, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x), w, static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows, cols, offset, casting_mode);
-        });
-      }
-      int rc = check_launch("rmsnorm_bwd_kernel");
+      int rc = casting_mode == LK_CAST_NONE
+                   ? rms_bwd_launch<T, T>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
+                                          static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols,
+                                          offset, casting_mode, g, st)
+                   : rms_bwd_launch<T, float>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
+                                              static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows,
+                                              cols, offset, casting_mode, g, st);
       if (rc) return rc;
     }
     if (part) {
       colsum_partials_kernel<T><<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(part, g, cols, static_cast<T*>(dw));
+      return check_launch("colsum_partials_kernel");
     }
   });
-  return check_launch("colsum_partials_kernel");
+  return LK_OK;
 }

@@ -78,9 +78,9 @@ def test_ce_large_vocab_bf16_rows_sum_to_zero():
     g = torch.Generator(device="cuda").manual_seed(1)
     x = (torch.randn(rows, v, device="cuda", generator=g) * 2).to(torch.bfloat16).requires_grad_(True)
     t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    ref = torch.nn.functional.cross_entropy(x.detach().float(), t, reduction="sum")  # before: CE is in place
     loss = lk.LigerCrossEntropyLoss(reduction="sum")(x, t)
     loss.backward()
-    ref = torch.nn.functional.cross_entropy(x.detach().float(), t, reduction="sum")
     assert loss.item() == pytest.approx(ref.item(), rel=2e-2)
     rs = x.grad.float().sum(dim=1)
     assert rs.abs().max().item() < 5e-2  # bf16 rounding of ~1e5 entries per row

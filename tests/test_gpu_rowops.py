@@ -103,7 +103,9 @@ def test_rope_llama3_gqa_fwd_bwd(dtype):
     # backward is the inverse rotation: grad of sum(qo * u) wrt q = R^T u
     u = torch.randn_like(qo)
     v = torch.randn_like(ko)
+    u0, v0 = u.clone(), v.clone()  # the backward rotates the incoming gradients in place (Liger contract)
     torch.autograd.backward([qo, ko], [u, v])
+    u, v = u0, v0
     bq, bk = liger_ref.rope(u[:1, :, :64].double().cpu().numpy(), v[:1, :, :64].double().cpu().numpy(),
                             cos.double().cpu().numpy()[:, :64], sin.double().cpu().numpy()[:, :64], backward=True)
     assert rel_close(q.grad[:1, :, :64].float().cpu().numpy(), bq, tol)[0]
