@@ -280,3 +280,39 @@ int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols,
 }
 
 }  // namespace lk
+
+namespace lk {
+
+template <typename T>
+__global__ void __launch_bounds__(256) cast_f32_kernel(const float* __restrict__ src, T* __restrict__ dst, int64_t n) {
+  const int64_t nvec = n / 8;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride) {
+    float4 a, b;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "l"(src + 8 * i));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) : "l"(src + 8 * i + 4));
+    Vec16<T> v;
+    if constexpr (Vec16<T>::N == 8) {
+      v.v[0] = a.x; v.v[1] = a.y; v.v[2] = a.z; v.v[3] = a.w;
+      v.v[4] = b.x; v.v[5] = b.y; v.v[6] = b.z; v.v[7] = b.w;
+      v.store(dst + 8 * i);
+    } else {
+      for (int k = 0; k < 4; ++k) { dst[8 * i + k] = from_f<T>((&a.x)[k]); dst[8 * i + 4 + k] = from_f<T>((&b.x)[k]); }
+    }
+  }
+  for (int64_t i = nvec * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    dst[i] = from_f<T>(src[i]);
+}
+
+int launch_cast_f32(const float* src, void* dst, int64_t n, int dtype, cudaStream_t st) {
+  if (n <= 0) return LK_OK;
+  unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n / 8 + 255) / 256, 8 * (int64_t)sm_count()));
+  LK_REQUIRE(((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0, LK_NON_CONTIGUOUS,
+             "cast buffers must be 16-byte aligned");
+  LK_DISPATCH_FLOAT(dtype, T, { cast_f32_kernel<T><<<grid, 256, 0, st>>>(src, static_cast<T*>(dst), n); });
+  return check_launch("cast_f32_kernel");
+}
+
+}  // namespace lk

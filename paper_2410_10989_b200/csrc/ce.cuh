@@ -216,6 +216,8 @@ int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols,
                         const int64_t* target, int64_t col_offset, int64_t ignore_index,
                         const float4* partials, int64_t n_parts, const float* tgt_logit,
                         float4* out, cudaStream_t st);
+// dst[i] = dtype(src[i]) for n fp32 values (the multi-chunk dW accumulator -> grad_w).
+int launch_cast_f32(const float* src, void* dst, int64_t n, int dtype, cudaStream_t st);
 int launch_colsum_rows(const void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
                        void* out, int out_dtype, int accumulate, cudaStream_t st);
 

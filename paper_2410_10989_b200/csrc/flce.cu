@@ -14,7 +14,7 @@
 #include <mutex>
 
 #include "ce.cuh"
-#include "gemm_sm100.cuh"
+#include "gemm_sm100_2cta.cuh"
 
 namespace lk {
 namespace tc {
@@ -70,10 +70,56 @@ int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_i
   return LK_OK;
 }
 
+// Tensor map for the epilogue's TMA store: box of 32 rows x 128 bytes, SWIZZLE_128B.
+// Returns 1 if the output can take the TMA path (else the legacy register epilogue runs).
+static int encode_out(CUtensorMap* map, const EpiArgs& e, int dtype) {
+  const void* ptr = nullptr;
+  int odt = e.out_dtype;
+  int64_t ld = e.ldo;
+  switch (e.kind) {
+    case EPI_LOGITS:
+    case EPI_STORE: ptr = e.out; break;
+    case EPI_ACCUM:
+      if (e.acc) { ptr = e.acc; odt = LK_F32; ld = e.ldacc; }
+      else ptr = e.out;
+      break;
+    default: ptr = e.out; odt = LK_F32; break;
+  }
+  const bool is32 = (e.kind == EPI_F32) || (e.kind == EPI_ACCUM && e.acc);
+  if (!ptr || e.M < 1 || e.N < 1) return 0;
+  if (!is32 && odt != dtype) return 0;  // 16-bit path stores the GEMM's own dtype
+  const int64_t esz = is32 ? 4 : 2;
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) || (ld * esz) % 16) return 0;
+  auto enc = get_encode();
+  if (!enc) return 0;
+  cuuint64_t dims[2] = {(cuuint64_t)e.N, (cuuint64_t)e.M};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)(128 / esz), 32u};
+  cuuint32_t es[2] = {1u, 1u};
+  const CUtensorMapDataType dt = is32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                      : (dtype == LK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                                          : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  CUresult r = enc(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 1 : 0;
+}
+
+// CTA-pair (cta_group::2) kernel by default; LK_CTA_GROUP=1 selects the single-CTA kernel.
+int default_cta_group() {
+  static int cg = [] {
+    const char* e = getenv("LK_CTA_GROUP");
+    return (e && e[0] == '1') ? 1 : 2;
+  }();
+  return cg;
+}
+
 int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
-                   int* counter, cudaStream_t st) {
+                   int* counter, cudaStream_t st, int cta_group) {
   LK_REQUIRE(dtype == LK_BF16 || dtype == LK_F16, LK_UNSUPPORTED, "tcgen05 path takes bf16/fp16");
-  CUtensorMap maps[4];
+  if (cta_group <= 0) cta_group = default_cta_group();
+  const int tile_m = cta_group == 2 ? tc2::PBM : BM;
+  const int b_rows_in_box = cta_group == 2 ? tc2::HALF : BN;
+  CUtensorMap maps[6];
   memset(maps, 0, sizeof(maps));
   Args args;
   memset(&args, 0, sizeof(args));
@@ -81,35 +127,62 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
   int total = 0;
   for (int p = 0; p < n_problems; ++p) {
     Problem& P = probs[p];
-    P.tiles_m = (int)((P.M + BM - 1) / BM);
+    P.tiles_m = (int)((P.M + tile_m - 1) / tile_m);
     P.tiles_n = (int)((P.N + BN - 1) / BN);
     P.k_blocks = (int)((P.K + BK - 1) / BK);
     int rc = encode_operand(&maps[2 * p], a[p], dtype, BM, &P.a_mode);
     if (rc) return rc;
-    rc = encode_operand(&maps[2 * p + 1], b[p], dtype, BN, &P.b_mode);
+    rc = encode_operand(&maps[2 * p + 1], b[p], dtype, b_rows_in_box, &P.b_mode);
     if (rc) return rc;
+    P.tma_out = getenv("LK_NO_TMA_EPILOGUE") ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
     args.prob[p] = P;
-    args.idesc[p] = make_idesc(dtype, a[p].mn_major, b[p].mn_major);
+    args.idesc[p] = cta_group == 2 ? tc2::make_idesc2(dtype, a[p].mn_major, b[p].mn_major)
+                                   : make_idesc(dtype, a[p].mn_major, b[p].mn_major);
     if (p == 0) args.tiles0 = P.tiles_m * P.tiles_n;
     total += P.tiles_m * P.tiles_n;
   }
-  if (n_problems == 1) { maps[2] = maps[0]; maps[3] = maps[1]; }
+  if (n_problems == 1) { maps[2] = maps[0]; maps[3] = maps[1]; maps[5] = maps[4]; }
   args.total_tiles = total;
   args.counter = counter;
   if (total == 0) return LK_OK;
   static std::once_flag attr_once;
   static cudaError_t attr_err = cudaSuccess;
-  auto kern = dtype == LK_BF16 ? gemm_kernel<__nv_bfloat16> : gemm_kernel<__half>;
   std::call_once(attr_once, [] {
     attr_err = cudaFuncSetAttribute(gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (attr_err == cudaSuccess)
       attr_err = cudaFuncSetAttribute(gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc2::gemm2_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tc2::SMEM_BYTES);
+    if (attr_err == cudaSuccess)
+      attr_err = cudaFuncSetAttribute(tc2::gemm2_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      tc2::SMEM_BYTES);
   });
   LK_REQUIRE(attr_err == cudaSuccess, LK_CUDA_ERROR,
              std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
-  const int grid = std::min(total, sm_count());
-  kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], args);
-  return check_launch("tcgen05 gemm_kernel");
+  if (cta_group == 1) {
+    auto kern = dtype == LK_BF16 ? gemm_kernel<__nv_bfloat16> : gemm_kernel<__half>;
+    const int grid = std::min(total, sm_count());
+    kern<<<grid, NUM_THREADS, SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], args);
+    return check_launch("tcgen05 gemm_kernel");
+  }
+  auto kern2 = dtype == LK_BF16 ? tc2::gemm2_kernel<__nv_bfloat16> : tc2::gemm2_kernel<__half>;
+  const int pairs = std::min(total, sm_count() / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(tc2::NUM_THREADS);
+  cfg.dynamicSmemBytes = tc2::SMEM_BYTES;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern2, maps[0], maps[1], maps[2], maps[3], maps[4], maps[5], args);
+  if (e != cudaSuccess) return fail(LK_CUDA_ERROR, std::string("cta-pair gemm launch: ") + cudaGetErrorString(e));
+  return check_launch("tcgen05 gemm2_kernel");
 }
 
 }  // namespace tc
@@ -298,14 +371,18 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     EpiArgs xe{};
     xe.kind = EPI_STORE; xe.out_dtype = dt; xe.out = a->grad_x ? static_cast<char*>(a->grad_x) + lo * H * es : nullptr;
     xe.ldo = H; xe.alpha = 1.f; xe.M = r; xe.N = H;
+    // dW: one chunk -> written straight to grad_w; several chunks -> fp32 accumulator
+    // (first chunk stores, later chunks reduce-add in L2 via TMA), cast to grad_w after
+    // the loop.  fp32 weights accumulate in grad_w itself.
     EpiArgs we{};
-    we.kind = EPI_ACCUM; we.out_dtype = dt; we.out = a->grad_w; we.ldo = H; we.M = V; we.N = H;
+    we.kind = EPI_ACCUM; we.out_dtype = dt; we.out = a->grad_w; we.ldo = H; we.M = V; we.N = H; we.alpha = 1.f;
+    (void)last;
     if (dt == LK_F32) {
       we.acc = static_cast<float*>(a->grad_w); we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
     } else if (L.nchunks == 1) {
       we.acc = nullptr; we.ldacc = H; we.beta = 0; we.final_out = 1;
     } else {
-      we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = last ? 1 : 0;
+      we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
     }
     ProfScope ps_bwd(2, st);
     if (tc) {
@@ -341,6 +418,10 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (rc) return rc;
   }
   ProfScope ps_tail(3, st);
+  if (want_grad && a->grad_w && dt != LK_F32 && L.nchunks > 1) {
+    rc = launch_cast_f32(dwacc, a->grad_w, V * H, dt, st);
+    if (rc) return rc;
+  }
   if (a->grad_bias) {
     rc = launch_colsum_rows(bacc, 1, V, V, LK_F32, a->grad_bias, dt, 0, st);
     if (rc) return rc;
@@ -461,7 +542,7 @@ extern "C" int lk_gemm_test(const void* a, const void* b, float* d, int64_t m, i
     LK_REQUIRE(tc::tma_ok(A) && tc::tma_ok(B), LK_NON_CONTIGUOUS, "operands not TMA-describable");
     tc::Problem P{};
     P.M = m; P.N = n; P.K = k; P.n_fast = layout == 2 ? 1 : 0; P.epi = e;
-    return tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st);
+    return tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st, use_tcgen05 == 2 ? 2 : 1);
 #else
     return fail(LK_UNSUPPORTED, "built without tcgen05");
 #endif

@@ -31,9 +31,10 @@ constexpr int B_BYTES = BN * BK * 2;   // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_THREADS = 256;
 constexpr int TMEM_COLS = 512;
-// barriers + sched ring + tmem slot, after the 1024-aligned stage buffers
+// stage ring | epilogue staging (4 warps x 2 x 4 KB) | barriers + sched ring + tmem slot
 constexpr int AUX_BYTES = 1024;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + AUX_BYTES + 1024;  // + alignment slack
+constexpr int EPI_STAGING_BYTES = 4 * 2 * 4096;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_STAGING_BYTES + AUX_BYTES + 1024;  // + alignment slack
 
 struct Problem {
   int64_t M, N, K;
@@ -42,6 +43,7 @@ struct Problem {
   // {64, 64 K, atoms}, 2 = MN-major via one 2D box per 64-wide atom
   int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
+  int tma_out;          // 1: epilogue writes through smem staging + TMA store (map mc<p>)
   EpiArgs epi;
 };
 
@@ -352,6 +354,178 @@ __device__ __forceinline__ void epi_f32(const EpiArgs& e, int64_t grow, int64_t 
       if (col0 + j < e.N) orow[col0 + j] = __uint_as_float(r[j]);
   }
 }
+
+// ------------------------------------------- TMA-store epilogues (default) ----
+// Each epilogue warp owns 32 rows of the tile and a double-buffered 4 KB staging
+// area in shared memory.  A 128-byte row segment (32 fp32 or 64 bf16) per thread
+// is written with SWIZZLE_128B placement (16-B chunk j of row r at chunk j ^ (r & 7),
+// bank-conflict-free), then one lane issues a TMA bulk tensor store -- or, for the
+// fp32 dW accumulator, a TMA reduce-add (the add happens in L2) -- of the 32-row box.
+// Out-of-range rows/columns are clipped by the tensor map bounds.  Versus one-row-
+// per-thread global stores this turns 32 scattered 16-B accesses per instruction
+// into one bulk copy, which frees the L1/shared-memory pipe the mainloop needs.
+constexpr int STG_BYTES = 4096;
+
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_2d(uint64_t map, uint32_t src, int x, int y) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];"
+               ::"l"(map), "r"(src), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void tma_reduce_add_2d(uint64_t map, uint32_t src, int x, int y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.bulk_group [%0, {%2, %3}], [%1];"
+               ::"l"(map), "r"(src), "r"(x), "r"(y) : "memory");
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
+struct Stager {
+  uint32_t base;  // this warp's two 4 KB buffers
+  int b;
+  __device__ __forceinline__ uint32_t acquire(int lane) {
+    if (lane == 0) bulk_wait_read1();  // the store that last read this buffer has finished reading
+    __syncwarp();
+    const uint32_t buf = base + b * STG_BYTES;
+    b ^= 1;
+    return buf;
+  }
+  __device__ __forceinline__ void flush(uint64_t map, uint32_t buf, int x, int y, bool reduce, int lane) {
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      if (reduce) tma_reduce_add_2d(map, buf, x, y);
+      else tma_store_2d(map, buf, x, y);
+      bulk_commit();
+    }
+  }
+};
+
+// One thread's 128-byte row: eight 16-byte chunks, swizzled.
+__device__ __forceinline__ void stage_row(uint32_t buf, int lane, const uint32_t (&w)[32]) {
+  const uint32_t row = buf + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    st_shared_v4(row + ((j ^ (lane & 7)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+}
+
+template <typename T>
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  T x = from_f<T>(a), y = from_f<T>(b);
+  return (uint32_t)(*reinterpret_cast<uint16_t*>(&x)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&y)) << 16);
+}
+
+// 16-bit output (logits with online-softmax partials, or alpha * acc), 64-column groups.
+template <typename T, bool LOGITS>
+__device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stager& sg, int lane, int64_t grow,
+                                          int row0, int64_t n0, int n_blk, uint32_t taddr) {
+  const bool row_ok = grow < e.M;
+  int64_t tcol = -1;
+  if (LOGITS && row_ok) {
+    const int64_t y = e.target[grow];
+    if (y != e.ignore_index) tcol = y - e.col_offset;
+  }
+  const bool cap = LOGITS && e.softcap > 0.f;
+  const float inv_cap = cap ? 1.f / e.softcap : 0.f;
+  float m = -INFINITY, s = 0.f, sz = 0.f, tv = 0.f;
+  bool have_t = false;
+#pragma unroll 1
+  for (int g = 0; g < BN / 64; ++g) {
+    uint32_t r0[32], r1[32];
+    tmem_ld32(taddr + g * 64, r0);
+    tmem_ld32(taddr + g * 64 + 32, r1);
+    tmem_wait_ld();
+    const int64_t col0 = n0 + g * 64;
+    uint32_t w[32];
+    if (LOGITS) {
+      const int nvalid = (int)(e.N - col0 < 64 ? (e.N - col0 > 0 ? e.N - col0 : 0) : 64);
+      float v[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        float z = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+        if (e.bias && j < nvalid) z += load_any(e.bias, col0 + j, e.out_dtype);
+        if (cap) z = e.softcap * tanh_fast(z * inv_cap);
+        v[j] = round_to<T>(z);
+      }
+      if (row_ok && nvalid > 0) {
+        float cm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < nvalid) cm = fmaxf(cm, v[j]);
+        const float mn = fmaxf(m, cm);
+        float acc = 0.f, zs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < nvalid) { acc += __expf(v[j] - mn); zs += v[j]; }
+        s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + acc;
+        m = mn;
+        sz += zs;
+        if (tcol >= col0 && tcol < col0 + nvalid) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (col0 + j == tcol) tv = v[j];
+          have_t = true;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) w[j] = pack2<T>(v[2 * j], v[2 * j + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        w[j] = pack2<T>(e.alpha * __uint_as_float(r0[2 * j]), e.alpha * __uint_as_float(r0[2 * j + 1]));
+        w[16 + j] = pack2<T>(e.alpha * __uint_as_float(r1[2 * j]), e.alpha * __uint_as_float(r1[2 * j + 1]));
+      }
+    }
+    const uint32_t buf = sg.acquire(lane);
+    stage_row(buf, lane, w);
+    sg.flush(omap, buf, (int)col0, row0, false, lane);
+  }
+  if (LOGITS && row_ok) {
+    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
+    if (have_t) e.tgt_logit[grow] = tv;
+  }
+}
+
+// fp32 output: plain store (F32 / first dW chunk) or reduce-add (later dW chunks).
+__device__ __forceinline__ void epi_tma32(uint64_t omap, Stager& sg, int lane, int row0, int64_t n0, bool reduce,
+                                          uint32_t taddr) {
+#pragma unroll 1
+  for (int c = 0; c < BN / 32; ++c) {
+    uint32_t r[32];
+    tmem_ld32(taddr + c * 32, r);
+    tmem_wait_ld();
+    const uint32_t buf = sg.acquire(lane);
+    stage_row(buf, lane, r);
+    sg.flush(omap, buf, (int)(n0 + c * 32), row0, reduce, lane);
+  }
+}
+
+// Dispatch one tile's epilogue for this warp.
+template <typename T>
+__device__ __forceinline__ void run_epilogue(const Problem& P, uint64_t omap, Stager& sg, int lane, int64_t grow,
+                                             int row0, int64_t n0, int n_blk, uint32_t taddr) {
+  const EpiArgs& e = P.epi;
+  if (P.tma_out) {
+    switch (e.kind) {
+      case EPI_LOGITS: epi_tma16<T, true>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
+      case EPI_STORE: epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
+      case EPI_ACCUM:
+        if (e.acc) epi_tma32(omap, sg, lane, row0, n0, e.beta != 0, taddr);
+        else epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr);
+        break;
+      default: epi_tma32(omap, sg, lane, row0, n0, false, taddr); break;
+    }
+    return;
+  }
+  switch (e.kind) {
+    case EPI_LOGITS: epi_logits<T>(e, grow, n0, n_blk, taddr); break;
+    case EPI_STORE: epi_store<T>(e, grow, n0, taddr); break;
+    case EPI_ACCUM: epi_accum<T>(e, grow, n0, taddr); break;
+    default: epi_f32<T>(e, grow, n0, taddr); break;
+  }
+}
 #endif  // __CUDA_ARCH__
 
 // ---------------------------------------------------------------- kernel ----
@@ -359,13 +533,15 @@ template <typename T>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUtensorMap mb0,
             const __grid_constant__ CUtensorMap ma1, const __grid_constant__ CUtensorMap mb1,
+            const __grid_constant__ CUtensorMap mc0, const __grid_constant__ CUtensorMap mc1,
             const __grid_constant__ Args args) {
 #if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ >= 1000)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* aux = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* sStg = smem + STAGES * STAGE_BYTES;
+  uint64_t* aux = reinterpret_cast<uint64_t*>(sStg + EPI_STAGING_BYTES);
   uint64_t* full = aux;                    // [STAGES]
   uint64_t* empty = full + STAGES;         // [STAGES]
   uint64_t* tfull = empty + STAGES;        // [2]
@@ -498,6 +674,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;
+    Stager sg{smem_u32(sStg) + (uint32_t)(q * 2 * STG_BYTES), 0};
     for (int it = 0;; ++it) {
       const int slot = it % SCHED;
       mbar_wait(&sfull[slot], (it / SCHED) & 1);
@@ -507,22 +684,20 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       if (tile < 0) break;
       const TileCoord tcd = decode_tile(args, tile);
       const Problem& P = args.prob[tcd.p];
+      const uint64_t omap = reinterpret_cast<uint64_t>(tcd.p ? &mc1 : &mc0);
       const int buf = it & 1;
       mbar_wait(&tfull[buf], (it >> 1) & 1);
       tc_fence_after();
       const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(q * 32) << 16);
-      const int64_t grow = (int64_t)tcd.m_blk * BM + q * 32 + lane;
+      const int row0 = tcd.m_blk * BM + q * 32;
+      const int64_t grow = (int64_t)row0 + lane;
       const int64_t n0 = (int64_t)tcd.n_blk * BN;
-      switch (P.epi.kind) {
-        case EPI_LOGITS: epi_logits<T>(P.epi, grow, n0, tcd.n_blk, taddr); break;
-        case EPI_STORE: epi_store<T>(P.epi, grow, n0, taddr); break;
-        case EPI_ACCUM: epi_accum<T>(P.epi, grow, n0, taddr); break;
-        default: epi_f32<T>(P.epi, grow, n0, taddr); break;
-      }
+      run_epilogue<T>(P, omap, sg, lane, grow, row0, n0, tcd.n_blk, taddr);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[buf]);
     }
+    if (lane == 0) bulk_wait_all();
   }
   __syncwarp();
   tc_fence_before();
@@ -559,8 +734,9 @@ bool tma_ok(const TmaOperand& op);
 
 // Launch one or two problems in a single persistent launch.
 // Problem p: C[M, N] = A·B with A given by `a[p]` and B by `b[p]`.
+// cta_group: 1 = single-CTA 128x256 tiles, 2 = CTA-pair 256x256 tiles, 0 = default (pair).
 int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
-                   int* counter, cudaStream_t st);
+                   int* counter, cudaStream_t st, int cta_group = 0);
 
 }  // namespace tc
 }  // namespace lk

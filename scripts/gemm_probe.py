@@ -28,16 +28,16 @@ def main():
         A = torch.randint(-2, 3, (m, k), device="cuda").to(torch.bfloat16)
         B = torch.randint(-2, 3, (k, n), device="cuda").to(torch.bfloat16)
         ref = A.float() @ B.float()
-        for layout in (0, 1, 2):
+        for layout, cg in [(l, c) for c in (1, 2) for l in (0, 1, 2)]:
             if layout == 0:
                 a, b = A.contiguous(), B.t().contiguous()
             elif layout == 1:
                 a, b = A.contiguous(), B.contiguous()
             else:
                 a, b = A.t().contiguous(), B.contiguous()
-            d = run(a, b, m, n, k, layout)
+            d = run(a, b, m, n, k, layout, tc=cg)
             eq = (d == ref)
-            info = f"m{m} n{n} k{k} layout{layout}: exact={bool(eq.all())} frac={eq.float().mean().item():.4f}"
+            info = f"m{m} n{n} k{k} layout{layout} cg{cg}: exact={bool(eq.all())} frac={eq.float().mean().item():.4f}"
             if not eq.all():
                 nan = torch.isnan(d).float().mean().item()
                 zero = (d == 0).float().mean().item()

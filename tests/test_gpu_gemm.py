@@ -38,14 +38,15 @@ def operands(m, n, k, layout, seed):
     return A.t().contiguous(), B.contiguous(), ref          # A[K,M], B[K,N]
 
 
+@pytest.mark.parametrize("cta_group", [1, 2])
 @pytest.mark.parametrize("layout", [0, 1, 2])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_tcgen05_gemm_exact(layout, shape):
+def test_tcgen05_gemm_exact(layout, shape, cta_group):
     m, n, k = shape
     if layout == 2 and m % 8:
         pytest.skip("M-major A needs M % 8 == 0 for TMA")
     a, b, ref = operands(m, n, k, layout, seed=m + n + k + layout)
-    d = run(a, b, m, n, k, layout, tc=True)
+    d = run(a, b, m, n, k, layout, tc=cta_group)
     bad = (d != ref).sum().item()
     assert bad == 0, f"{bad} mismatches; first at {torch.nonzero(d != ref)[:4].tolist()}"
 
@@ -63,7 +64,7 @@ def test_tcgen05_gemm_random_bf16_large():
     g = torch.Generator(device="cuda").manual_seed(0)
     A = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
     B = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
-    d = run(A, B, m, n, k, 0, tc=True)
+    d = run(A, B, m, n, k, 0, tc=2)
     ref = A.float() @ B.float().t()
     err = (d - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
