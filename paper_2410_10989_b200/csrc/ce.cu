@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) vp_row_stats_kernel(const T* __restrict__
     z = warp_sum(z);
     if (lane == 0) {
       float zt = 0.f;
-      if (yl >= 0 && yl < n) zt = partials ? tgt[row] : to_f<T>(x[row * ld + yl]);
+      if (yl >= 0 && yl < n) zt = to_f<T>(x[row * ld + yl]);  // stored (capped, rounded) logit
       out[row] = make_float4(m, s, z, zt);
     }
   }

@@ -133,9 +133,7 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
       wz = warp_sum(wz);
       if (lane == 0) {
         float zt = 0.f;
-        if (a.partials) {
-          zt = a.tgt_logit[row];
-        } else if (yl >= 0 && yl < n) {
+        if (yl >= 0 && yl < n) {
           zt = to_f<T>(x[yl]);
           if (has_cap && !a.input_capped) zt = cap_val<T>(zt, cap, true);
         }

@@ -330,7 +330,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     le.kind = EPI_LOGITS; le.out_dtype = dt; le.out = zbuf; le.ldo = L.ldz; le.alpha = 1.f;
     le.bias = a->bias; le.softcap = a->softcap; le.target = a->target + lo; le.col_offset = 0;
     le.ignore_index = a->ignore_index; le.partials = parts; le.n_parts = L.nparts; le.tgt_logit = tgt;
-    le.M = r; le.N = V;
+    le.M = r; le.N = V; le.want_sum = a->label_smoothing > 0.f ? 1 : 0;
     {
       ProfScope ps(0, st);
       if (tc) {
@@ -464,6 +464,7 @@ extern "C" int lk_flce_vp_logits(const void* x, const void* weight_shard, const 
   le.kind = EPI_LOGITS; le.out_dtype = dtype; le.out = logits_buf; le.ldo = ldz; le.alpha = 1.f;
   le.softcap = softcap; le.target = target; le.col_offset = vocab_offset; le.ignore_index = ignore_index;
   le.partials = parts; le.n_parts = nparts; le.tgt_logit = tgt; le.M = rows; le.N = vocab_local;
+  le.want_sum = 1;
   int rc;
   LK_CUDA(cudaMemsetAsync(tgt, 0, (size_t)rows * 4, st));
   if (tc) {

@@ -33,7 +33,8 @@ struct EpiArgs {
   int64_t ignore_index;
   float4* partials;       // [M, n_parts]
   int64_t n_parts;
-  float* tgt_logit;       // [M]
+  float* tgt_logit;       // [M] (legacy register epilogue only)
+  int want_sum;           // EPI_LOGITS: also accumulate sum of logits (label smoothing)
   int64_t M, N;           // valid output extent
 };
 

@@ -417,20 +417,53 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return (uint32_t)(*reinterpret_cast<uint16_t*>(&x)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&y)) << 16);
 }
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+template <int N>
+__device__ __forceinline__ float tree_max(const float* v) {
+  float t[N / 2];
+#pragma unroll
+  for (int i = 0; i < N / 2; ++i) t[i] = fmaxf(v[2 * i], v[2 * i + 1]);
+#pragma unroll
+  for (int w = N / 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) t[i] = fmaxf(t[2 * i], t[2 * i + 1]);
+  return t[0];
+}
+
+// Logit transform of one 64-column group: (+bias) -> (softcap) -> round to the logits
+// dtype.  The branches are warp-uniform and sit outside the unrolled element loop.
+template <typename T>
+__device__ __forceinline__ void logits_values(const EpiArgs& e, const uint32_t (&r0)[32], const uint32_t (&r1)[32],
+                                              int64_t col0, int nvalid, float (&v)[64]) {
+#pragma unroll
+  for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
+  if (e.bias) {
+    for (int j = 0; j < 64; ++j)
+      if (j < nvalid) v[j] += load_any(e.bias, col0 + j, e.out_dtype);
+  }
+  if (e.softcap > 0.f) {
+    const float c = e.softcap, ic = 1.f / e.softcap;
+#pragma unroll
+    for (int j = 0; j < 64; ++j) v[j] = c * tanh_fast(v[j] * ic);
+  }
+#pragma unroll
+  for (int j = 0; j < 64; ++j) v[j] = round_to<T>(v[j]);
+}
+
 // 16-bit output (logits with online-softmax partials, or alpha * acc), 64-column groups.
+// The statistics use the rounded values, so the finalize's softmax is self-consistent;
+// the target logit is not captured here (the finalize reads it from the chunk buffer).
 template <typename T, bool LOGITS>
 __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stager& sg, int lane, int64_t grow,
                                           int row0, int64_t n0, int n_blk, uint32_t taddr) {
+  constexpr float LOG2E = 1.4426950408889634f;
   const bool row_ok = grow < e.M;
-  int64_t tcol = -1;
-  if (LOGITS && row_ok) {
-    const int64_t y = e.target[grow];
-    if (y != e.ignore_index) tcol = y - e.col_offset;
-  }
-  const bool cap = LOGITS && e.softcap > 0.f;
-  const float inv_cap = cap ? 1.f / e.softcap : 0.f;
-  float m = -INFINITY, s = 0.f, sz = 0.f, tv = 0.f;
-  bool have_t = false;
+  const bool want_sum = LOGITS && e.want_sum;
+  float m = -INFINITY, s = 0.f, sz = 0.f;
 #pragma unroll 1
   for (int g = 0; g < BN / 64; ++g) {
     uint32_t r0[32], r1[32];
@@ -440,34 +473,38 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
     const int64_t col0 = n0 + g * 64;
     uint32_t w[32];
     if (LOGITS) {
-      const int nvalid = (int)(e.N - col0 < 64 ? (e.N - col0 > 0 ? e.N - col0 : 0) : 64);
+      const int64_t rem = e.N - col0;
+      const int nvalid = (int)(rem < 64 ? (rem > 0 ? rem : 0) : 64);
       float v[64];
+      logits_values<T>(e, r0, r1, col0, nvalid, v);
+      if (nvalid == 64) {
+        const float mn = fmaxf(m, tree_max<64>(v));
+        const float ml = mn * LOG2E;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-      for (int j = 0; j < 64; ++j) {
-        float z = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
-        if (e.bias && j < nvalid) z += load_any(e.bias, col0 + j, e.out_dtype);
-        if (cap) z = e.softcap * tanh_fast(z * inv_cap);
-        v[j] = round_to<T>(z);
-      }
-      if (row_ok && nvalid > 0) {
-        float cm = -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < nvalid) cm = fmaxf(cm, v[j]);
-        const float mn = fmaxf(m, cm);
-        float acc = 0.f, zs = 0.f;
-#pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < nvalid) { acc += __expf(v[j] - mn); zs += v[j]; }
-        s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + acc;
-        m = mn;
-        sz += zs;
-        if (tcol >= col0 && tcol < col0 + nvalid) {
-#pragma unroll
-          for (int j = 0; j < 64; ++j)
-            if (col0 + j == tcol) tv = v[j];
-          have_t = true;
+        for (int j = 0; j < 64; j += 4) {
+          a0 += ex2f(fmaf(v[j], LOG2E, -ml));
+          a1 += ex2f(fmaf(v[j + 1], LOG2E, -ml));
+          a2 += ex2f(fmaf(v[j + 2], LOG2E, -ml));
+          a3 += ex2f(fmaf(v[j + 3], LOG2E, -ml));
         }
+        if (want_sum) {
+          float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 64; j += 4) { z0 += v[j]; z1 += v[j + 1]; z2 += v[j + 2]; z3 += v[j + 3]; }
+          sz += (z0 + z1) + (z2 + z3);
+        }
+        s = s * ex2f((m - mn) * LOG2E) + ((a0 + a1) + (a2 + a3));  // m = -inf first: ex2(-inf) = 0
+        m = mn;
+      } else if (nvalid > 0) {
+        float cm = -INFINITY;
+        for (int j = 0; j < nvalid; ++j) cm = fmaxf(cm, v[j]);
+        const float mn = fmaxf(m, cm);
+        float a = 0.f, z = 0.f;
+        for (int j = 0; j < nvalid; ++j) { a += ex2f((v[j] - mn) * LOG2E); z += v[j]; }
+        s = s * ex2f((m - mn) * LOG2E) + a;
+        m = mn;
+        if (want_sum) sz += z;
       }
 #pragma unroll
       for (int j = 0; j < 32; ++j) w[j] = pack2<T>(v[2 * j], v[2 * j + 1]);
@@ -482,10 +519,7 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
     stage_row(buf, lane, w);
     sg.flush(omap, buf, (int)col0, row0, false, lane);
   }
-  if (LOGITS && row_ok) {
-    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
-    if (have_t) e.tgt_logit[grow] = tv;
-  }
+  if (LOGITS && row_ok) e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
 }
 
 // fp32 output: plain store (F32 / first dW chunk) or reduce-add (later dW chunks).

@@ -57,7 +57,23 @@ __global__ void __launch_bounds__(256) glu_fwd_kernel(const T* __restrict__ a, c
   constexpr int NV = Vec16<T>::N;
   const int64_t nvec = n / NV;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // two vectors per thread per iteration: four 16-byte loads in flight before any math
+  for (; i + stride < nvec; i += 2 * stride) {
+    Vec16<T> va, vb, va2, vb2;
+    va.load_nc(a + i * NV);
+    vb.load_nc(b + i * NV);
+    va2.load_nc(a + (i + stride) * NV);
+    vb2.load_nc(b + (i + stride) * NV);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      va.v[k] = Glu<T, ACT>::fwd(va.v[k], vb.v[k]);
+      va2.v[k] = Glu<T, ACT>::fwd(va2.v[k], vb2.v[k]);
+    }
+    va.store(c + i * NV);
+    va2.store(c + (i + stride) * NV);
+  }
+  for (; i < nvec; i += stride) {
     Vec16<T> va, vb;
     va.load_nc(a + i * NV);
     vb.load_nc(b + i * NV);

@@ -47,10 +47,19 @@ __global__ void __launch_bounds__(256) rope_kernel(T* __restrict__ q, T* __restr
       x1[0] = to_f<T>(base[i0]);
       x2[0] = to_f<T>(base[half + i0]);
     }
+    if constexpr (VEC && sizeof(C) == sizeof(T)) {
+      // same width as q/k: one 16-byte load each for cos and sin (rows are d-aligned)
+      Vec16<C> vc, vs;
+      vc.load(cosp + crow + i0);
+      vs.load(sinp + crow + i0);
 #pragma unroll
-    for (int e = 0; e < NV; ++e) {
-      c[e] = to_f<C>(cosp[crow + i0 + e]);
-      s[e] = sgn * to_f<C>(sinp[crow + i0 + e]);
+      for (int e = 0; e < NV; ++e) { c[e] = vc.v[e]; s[e] = sgn * vs.v[e]; }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        c[e] = to_f<C>(cosp[crow + i0 + e]);
+        s[e] = sgn * to_f<C>(sinp[crow + i0 + e]);
+      }
     }
     float y1[NV], y2[NV];
 #pragma unroll
@@ -77,6 +86,8 @@ static int launch_rope(void* q, void* k, const void* cs, const void* sn, int64_t
   constexpr int NV = Vec16<T>::N;
   bool vec = ((d / 2) % NV == 0) && ((reinterpret_cast<uintptr_t>(q) & 15) == 0) &&
              ((reinterpret_cast<uintptr_t>(k) & 15) == 0);
+  if (sizeof(C) == sizeof(T))  // vector cos/sin loads need 16-byte aligned tables
+    vec = vec && ((reinterpret_cast<uintptr_t>(cs) & 15) == 0) && ((reinterpret_cast<uintptr_t>(sn) & 15) == 0);
   const int64_t items = batch * seq * (nq + nk) * ((d / 2) / (vec ? NV : 1));
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)sm_count()));
   if (vec)
