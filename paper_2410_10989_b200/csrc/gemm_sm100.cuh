@@ -117,6 +117,20 @@ __device__ __forceinline__ void tma_3d(uint64_t map, uint32_t bar, uint32_t dst,
       ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_2d(uint64_t map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(uint64_t map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y),
+               "r"(z) : "memory");
+}
+// L2 prefetch of one operand box (mode as in Problem::a_mode/b_mode; mode 2 prefetches its first atom pair).
+__device__ __forceinline__ void prefetch_operand(uint64_t map, int mode, int k0, int mn0) {
+  if (mode == 0) tma_prefetch_2d(map, k0, mn0);
+  else if (mode == 1) tma_prefetch_3d(map, 0, k0, mn0 >> 6);
+  else tma_prefetch_2d(map, mn0, k0);
+}
 __device__ __forceinline__ uint32_t elect_one() {
   uint32_t pred = 0;
   asm volatile(

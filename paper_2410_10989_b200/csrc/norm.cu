@@ -15,6 +15,7 @@
 // the row is re-read from L1/L2 for the second pass.  The backward is persistent:
 // grid = 2 x SMs CTAs, contiguous row ranges per CTA.
 #include "common.cuh"
+#include "norm_rowstream.cuh"
 
 namespace lk {
 
@@ -212,222 +213,6 @@ rmsnorm_bwd_stream(const T* dy, const T* __restrict__ x, const T* __restrict__ w
   }
 }
 
-// --------------------------------------------------- TMA row-stream path ----
-// Persistent CTAs (2 per SM); CTA c handles rows c, c + G, c + 2G, ...  Rows are
-// streamed into a ring of shared-memory stages by 1D TMA bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx), so STAGES rows per CTA are in flight
-// while the current row is reduced and written.  Registers hold only the dgamma
-// partial (backward).  Requires 16-byte aligned rows.
-constexpr int RS_THREADS = 256;
-constexpr int RS_SMEM = 96 * 1024;  // ring budget per CTA (2 CTAs per SM)
-
-__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void rs_mbar_init(uint64_t* b, uint32_t c) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(c) : "memory");
-}
-__device__ __forceinline__ void rs_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void rs_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done) : "r"(s_u32(b)), "r"(parity) : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void rs_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-               ::"r"(s_u32(dst)), "l"(src), "r"(bytes), "r"(s_u32(bar)) : "memory");
-}
-
-template <typename T>
-__device__ __forceinline__ void ld_vec_smem(const T* p, float (&v)[Vec16<T>::N]) {
-  uint4 raw = *reinterpret_cast<const uint4*>(p);
-  const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-  for (int i = 0; i < Vec16<T>::N; ++i) v[i] = to_f<T>(e[i]);
-}
-
-template <typename T, typename R>
-__global__ void __launch_bounds__(RS_THREADS)
-rmsnorm_fwd_stream_tma(const T* __restrict__ x, const T* __restrict__ w, T* __restrict__ y, R* __restrict__ rstd,
-                       int64_t rows, int64_t cols, float eps, float offset, int mode, int stages) {
-  constexpr int NV = Vec16<T>::N;
-  extern __shared__ __align__(128) uint8_t rs_smem[];
-  const uint32_t row_bytes = (uint32_t)(cols * sizeof(T));
-  const uint32_t stage_bytes = (row_bytes + 127) / 128 * 128;
-  T* wsm = reinterpret_cast<T*>(rs_smem);                                   // gamma copy
-  uint8_t* ring = rs_smem + stage_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)stages * stage_bytes);
-  __shared__ float scratch[32];
-  const int tid = threadIdx.x;
-  const int64_t nvec = cols / NV;
-  const int64_t G = gridDim.x;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) rs_mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (w)
-    for (int64_t i = tid; i < nvec; i += RS_THREADS)
-      reinterpret_cast<uint4*>(wsm)[i] = reinterpret_cast<const uint4*>(w)[i];
-  __syncthreads();
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      const int64_t row = blockIdx.x + (int64_t)s * G;
-      if (row >= rows) break;
-      rs_expect_tx(&full[s], row_bytes);
-      rs_bulk_g2s(ring + (size_t)s * stage_bytes, x + row * cols, row_bytes, &full[s]);
-    }
-  }
-  int s = 0;
-  uint32_t phase = 0;
-  for (int64_t row = blockIdx.x; row < rows; row += G) {
-    const T* xs = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
-    rs_wait(&full[s], phase);
-    float ss = 0.f;
-    for (int64_t i = tid; i < nvec; i += RS_THREADS) {
-      float v[NV];
-      ld_vec_smem<T>(xs + i * NV, v);
-#pragma unroll
-      for (int e = 0; e < NV; ++e) ss += v[e] * v[e];
-    }
-    ss = block_sum(ss, scratch);
-    const float r = rsqrtf(ss / (float)cols + eps);
-    if (tid == 0) rstd[row] = from_f<R>(r);
-    T* yr = y + row * cols;
-    for (int64_t i = tid; i < nvec; i += RS_THREADS) {
-      float v[NV], wv[NV];
-      ld_vec_smem<T>(xs + i * NV, v);
-      if (w) ld_vec_smem<T>(wsm + i * NV, wv);
-      Vec16<T> o;
-#pragma unroll
-      for (int e = 0; e < NV; ++e) o.v[e] = fwd_val<T>(v[e], r, w ? wv[e] : 0.f, w != nullptr, offset, mode);
-      o.store(yr + i * NV);
-    }
-    __syncthreads();  // stage s fully consumed
-    if (tid == 0) {
-      const int64_t nxt = row + (int64_t)stages * G;
-      if (nxt < rows) {
-        rs_expect_tx(&full[s], row_bytes);
-        rs_bulk_g2s(ring + (size_t)s * stage_bytes, x + nxt * cols, row_bytes, &full[s]);
-      }
-    }
-    if (++s == stages) { s = 0; phase ^= 1; }
-  }
-}
-
-template <typename T, typename R, int KMAX>
-__global__ void __launch_bounds__(RS_THREADS)
-rmsnorm_bwd_stream_tma(const T* dy, const T* __restrict__ x, const T* __restrict__ w, const R* __restrict__ rstd,
-                       T* dx, float* __restrict__ dw_part, int64_t rows, int64_t cols, float offset, int mode,
-                       int stages) {
-  constexpr int NV = Vec16<T>::N;
-  extern __shared__ __align__(128) uint8_t rs_smem[];
-  const uint32_t row_bytes = (uint32_t)(cols * sizeof(T));
-  const uint32_t half_bytes = (row_bytes + 127) / 128 * 128;
-  const uint32_t stage_bytes = 2 * half_bytes;  // dy row | x row
-  T* wsm = reinterpret_cast<T*>(rs_smem);
-  uint8_t* ring = rs_smem + half_bytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + (size_t)stages * stage_bytes);
-  __shared__ float scratch[32];
-  const int tid = threadIdx.x;
-  const int64_t nvec = cols / NV;
-  const int64_t G = gridDim.x;
-  float acc[KMAX][NV];
-#pragma unroll
-  for (int k = 0; k < KMAX; ++k)
-#pragma unroll
-    for (int e = 0; e < NV; ++e) acc[k][e] = 0.f;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) rs_mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (w)
-    for (int64_t i = tid; i < nvec; i += RS_THREADS)
-      reinterpret_cast<uint4*>(wsm)[i] = reinterpret_cast<const uint4*>(w)[i];
-  __syncthreads();
-  auto issue = [&](int s, int64_t row) {
-    uint8_t* st = ring + (size_t)s * stage_bytes;
-    rs_expect_tx(&full[s], 2 * row_bytes);
-    rs_bulk_g2s(st, dy + row * cols, row_bytes, &full[s]);
-    rs_bulk_g2s(st + half_bytes, x + row * cols, row_bytes, &full[s]);
-  };
-  if (tid == 0)
-    for (int s = 0; s < stages; ++s) {
-      const int64_t row = blockIdx.x + (int64_t)s * G;
-      if (row >= rows) break;
-      issue(s, row);
-    }
-  int s = 0;
-  uint32_t phase = 0;
-  for (int64_t row = blockIdx.x; row < rows; row += G) {
-    const T* gs = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes);
-    const T* xs = reinterpret_cast<const T*>(ring + (size_t)s * stage_bytes + half_bytes);
-    rs_wait(&full[s], phase);
-    const float r = to_f<R>(rstd[row]);
-    float dot = 0.f;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      const int64_t i = tid + (int64_t)k * RS_THREADS;
-      if (i < nvec) {
-        float g[NV], xv[NV], wv[NV];
-        ld_vec_smem<T>(gs + i * NV, g);
-        ld_vec_smem<T>(xs + i * NV, xv);
-        if (w) ld_vec_smem<T>(wsm + i * NV, wv);
-#pragma unroll
-        for (int e = 0; e < NV; ++e) {
-          float mm = w ? g[e] * (offset + wv[e]) : g[e];
-          if (mode == LK_CAST_LLAMA) mm = round_to<T>(mm);
-          dot += mm * xv[e];
-          float xh = xv[e] * r;
-          if (mode == LK_CAST_LLAMA) xh = round_to<T>(xh);
-          acc[k][e] += g[e] * xh;
-        }
-      }
-    }
-    dot = block_sum(dot, scratch);
-    const float c = r * r * r * dot / (float)cols;
-    T* dxr = dx + row * cols;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      const int64_t i = tid + (int64_t)k * RS_THREADS;
-      if (i < nvec) {
-        float g[NV], xv[NV], wv[NV];
-        ld_vec_smem<T>(gs + i * NV, g);
-        ld_vec_smem<T>(xs + i * NV, xv);
-        if (w) ld_vec_smem<T>(wsm + i * NV, wv);
-        Vec16<T> o;
-#pragma unroll
-        for (int e = 0; e < NV; ++e) {
-          float mm = w ? g[e] * (offset + wv[e]) : g[e];
-          if (mode == LK_CAST_LLAMA) mm = round_to<T>(mm);
-          o.v[e] = r * mm - c * xv[e];
-        }
-        o.store(dxr + i * NV);
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const int64_t nxt = row + (int64_t)stages * G;
-      if (nxt < rows) issue(s, nxt);
-    }
-    if (++s == stages) { s = 0; phase ^= 1; }
-  }
-  if (dw_part) {
-    float* p = dw_part + (int64_t)blockIdx.x * cols;
-#pragma unroll
-    for (int k = 0; k < KMAX; ++k) {
-      const int64_t i = tid + (int64_t)k * RS_THREADS;
-      if (i < nvec)
-#pragma unroll
-        for (int e = 0; e < NV; e += 4)
-          *reinterpret_cast<float4*>(p + i * NV + e) = make_float4(acc[k][e], acc[k][e + 1], acc[k][e + 2], acc[k][e + 3]);
-    }
-  }
-}
-
 // dw[c] = sum_g part[g, c], fixed order over g (deterministic second stage).
 template <typename T>
 __global__ void colsum_partials_kernel(const float* __restrict__ part, int64_t g, int64_t cols,
@@ -473,27 +258,17 @@ static bool aligned16_all(std::initializer_list<const void*> ptrs) {
   return true;
 }
 
-// Ring depth for the TMA row-stream kernels: (1 gamma row + stages x rows_per_stage rows) must fit.
-template <typename T>
-static int rs_stages(int64_t cols, int rows_per_stage) {
-  const int64_t rb = (cols * (int64_t)sizeof(T) + 127) / 128 * 128;
-  const int64_t avail = RS_SMEM - rb - 256;
-  const int64_t s = avail / (rb * rows_per_stage);
-  return (int)std::min<int64_t>(8, s);
-}
-
 template <typename T, typename R>
 static int rms_fwd_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
                           float offset, int mode, cudaStream_t st) {
-  const int stages = rs_stages<T>(cols, 1);
-  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && stages >= 2) {
-    const int64_t rb = (cols * (int64_t)sizeof(T) + 127) / 128 * 128;
-    const size_t smem = (size_t)rb * (1 + stages) + 8 * stages + 64;
-    auto kern = rmsnorm_fwd_stream_tma<T, R>;
+  const size_t smem = rs::fwd_smem(cols, (int)sizeof(T));
+  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && smem <= 220 * 1024) {
+    auto kern = rs::rmsnorm_fwd_warp<T, R>;
     LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(rows, 2 * (int64_t)sm_count()));
-    kern<<<grid, RS_THREADS, smem, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode, stages);
-    return check_launch("rmsnorm_fwd_stream_tma");
+    const int64_t warps_needed = (rows + rs::FWD_WARPS - 1) / rs::FWD_WARPS;
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(warps_needed, sm_count()));
+    kern<<<grid, rs::FWD_WARPS * 32, smem, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode);
+    return check_launch("rmsnorm_fwd_warp");
   }
   NormCfg c = pick_cfg<T>(cols, {x, w, y});
   unsigned grid = (unsigned)std::min<int64_t>(rows, 1 << 20);
@@ -511,25 +286,26 @@ static int64_t rms_bwd_grid(int64_t rows) {
 
 template <typename T, typename R>
 static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
-                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st) {
-  const int stages = rs_stages<T>(cols, 2);
+                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used) {
+  const size_t smem = rs::bwd_smem(cols, (int)sizeof(T));
   const int64_t nvec = cols / Vec16<T>::N;
-  const int kmax = (int)((nvec + RS_THREADS - 1) / RS_THREADS);
-  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) && stages >= 2 &&
-      kmax <= 4) {
-    const int64_t rb = (cols * (int64_t)sizeof(T) + 127) / 128 * 128;
-    const size_t smem = (size_t)rb * (1 + 2 * stages) + 8 * stages + 64;
-    int rc = LK_OK;
+  const int kpl = (int)((nvec + 31) / 32);
+  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) &&
+      smem <= 220 * 1024 && kpl <= 16) {
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count(), g));
+    *g_used = grid;
     auto go = [&](auto kern) -> int {
       LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<(unsigned)g, RS_THREADS, smem, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, stages);
-      return check_launch("rmsnorm_bwd_stream_tma");
+      kern<<<grid, rs::BWD_WARPS * 32, smem, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode);
+      return check_launch("rmsnorm_bwd_warp");
     };
-    if (kmax == 1) rc = go(rmsnorm_bwd_stream_tma<T, R, 1>);
-    else if (kmax == 2) rc = go(rmsnorm_bwd_stream_tma<T, R, 2>);
-    else rc = go(rmsnorm_bwd_stream_tma<T, R, 4>);
-    return rc;
+    if (kpl <= 1) return go(rs::rmsnorm_bwd_warp<T, R, 1>);
+    if (kpl <= 2) return go(rs::rmsnorm_bwd_warp<T, R, 2>);
+    if (kpl <= 4) return go(rs::rmsnorm_bwd_warp<T, R, 4>);
+    if (kpl <= 8) return go(rs::rmsnorm_bwd_warp<T, R, 8>);
+    return go(rs::rmsnorm_bwd_warp<T, R, 16>);
   }
+  *g_used = g;
   NormCfg c = pick_cfg<T>(cols, {dy, x, w, dx});
   if (c.reg) {
     LK_KV_DISPATCH(c.kv, KV, { rmsnorm_bwd_reg<T, R, KV><<<(unsigned)g, c.block, 0, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode); });
@@ -584,18 +360,20 @@ extern "C" int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight,
   LK_REQUIRE(rows == 0 || (dy && x && rstd && dx), LK_INVALID_ARGUMENT, "null pointer");
   LK_DISPATCH_FLOAT(dtype, T, {
     const T* w = static_cast<const T*>(weight);
+    int64_t g_used = g;
     if (rows > 0) {
       int rc = casting_mode == LK_CAST_NONE
                    ? rms_bwd_launch<T, T>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                           static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols,
-                                          offset, casting_mode, g, st)
+                                          offset, casting_mode, g, st, &g_used)
                    : rms_bwd_launch<T, float>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                               static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows,
-                                              cols, offset, casting_mode, g, st);
+                                              cols, offset, casting_mode, g, st, &g_used);
       if (rc) return rc;
     }
     if (part) {
-      colsum_partials_kernel<T><<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(part, g, cols, static_cast<T*>(dw));
+      colsum_partials_kernel<T><<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(part, g_used, cols,
+                                                                                static_cast<T*>(dw));
       return check_launch("colsum_partials_kernel");
     }
   });
