@@ -227,11 +227,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
             tma_2d_cg2(mb, fb, b_dst, n0, k0);
             tma_2d_cg2(mb, fb, b_dst + 8192, n0 + 64, k0);
           }
-          // warm L2 one ring-depth ahead so DRAM first-touch latency is off the critical path
-          if (kb + STAGES < kblocks) {
-            tc::prefetch_operand(ma, a_mode, k0 + STAGES * BK, m0);
-            tc::prefetch_operand(mb, b_mode, k0 + STAGES * BK, n0);
-          }
+          // (an L2 prefetch one ring-depth ahead was measured slower: logits 7.3 -> 8.1 ms)
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }

@@ -261,14 +261,19 @@ static bool aligned16_all(std::initializer_list<const void*> ptrs) {
 template <typename T, typename R>
 static int rms_fwd_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
                           float offset, int mode, cudaStream_t st) {
-  const size_t smem = rs::fwd_smem(cols, (int)sizeof(T));
-  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && smem <= 220 * 1024) {
-    auto kern = rs::rmsnorm_fwd_warp<T, R>;
-    LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t warps_needed = (rows + rs::FWD_WARPS - 1) / rs::FWD_WARPS;
-    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(warps_needed, sm_count()));
-    kern<<<grid, rs::FWD_WARPS * 32, smem, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode);
-    return check_launch("rmsnorm_fwd_warp");
+  const int64_t nvec = cols / Vec16<T>::N;
+  if (!getenv("LK_NORM_NO_FAST") && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && nvec <= 32 * 16) {
+    const unsigned grid = (unsigned)((rows + 3) / 4);
+    const int vpl = (int)((nvec + 31) / 32);
+    auto go = [&](auto kern) -> int {
+      kern<<<grid, rs::FWD_THREADS, 0, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode);
+      return check_launch("rmsnorm_fwd_warp");
+    };
+    if (vpl <= 1) return go(rs::rmsnorm_fwd_warp<T, R, 1>);
+    if (vpl <= 2) return go(rs::rmsnorm_fwd_warp<T, R, 2>);
+    if (vpl <= 4) return go(rs::rmsnorm_fwd_warp<T, R, 4>);
+    if (vpl <= 8) return go(rs::rmsnorm_fwd_warp<T, R, 8>);
+    return go(rs::rmsnorm_fwd_warp<T, R, 16>);
   }
   NormCfg c = pick_cfg<T>(cols, {x, w, y});
   unsigned grid = (unsigned)std::min<int64_t>(rows, 1 << 20);
@@ -287,23 +292,16 @@ static int64_t rms_bwd_grid(int64_t rows) {
 template <typename T, typename R>
 static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
                           int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used) {
-  const size_t smem = rs::bwd_smem(cols, (int)sizeof(T));
   const int64_t nvec = cols / Vec16<T>::N;
-  const int kpl = (int)((nvec + 31) / 32);
-  if (!getenv("LK_NORM_NO_TMA") && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) &&
-      smem <= 220 * 1024 && kpl <= 16) {
+  const int vpt = (int)((nvec + rs::BWD_THREADS - 1) / rs::BWD_THREADS);
+  if (!getenv("LK_NORM_NO_FAST") && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) && vpt <= 2) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count(), g));
     *g_used = grid;
-    auto go = [&](auto kern) -> int {
-      LK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      kern<<<grid, rs::BWD_WARPS * 32, smem, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode);
-      return check_launch("rmsnorm_bwd_warp");
-    };
-    if (kpl <= 1) return go(rs::rmsnorm_bwd_warp<T, R, 1>);
-    if (kpl <= 2) return go(rs::rmsnorm_bwd_warp<T, R, 2>);
-    if (kpl <= 4) return go(rs::rmsnorm_bwd_warp<T, R, 4>);
-    if (kpl <= 8) return go(rs::rmsnorm_bwd_warp<T, R, 8>);
-    return go(rs::rmsnorm_bwd_warp<T, R, 16>);
+    if (vpt <= 1)
+      rs::rmsnorm_bwd_rows<T, R, 1, 4><<<grid, rs::BWD_THREADS, 0, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode);
+    else
+      rs::rmsnorm_bwd_rows<T, R, 2, 2><<<grid, rs::BWD_THREADS, 0, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode);
+    return check_launch("rmsnorm_bwd_rows");
   }
   *g_used = g;
   NormCfg c = pick_cfg<T>(cols, {dy, x, w, dx});

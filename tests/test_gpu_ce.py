@@ -86,6 +86,35 @@ def test_ce_large_vocab_bf16_rows_sum_to_zero():
     assert rs.abs().max().item() < 5e-2  # bf16 rounding of ~1e5 entries per row
 
 
+@pytest.mark.parametrize("v,dtype", [(32000, torch.bfloat16), (128256, torch.bfloat16), (256000, torch.bfloat16),
+                                     (128256, torch.float32), (40000, torch.float16), (5003, torch.bfloat16)])
+def test_ce_cluster_path_matches_two_pass_path(v, dtype, monkeypatch):
+    """Single-read cluster kernel (row split over a CTA cluster, DSMEM statistics) vs the two-pass kernel."""
+    rows = 48
+    g = torch.Generator(device="cuda").manual_seed(v)
+    z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(dtype)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    t[::5] = -100
+    kw = dict(label_smoothing=0.1, softcap=20.0, lse_square_scale=1e-4)
+
+    def run():
+        x = z.clone().requires_grad_(True)
+        loss = lk.LigerCrossEntropyLoss(reduction="none", **kw)(x, t)
+        loss.sum().backward()
+        return loss.detach().float(), x.grad.float()
+
+    l1, g1 = run()
+    monkeypatch.setenv("LK_CE_NO_CLUSTER", "1")
+    l2, g2 = run()
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    assert rel_close(l1.cpu().numpy(), l2.cpu().numpy(), tol)[0]
+    assert rel_close(g1.cpu().numpy(), g2.cpu().numpy(), tol)[0]
+    _, rrows, _, rgrad = liger_ref.ce(z[:8].double().cpu().numpy(), t[:8].cpu().numpy(), reduction="none", **kw)
+    assert rel_close(l1[:8].cpu().numpy(), rrows, TOL.get(dtype, 2e-2))[0]
+    assert rel_close(g1[:8].cpu().numpy(), rgrad, TOL.get(dtype, 2e-2))[0]
+    assert torch.all(g1[t == -100] == 0)
+
+
 def test_ce_inplace_and_backward_scale():
     rows, v = 8, 100
     x = torch.randn(rows, v, device="cuda", requires_grad=True)
