@@ -166,7 +166,8 @@ def vocab_parallel_flce(
     t = target.reshape(-1).to(torch.int64).contiguous()
     bt, h = x.shape
     n_valid = ops.count(t, shard.total, ignore_index)
-    gw_acc = torch.zeros(shard.size, h, dtype=torch.float32, device=x.device)
+    acc_dtype = torch.float64 if w_shard.dtype == torch.float64 else torch.float32  # fp32 for the kernels
+    gw_acc = torch.zeros(shard.size, h, dtype=acc_dtype, device=x.device)
     gx = torch.empty(bt, h, dtype=x.dtype, device=x.device)
     loss_rows = torch.empty(bt, dtype=torch.float32, device=x.device)
     kw = dict(ignore_index=ignore_index, label_smoothing=label_smoothing, lse_square_scale=lse_square_scale,
