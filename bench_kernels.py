@@ -46,6 +46,23 @@ def timed(fn, reps, flush):
     return statistics.median(times)
 
 
+def steady(fns, reps):
+    """Back-to-back launches cycling over independent buffer sets (each set's bytes were last
+    touched len(fns)-1 launches earlier, so L2 holds none of them): in-stream cost per launch
+    with launch gaps hidden, as inside a model step."""
+    for f in fns:
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        for f in fns:
+            f()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / (reps * len(fns))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
@@ -76,22 +93,32 @@ def main():
 
     # ---- RMSNorm (x: 8192 x 4096) ----
     if want("rmsnorm"):
-        x = torch.randn(BT, H, device=dev, generator=g).to(bf)
+        sets = []
+        for _ in range(4):
+            x = torch.randn(BT, H, device=dev, generator=g).to(bf)
+            sets.append(dict(x=x, y=torch.empty_like(x), rstd=torch.empty(BT, device=dev),
+                             dy=torch.randn(BT, H, device=dev, generator=g).to(bf), dx=torch.empty_like(x)))
         w = (torch.rand(H, device=dev, generator=g) + 0.5).to(bf)
-        y = torch.empty_like(x)
-        rstd = torch.empty(BT, device=dev)
-        dy = torch.randn(BT, H, device=dev, generator=g).to(bf)
-        dx = torch.empty_like(x)
         dw = torch.empty_like(w)
         ws = torch.empty(L.lk_rmsnorm_bwd_workspace_bytes(BT, H), dtype=torch.uint8, device=dev)
-        f = lambda: _capi.check(L.lk_rmsnorm_fwd(x.data_ptr(), w.data_ptr(), y.data_ptr(), rstd.data_ptr(), BT, H,  # noqa: E731
-                                                 1e-6, 0.0, 0, 1, st()))
-        b = lambda: _capi.check(L.lk_rmsnorm_bwd(dy.data_ptr(), x.data_ptr(), w.data_ptr(), rstd.data_ptr(),  # noqa: E731
-                                                 dx.data_ptr(), dw.data_ptr(), BT, H, 0.0, 0, 1, ws.data_ptr(),
-                                                 ws.numel(), st()))
-        report("rmsnorm_fwd", 2 * BT * H * 2 + H * 2 + BT * 4, timed(f, args.reps, flush))
-        report("rmsnorm_bwd", 3 * BT * H * 2 + H * 2 * 2 + BT * 4, timed(b, args.reps, flush))
-        del x, y, dy, dx
+
+        def mk_f(d):
+            return lambda: _capi.check(L.lk_rmsnorm_fwd(d["x"].data_ptr(), w.data_ptr(), d["y"].data_ptr(),
+                                                        d["rstd"].data_ptr(), BT, H, 1e-6, 0.0, 0, 1, st()))
+
+        def mk_b(d):
+            return lambda: _capi.check(L.lk_rmsnorm_bwd(d["dy"].data_ptr(), d["x"].data_ptr(), w.data_ptr(),
+                                                        d["rstd"].data_ptr(), d["dx"].data_ptr(), dw.data_ptr(), BT,
+                                                        H, 0.0, 0, 1, ws.data_ptr(), ws.numel(), st()))
+        fb = 2 * BT * H * 2 + H * 2 + BT * 4
+        bb = 3 * BT * H * 2 + H * 2 * 2 + BT * 4
+        report("rmsnorm_fwd", fb, timed(mk_f(sets[0]), args.reps, flush),
+               {"steady_ms": (sm_ := steady([mk_f(d) for d in sets], args.reps)),
+                "steady_frac": fb / (sm_ / 1e3) / 1e9 / hbm})
+        report("rmsnorm_bwd", bb, timed(mk_b(sets[0]), args.reps, flush),
+               {"steady_ms": (sm_ := steady([mk_b(d) for d in sets], args.reps)),
+                "steady_frac": bb / (sm_ / 1e3) / 1e9 / hbm})
+        del sets
 
     # ---- RoPE (q: 4 x 2048 x 32 x 128, k: 4 x 2048 x 8 x 128) ----
     if want("rope"):
@@ -136,7 +163,8 @@ def main():
                                                        ws.data_ptr(), ws.numel(), st()))
         ms = timed(f, args.reps, flush)
         report("cross_entropy_fwd_bwd", 2 * rows * V * 2, ms,
-               {"note": "algorithmic bytes = 1 read + 1 write of the logits (the in-place minimum)"})
+               {"note": "algorithmic bytes = 1 read + 1 write of the logits (the in-place minimum)",
+                "steady_ms": (sm_ := steady([f], args.reps)), "steady_frac": 2 * rows * V * 2 / (sm_ / 1e3) / 1e9 / hbm})
     print(json.dumps({"summary": {o["kernel"]: round(o["frac"], 3) for o in out}}), flush=True)
 
 

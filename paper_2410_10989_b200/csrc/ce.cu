@@ -175,7 +175,12 @@ extern "C" int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* tar
   a.label_smoothing = label_smoothing; a.lse_square_scale = lse_square_scale; a.softcap = softcap;
   a.input_capped = 0; a.reduction = reduction; a.compute_grad = compute_grad; a.n_valid = counts;
   a.loss_rows = loss_rows; a.z_loss_rows = z_loss_rows;
-  rc = launch_ce_cluster(a, dtype, st);  // one read + one write per logit when the row fits a cluster
+  // LK_CE_IMPL = ring (default) | cluster | block (one CTA per row, ce_rows_kernel)
+  const char* impl_env = getenv("LK_CE_IMPL");  // read per call so tests can switch paths
+  const char impl = impl_env ? impl_env[0] : 'r';
+  rc = LK_UNSUPPORTED;
+  if (impl == 'r') rc = launch_ce_ring(a, dtype, st);
+  if (rc == LK_UNSUPPORTED && impl == 'c') rc = launch_ce_cluster(a, dtype, st);
   if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(a, dtype, st);
   if (rc) return rc;
   if (loss_sum) { rc = launch_reduce_sum(loss_rows, rows, loss_sum, st); if (rc) return rc; }

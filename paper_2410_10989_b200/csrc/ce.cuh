@@ -206,6 +206,8 @@ __global__ void count_targets_kernel(const int64_t* __restrict__ t, int64_t rows
                                      int64_t ignore_index, unsigned long long* out);
 
 int launch_ce_rows(const CeRowArgs& a, int dtype, cudaStream_t st);
+// Persistent TMA-ring standalone CE (ce_ring.cu, default); LK_UNSUPPORTED if not applicable.
+int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st);
 // Single-read cluster variant for standalone CE (ce_cluster.cu); LK_UNSUPPORTED if not applicable.
 int launch_ce_cluster(const CeRowArgs& a, int dtype, cudaStream_t st);
 int launch_count_targets(const int64_t* t, int64_t rows, int64_t vocab, int64_t ignore_index,

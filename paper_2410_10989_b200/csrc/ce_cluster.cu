@@ -193,7 +193,6 @@ __global__ void __launch_bounds__(BLOCK) ce_cluster_kernel(CeRowArgs a, int64_t 
 
 // Returns LK_UNSUPPORTED when the shape cannot take the cluster path (caller falls back).
 int launch_ce_cluster(const CeRowArgs& a, int dtype, cudaStream_t st) {
-  if (getenv("LK_CE_NO_CLUSTER")) return LK_UNSUPPORTED;
   if (a.rows <= 0 || a.partials || a.row_stats) return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   const int64_t nv = 16 / esz;

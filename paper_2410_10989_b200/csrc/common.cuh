@@ -8,6 +8,8 @@
 #include <string>
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <unordered_map>
 
 #include "../../include/liger_b200.h"
 
@@ -56,6 +58,18 @@ inline int sm_count() {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
   }
   return n;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel (per size increase).
+inline cudaError_t ensure_smem(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> g(mu);
+  int& have = done[fn];
+  if (have >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

@@ -16,6 +16,8 @@
 // grid = 2 x SMs CTAs, contiguous row ranges per CTA.
 #include "common.cuh"
 #include "norm_rowstream.cuh"
+#include "norm_ring.cuh"
+#include "norm_cta.cuh"
 
 namespace lk {
 
@@ -213,15 +215,36 @@ rmsnorm_bwd_stream(const T* dy, const T* __restrict__ x, const T* __restrict__ w
   }
 }
 
-// dw[c] = sum_g part[g, c], fixed order over g (deterministic second stage).
+// dw[c] = sum_g part[g, c] in a fixed order (deterministic second stage).  A CTA owns 32
+// columns (one coalesced 128-byte segment per partial row) and 32 row groups: thread
+// (ty, tx) sums rows ty, ty + 32, ... of column tx with 8 independent accumulators (all of a
+// thread's loads in flight at once), then the 32 group sums are added in ty order.
+// (One thread per column walking ~450 partial rows serially was latency-bound at 16 us.)
 template <typename T>
-__global__ void colsum_partials_kernel(const float* __restrict__ part, int64_t g, int64_t cols,
-                                       T* __restrict__ out) {
-  int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (c >= cols) return;
-  float s = 0.f;
-  for (int64_t i = 0; i < g; ++i) s += part[i * cols + c];
-  out[c] = from_f<T>(s);
+__global__ void __launch_bounds__(1024) colsum_partials_kernel(const float* __restrict__ part, int64_t g,
+                                                               int64_t cols, T* __restrict__ out) {
+  __shared__ float red[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + tx;
+  float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  if (c < cols) {
+    int64_t i = ty;
+    for (; i + 7 * 32 < g; i += 8 * 32) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += part[(i + u * 32) * cols + c];
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (i + u * 32 < g) a[u] += part[(i + u * 32) * cols + c];
+  }
+  red[ty][tx] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  __syncthreads();
+  if (ty == 0 && c < cols) {
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s += red[k][tx];
+    out[c] = from_f<T>(s);
+  }
 }
 
 struct NormCfg {
@@ -258,11 +281,188 @@ static bool aligned16_all(std::initializer_list<const void*> ptrs) {
   return true;
 }
 
+// Implementation choice: LK_NORM_IMPL = ring (default) | warp | generic.
+// LK_NORM_IMPL = cta (default) | ring | warp | generic; read per call so tests can switch.
+enum { IMPL_CTA = 0, IMPL_WARP = 1, IMPL_GENERIC = 2, IMPL_RING = 3 };
+static int norm_impl() {
+  const char* e = getenv("LK_NORM_IMPL");
+  if (getenv("LK_NORM_NO_FAST")) return IMPL_GENERIC;
+  if (!e) return IMPL_CTA;
+  switch (e[0]) {
+    case 'w': return IMPL_WARP;
+    case 'g': return IMPL_GENERIC;
+    case 'r': return IMPL_RING;
+    default: return IMPL_CTA;
+  }
+}
+
+#define LK_VPT8_DISPATCH(vpt, VPT, ...)                     \
+  switch (vpt) {                                            \
+    case 1: { constexpr int VPT = 1; __VA_ARGS__; break; }  \
+    case 2: { constexpr int VPT = 2; __VA_ARGS__; break; }  \
+    case 4: { constexpr int VPT = 4; __VA_ARGS__; break; }  \
+    default: { constexpr int VPT = 8; __VA_ARGS__; break; } \
+  }
+
+// vectors per thread so that a row takes <= `target` threads (VPT <= 8, <= max_threads)
+static int cta_vpt(int64_t nvec, int target, int max_threads) {
+  int v = 1;
+  while (v < 8 && (nvec + v - 1) / v > target) v *= 2;
+  return (nvec + v - 1) / v <= max_threads ? v : 0;
+}
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+
+template <typename T, typename R>
+static int rms_fwd_cta_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
+                              float offset, int mode, cudaStream_t st) {
+  constexpr int NV = Vec16<T>::N;
+  if (cols % NV || !aligned16_all({x, w, y}) || rows > 0x7fffffff || rows * cols > ((int64_t)1 << 40))
+    return LK_UNSUPPORTED;
+  const int64_t nvec = cols / NV;
+  const int vpt = cta_vpt(nvec, env_int("LK_NORM_FWD_THREADS", 128), 256);
+  if (!vpt) return LK_UNSUPPORTED;
+  const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
+  LK_VPT8_DISPATCH(vpt, VPT, {
+    rc::rmsnorm_fwd_cta<T, R, VPT><<<(unsigned)rows, threads, 0, st>>>(x, w, y, rstd, (int)rows, (int)cols, eps,
+                                                                       offset, mode);
+  });
+  return check_launch("rmsnorm_fwd_cta");
+}
+
+template <typename T, typename R>
+static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part,
+                              int64_t rows, int64_t cols, float offset, int mode, int64_t g, cudaStream_t st,
+                              int64_t* g_used) {
+  constexpr int NV = Vec16<T>::N;
+  if (cols % NV || !aligned16_all({dy, x, w, dx}) || rows > 0x7fffffff) return LK_UNSUPPORTED;
+  const int64_t nvec = cols / NV;
+  int rc = LK_OK;
+  if constexpr (std::is_same<T, __nv_bfloat16>::value && std::is_same<R, float>::value) {
+    if (mode == LK_CAST_LLAMA && offset == 0.f && w && !getenv("LK_NORM_NO_BF16_FAST")) {
+      // 128-thread CTAs (VPT = 4 at H = 4096): 82% of HBM vs 78% with 256 threads (profiles/)
+      const int vpt = cta_vpt(nvec, env_int("LK_NORM_BWD_THREADS", 128), 512);
+      if (!vpt) return LK_UNSUPPORTED;
+      const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
+      const int64_t rb = cols * 2;
+      const int slots = (int)std::max<int64_t>(2, std::min<int64_t>(env_int("LK_NORM_BWD_SLOTS", 3),
+                                                                    (96 * 1024) / (2 * rb)));
+      const int smem = (int)(slots * 2 * rb);
+      if (rb % 16 || smem > 200 * 1024) return LK_UNSUPPORTED;
+      const bool exact = nvec == (int64_t)vpt * threads;
+      LK_VPT8_DISPATCH(vpt, VPT, {
+        auto kern = exact ? rc::rmsnorm_bwd_cta_bf16_llama<VPT, true> : rc::rmsnorm_bwd_cta_bf16_llama<VPT, false>;
+        LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), smem));
+        int per_sm = 0;
+        LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
+        const unsigned grid =
+            (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
+        *g_used = grid;
+        kern<<<grid, threads, smem, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, slots);
+        rc = check_launch("rmsnorm_bwd_cta_bf16_llama");
+      });
+      return rc;
+    }
+  }
+  const int vpt = cta_vpt(nvec, env_int("LK_NORM_BWD_THREADS", 256), 512);
+  if (!vpt) return LK_UNSUPPORTED;
+  const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
+  LK_VPT8_DISPATCH(vpt, VPT, {
+    auto kern = rc::rmsnorm_bwd_cta<T, R, VPT>;
+    int per_sm = 0;
+    LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+    per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
+    *g_used = grid;
+    kern<<<grid, threads, 0, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, offset, mode);
+    rc = check_launch("rmsnorm_bwd_cta");
+  });
+  return rc;
+}
+
+#define LK_VPT_DISPATCH(vpt, VPT, ...)                      \
+  switch (vpt) {                                            \
+    case 1: { constexpr int VPT = 1; __VA_ARGS__; break; }  \
+    case 2: { constexpr int VPT = 2; __VA_ARGS__; break; }  \
+    default: { constexpr int VPT = 4; __VA_ARGS__; break; } \
+  }
+
+// Consumer warps and vectors per thread for the ring kernels: nw*32*vpt >= nvec.
+static bool ring_geometry(int64_t nvec, int* nw, int* vpt) {
+  *nw = (int)std::min<int64_t>(rr::MAX_NW, std::max<int64_t>(1, (nvec + 31) / 32));
+  const int64_t per = (nvec + *nw * 32 - 1) / (*nw * 32);
+  if (per > 4) return false;
+  *vpt = per <= 1 ? 1 : (per <= 2 ? 2 : 4);
+  return true;
+}
+
+// Persistent TMA-ring RMSNorm (norm_ring.cuh).  Returns LK_UNSUPPORTED when the shape
+// does not fit (row > 2048 vectors, unaligned rows, fewer than 2 stages).
+template <typename T, typename R>
+static int rms_fwd_ring_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
+                               float offset, int mode, cudaStream_t st) {
+  constexpr int NV = Vec16<T>::N;
+  int nw, vpt;
+  if (cols % NV || !aligned16_all({x, w, y}) || !ring_geometry(cols / NV, &nw, &vpt)) return LK_UNSUPPORTED;
+  const rr::Layout one = rr::layout(cols, sizeof(T), rr::FWD_RB, 1, 0);
+  int stages = (int)((ring::MAX_SMEM - one.total - 256) / (one.stage_bytes + 16));
+  stages = std::min(stages, 16);
+  if (stages < 2) return LK_UNSUPPORTED;
+  const rr::Layout L = rr::layout(cols, sizeof(T), rr::FWD_RB, 1, stages);
+  const int64_t nb = (rows + rr::FWD_RB - 1) / rr::FWD_RB;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nb, sm_count()));
+  int rc = LK_OK;
+  LK_VPT_DISPATCH(vpt, VPT, {
+    auto kern = rr::rmsnorm_fwd_ring<T, R, VPT>;
+    LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), (int)L.total));
+    kern<<<grid, (nw + 1) * 32, L.total, st>>>(x, w, y, rstd, rows, cols, eps, offset, mode, stages);
+    rc = check_launch("rmsnorm_fwd_ring");
+  });
+  return rc;
+}
+
+template <typename T, typename R>
+static int rms_bwd_ring_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part,
+                               int64_t rows, int64_t cols, float offset, int mode, int64_t g, cudaStream_t st,
+                               int64_t* g_used) {
+  constexpr int NV = Vec16<T>::N;
+  int nw, vpt;
+  if (cols % NV || !aligned16_all({dy, x, w, dx}) || !ring_geometry(cols / NV, &nw, &vpt)) return LK_UNSUPPORTED;
+  const rr::Layout one = rr::layout(cols, sizeof(T), rr::BWD_RB, 2, 0);
+  int stages = (int)((ring::MAX_SMEM - one.total - 256) / (one.stage_bytes + 16));
+  stages = std::min(stages, 16);
+  if (stages < 2) return LK_UNSUPPORTED;
+  const rr::Layout L = rr::layout(cols, sizeof(T), rr::BWD_RB, 2, stages);
+  const int64_t nb = (rows + rr::BWD_RB - 1) / rr::BWD_RB;
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>({nb, g, (int64_t)sm_count()}));
+  *g_used = grid;
+  int rc = LK_OK;
+  LK_VPT_DISPATCH(vpt, VPT, {
+    auto kern = rr::rmsnorm_bwd_ring<T, R, VPT>;
+    LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), (int)L.total));
+    kern<<<grid, (nw + 1) * 32, L.total, st>>>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, stages);
+    rc = check_launch("rmsnorm_bwd_ring");
+  });
+  return rc;
+}
+
 template <typename T, typename R>
 static int rms_fwd_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
                           float offset, int mode, cudaStream_t st) {
+  const int impl = norm_impl();
+  if (impl == IMPL_CTA) {
+    int rc = rms_fwd_cta_launch<T, R>(x, w, y, rstd, rows, cols, eps, offset, mode, st);
+    if (rc != LK_UNSUPPORTED) return rc;
+  }
+  if (impl == IMPL_CTA || impl == IMPL_RING) {
+    int rc = rms_fwd_ring_launch<T, R>(x, w, y, rstd, rows, cols, eps, offset, mode, st);
+    if (rc != LK_UNSUPPORTED) return rc;
+  }
   const int64_t nvec = cols / Vec16<T>::N;
-  if (!getenv("LK_NORM_NO_FAST") && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && nvec <= 32 * 16) {
+  if ((impl == IMPL_WARP || impl == IMPL_CTA || impl == IMPL_RING) && cols % Vec16<T>::N == 0 && aligned16_all({x, w, y}) && nvec <= 32 * 16) {
     const unsigned grid = (unsigned)((rows + 3) / 4);
     const int vpl = (int)((nvec + 31) / 32);
     auto go = [&](auto kern) -> int {
@@ -285,16 +485,25 @@ static int rms_fwd_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, i
   return check_launch("rmsnorm_fwd");
 }
 
-static int64_t rms_bwd_grid(int64_t rows) {
-  return std::max<int64_t>(1, std::min<int64_t>(rows, 2 * (int64_t)sm_count()));
+static int64_t rms_bwd_grid(int64_t rows) {  // upper bound of the partial rows any path writes
+  return std::max<int64_t>(1, std::min<int64_t>(rows, 8 * (int64_t)sm_count()));
 }
 
 template <typename T, typename R>
 static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
                           int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used) {
+  const int impl = norm_impl();
+  if (impl == IMPL_CTA) {
+    int rc = rms_bwd_cta_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used);
+    if (rc != LK_UNSUPPORTED) return rc;
+  }
+  if (impl == IMPL_CTA || impl == IMPL_RING) {
+    int rc = rms_bwd_ring_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used);
+    if (rc != LK_UNSUPPORTED) return rc;
+  }
   const int64_t nvec = cols / Vec16<T>::N;
   const int vpt = (int)((nvec + rs::BWD_THREADS - 1) / rs::BWD_THREADS);
-  if (!getenv("LK_NORM_NO_FAST") && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) && vpt <= 2) {
+  if ((impl == IMPL_WARP || impl == IMPL_CTA || impl == IMPL_RING) && cols % Vec16<T>::N == 0 && aligned16_all({dy, x, w, dx}) && vpt <= 2) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count(), g));
     *g_used = grid;
     if (vpt <= 1)
@@ -370,8 +579,8 @@ extern "C" int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight,
       if (rc) return rc;
     }
     if (part) {
-      colsum_partials_kernel<T><<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(part, g_used, cols,
-                                                                                static_cast<T*>(dw));
+      colsum_partials_kernel<T><<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(part, g_used, cols,
+                                                                              static_cast<T*>(dw));
       return check_launch("colsum_partials_kernel");
     }
   });

@@ -101,6 +101,9 @@ rmsnorm_bwd_rows(const T* dy, const T* __restrict__ x, const T* __restrict__ w, 
       unpack<T>(__ldg(reinterpret_cast<const uint4*>(w) + i), wv);
 #pragma unroll
       for (int e = 0; e < NV; ++e) wv[e] += offset;
+    } else {
+#pragma unroll
+      for (int e = 0; e < NV; ++e) wv[e] = 0.f;  // idle columns: 0 * garbage would be NaN in the row dot
     }
   };
   for (int64_t rb = r0; rb < r1; rb += BWD_ROWS) {

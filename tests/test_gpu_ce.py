@@ -87,14 +87,17 @@ def test_ce_large_vocab_bf16_rows_sum_to_zero():
 
 
 @pytest.mark.parametrize("v,dtype", [(32000, torch.bfloat16), (128256, torch.bfloat16), (256000, torch.bfloat16),
-                                     (128256, torch.float32), (40000, torch.float16), (5003, torch.bfloat16)])
-def test_ce_cluster_path_matches_two_pass_path(v, dtype, monkeypatch):
-    """Single-read cluster kernel (row split over a CTA cluster, DSMEM statistics) vs the two-pass kernel."""
-    rows = 48
+                                     (128256, torch.float32), (40000, torch.float16), (5003, torch.bfloat16),
+                                     (1000, torch.float32), (8192, torch.bfloat16)])
+@pytest.mark.parametrize("impl", ["cluster", "block"])
+def test_ce_ring_path_matches_other_paths(v, dtype, impl, monkeypatch):
+    """Default persistent TMA-ring kernel vs the cluster (DSMEM) and one-CTA-per-row kernels, and the oracle."""
+    rows = 300  # > SM count: several rows per persistent CTA
     g = torch.Generator(device="cuda").manual_seed(v)
     z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(dtype)
     t = torch.randint(0, v, (rows,), device="cuda", generator=g)
     t[::5] = -100
+    t[1] = v - 1  # target in the ragged last piece
     kw = dict(label_smoothing=0.1, softcap=20.0, lse_square_scale=1e-4)
 
     def run():
@@ -104,15 +107,43 @@ def test_ce_cluster_path_matches_two_pass_path(v, dtype, monkeypatch):
         return loss.detach().float(), x.grad.float()
 
     l1, g1 = run()
-    monkeypatch.setenv("LK_CE_NO_CLUSTER", "1")
+    monkeypatch.setenv("LK_CE_IMPL", impl)
     l2, g2 = run()
+    monkeypatch.delenv("LK_CE_IMPL")
     tol = 1e-5 if dtype == torch.float32 else 1e-2
-    assert rel_close(l1.cpu().numpy(), l2.cpu().numpy(), tol)[0]
-    assert rel_close(g1.cpu().numpy(), g2.cpu().numpy(), tol)[0]
-    _, rrows, _, rgrad = liger_ref.ce(z[:8].double().cpu().numpy(), t[:8].cpu().numpy(), reduction="none", **kw)
-    assert rel_close(l1[:8].cpu().numpy(), rrows, TOL.get(dtype, 2e-2))[0]
-    assert rel_close(g1[:8].cpu().numpy(), rgrad, TOL.get(dtype, 2e-2))[0]
+    ok, err = rel_close(l1.cpu().numpy(), l2.cpu().numpy(), tol)
+    assert ok, err
+    ok, err = rel_close(g1.cpu().numpy(), g2.cpu().numpy(), tol)
+    assert ok, err
+    sel = [0, 1, 2, 3, 4, 5, 6, 7, 150, 299]
+    _, rrows, _, rgrad = liger_ref.ce(z[sel].double().cpu().numpy(), t[sel].cpu().numpy(), reduction="none", **kw)
+    ok, err = rel_close(l1[sel].cpu().numpy(), rrows, TOL.get(dtype, 2e-2))
+    assert ok, err
+    ok, err = rel_close(g1[sel].cpu().numpy(), rgrad, TOL.get(dtype, 2e-2))
+    assert ok, err
     assert torch.all(g1[t == -100] == 0)
+    assert torch.all(l1[t == -100] == 0)
+
+
+def test_ce_ring_plain_mean_and_no_grad():
+    """Ring kernel without options (no cap / smoothing), MEAN reduction, and the loss-only path."""
+    rows, v = 777, 128256
+    g = torch.Generator(device="cuda").manual_seed(1)
+    z = torch.randn(rows, v, device="cuda", generator=g).to(torch.bfloat16)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    t[::7] = -100
+    x = z.clone().requires_grad_(True)
+    loss = lk.LigerCrossEntropyLoss()(x, t)
+    loss.backward()
+    ref = torch.nn.functional.cross_entropy(z.float(), t, ignore_index=-100)
+    assert abs(loss.item() - ref.item()) <= 2e-3 * abs(ref.item())
+    zr = z.float().requires_grad_(True)
+    torch.nn.functional.cross_entropy(zr, t, ignore_index=-100).backward()
+    ok, err = rel_close(x.grad.float().cpu().numpy(), zr.grad.cpu().numpy(), 2e-2)
+    assert ok, err
+    with torch.no_grad():
+        l2 = lk.LigerCrossEntropyLoss()(z.clone(), t)
+    assert abs(l2.item() - loss.item()) <= 1e-6 * abs(loss.item())
 
 
 def test_ce_inplace_and_backward_scale():

@@ -46,13 +46,55 @@ def test_rmsnorm_bf16_vs_oracle(mode, shape):
     ry, _ = liger_ref.rmsnorm_fwd(x[sel].double().cpu().numpy(), w.double().cpu().numpy(), 1e-6, offset)
     rdx, _ = liger_ref.rmsnorm_bwd(dy[sel].double().cpu().numpy(), x[sel].double().cpu().numpy(),
                                    w.double().cpu().numpy(), 1e-6, offset)
-    assert rel_close(y[sel].float().detach().cpu().numpy(), ry, 2e-2)[0]
-    assert rel_close(xr.grad[sel].float().cpu().numpy(), rdx, 2e-2)[0]
+    ok, err = rel_close(y[sel].float().detach().cpu().numpy(), ry, 2e-2)
+    assert ok, ("y", err)
+    ok, err = rel_close(xr.grad[sel].float().cpu().numpy(), rdx, 2e-2)
+    assert ok, ("dx", err)
     # dW over all rows against a torch fp32 restatement
     xf, dyf = x.float(), dy.float()
     r = torch.rsqrt((xf * xf).mean(1, keepdim=True) + 1e-6)
     rdw = (dyf * xf * r).sum(0)
     assert close(wr.grad, rdw, 2e-2)
+
+
+@pytest.mark.parametrize("impl", ["ring", "warp", "generic"])
+@pytest.mark.parametrize("shape,dtype", [((8192, 4096), torch.bfloat16), ((300, 1000), torch.bfloat16),
+                                         ((37, 1000), torch.bfloat16), ((1000, 2048), torch.float32),
+                                         ((513, 256), torch.float16), ((3, 64), torch.bfloat16)])
+@pytest.mark.parametrize("mode", ["llama", "gemma", "none"])
+def test_rmsnorm_default_matches_other_paths(impl, shape, dtype, mode, monkeypatch):
+    """Default (CTA register) kernels vs the TMA-ring, register-warp and generic kernels."""
+    rows, cols = shape
+    g = torch.Generator(device="cuda").manual_seed(rows * 7 + cols)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(dtype)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(dtype)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(dtype)
+    offset = 1.0 if mode == "gemma" else 0.0
+
+    def run(in_place):
+        xr = x.clone().requires_grad_(True)
+        wr = w.clone().requires_grad_(True)
+        y = lk.liger_rms_norm(xr, wr, 1e-6, offset, mode, in_place)
+        y.backward(dy.clone())
+        return y.detach().float(), xr.grad.float(), wr.grad.float()
+
+    a = run(True)
+    monkeypatch.setenv("LK_NORM_IMPL", impl)
+    b = run(False)
+    monkeypatch.delenv("LK_NORM_IMPL")
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    for name, u, v in zip(("y", "dx", "dw"), a, b):
+        ok, err = rel_close(u.cpu().numpy(), v.cpu().numpy(), tol)
+        assert ok, (name, err)
+    sel = slice(0, min(rows, 256))
+    ry, _ = liger_ref.rmsnorm_fwd(x[sel].double().cpu().numpy(), w.double().cpu().numpy(), 1e-6, offset)
+    rdx, _ = liger_ref.rmsnorm_bwd(dy[sel].double().cpu().numpy(), x[sel].double().cpu().numpy(),
+                                   w.double().cpu().numpy(), 1e-6, offset)
+    rt = 1e-4 if dtype == torch.float32 else 2e-2
+    ok, err = rel_close(a[0][sel].cpu().numpy(), ry, rt)
+    assert ok, ("y vs oracle", err)
+    ok, err = rel_close(a[1][sel].cpu().numpy(), rdx, rt)
+    assert ok, ("dx vs oracle", err)
 
 
 def test_rmsnorm_dw_deterministic_and_batch_linear():
