@@ -59,7 +59,11 @@ __device__ __forceinline__ float2 capped(float2 z, float cap, float inv_cap) {
   }
 }
 
-template <typename T, bool CAP, bool LS>
+// PART: FLCE finalize -- the logits GEMM epilogue already wrote per-(row, 256-column tile)
+// (max, sumexp, sum) partials and the softcapped, rounded logits, so the statistics pass is a
+// combine of ~V/256 partials and only the gradient pass streams the row (one read + one
+// write per logit, rowfuse/flce.py:155-157).
+template <typename T, bool CAP, bool LS, bool PART>
 __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int stages) {
   using P = Pairs<T>;
   constexpr int NP = P::NP;
@@ -74,7 +78,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   const int64_t n_local = rows > b ? (rows - b + G - 1) / G : 0;
   const int64_t row_bytes = n * (int64_t)sizeof(T);
   const int64_t npc = (row_bytes + PIECE - 1) / PIECE;
-  const int passes = a.compute_grad ? 2 : 1;
+  const int passes = PART ? (a.compute_grad ? 1 : 0) : (a.compute_grad ? 2 : 1);
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) { ring::mbar_init(&full[s], 1); ring::mbar_init(&empty[s], NC); }
     ring::fence_init();
@@ -132,14 +136,22 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       float zt = 0.f;
       if (yl >= 0 && yl < n) {
         zt = to_f<T>(xr[yl]);  // read before any pass-2 write of this row (after the barrier below)
-        if (CAP) zt = cap * tanhf(zt * inv_cap);
+        if (CAP && !PART) zt = cap * tanhf(zt * inv_cap);
       }
       sh->zt[par] = zt;
     }
     // ---- pass 1: online (max, sumexp[, sum]) ----
     float m = -INFINITY, se = 0.f;
     float2 sz2 = make_float2(0.f, 0.f);
-    for (int64_t j = 0; j < npc; ++j, cur.next()) {
+    if constexpr (PART) {
+      const float4* pp = a.partials + row * a.n_parts;
+      for (int64_t jp = tid; jp < a.n_parts; jp += NC * 32) {
+        const float4 q = pp[jp];
+        ms_combine(m, se, q.x, q.y);
+        sz2.x += q.z;
+      }
+    }
+    for (int64_t j = 0; j < (PART ? 0 : npc); ++j, cur.next()) {
       const int s = cur.s;
       ring::wait(&full[s], cur.phase);
       const int nvec = (int)(min((int64_t)PIECE, row_bytes - j * PIECE) / 16);
@@ -255,9 +267,11 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
             float2 zz = z[e], dc = make_float2(1.f, 1.f);
             if (CAP) {
               const float2 u = __fmul2_rn(zz, make_float2(inv_cap, inv_cap));
-              const float2 t =
-                  sizeof(T) == 4 ? make_float2(tanhf(u.x), tanhf(u.y)) : make_float2(tanh_fast(u.x), tanh_fast(u.y));
-              zz = __fmul2_rn(t, make_float2(cap, cap));
+              float2 t = u;  // PART: the buffer already holds cap * tanh(z / cap)
+              if (!PART) {
+                t = sizeof(T) == 4 ? make_float2(tanhf(u.x), tanhf(u.y)) : make_float2(tanh_fast(u.x), tanh_fast(u.y));
+                zz = __fmul2_rn(t, make_float2(cap, cap));
+              }
               dc = __ffma2_rn(__fmul2_rn(t, t), make_float2(-1.f, -1.f), make_float2(1.f, 1.f));  // 1 - t^2
             }
             float2 g = __ffma2_rn(ex2(__ffma2_rn(zz, l2e2, nmb)), coef2, neps2);
@@ -279,8 +293,11 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
             }
             float dct = 1.f;
             if (CAP) {
-              const float t = sizeof(T) == 4 ? tanhf(zt * inv_cap) : tanh_fast(zt * inv_cap);
-              zt = cap * t;
+              float t = zt * inv_cap;
+              if (!PART) {
+                t = sizeof(T) == 4 ? tanhf(t) : tanh_fast(t);
+                zt = cap * t;
+              }
               dct = 1.f - t * t;
             }
             const float gt = (ex2(fmaf(zt, L2E, nmb.x)) * coef + neps2.x - hit_s) * dct;
@@ -295,7 +312,9 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
 }  // namespace cer
 
 int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
-  if (a.rows <= 0 || a.partials || a.row_stats || a.input_capped) return LK_UNSUPPORTED;
+  // raw logits (standalone CE) or FLCE finalize (partials + capped logits); not vocab-parallel
+  const bool part = a.partials != nullptr;
+  if (a.rows <= 0 || a.row_stats || (part && !a.input_capped) || (!part && a.input_capped)) return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   if ((a.n_cols * esz) % 16 || (a.ld * esz) % 16 || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;
   const int stages = 13;
@@ -308,10 +327,16 @@ int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
     return check_launch("ce_ring_kernel");
   };
   LK_DISPATCH_FLOAT(dtype, T, {
-    if (cap && ls) return go(cer::ce_ring_kernel<T, true, true>);
-    if (cap) return go(cer::ce_ring_kernel<T, true, false>);
-    if (ls) return go(cer::ce_ring_kernel<T, false, true>);
-    return go(cer::ce_ring_kernel<T, false, false>);
+    if (part) {
+      if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, true>);
+      if (cap) return go(cer::ce_ring_kernel<T, true, false, true>);
+      if (ls) return go(cer::ce_ring_kernel<T, false, true, true>);
+      return go(cer::ce_ring_kernel<T, false, false, true>);
+    }
+    if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, false>);
+    if (cap) return go(cer::ce_ring_kernel<T, true, false, false>);
+    if (ls) return go(cer::ce_ring_kernel<T, false, true, false>);
+    return go(cer::ce_ring_kernel<T, false, false, false>);
   });
   return LK_OK;
 }

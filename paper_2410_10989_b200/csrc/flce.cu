@@ -85,6 +85,7 @@ static int encode_out(CUtensorMap* map, const EpiArgs& e, int dtype) {
       break;
     default: ptr = e.out; odt = LK_F32; break;
   }
+  if (e.kind == EPI_ACCUM && e.acc && e.final_out) return 0;  // acc + tile -> dtype: register epilogue
   const bool is32 = (e.kind == EPI_F32) || (e.kind == EPI_ACCUM && e.acc);
   if (!ptr || e.M < 1 || e.N < 1) return 0;
   if (!is32 && odt != dtype) return 0;  // 16-bit path stores the GEMM's own dtype
@@ -188,6 +189,8 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
 }  // namespace tc
 
 // ------------------------------------------------------------- planning ----
+static bool separate_cast() { return getenv("LK_FLCE_SEPARATE_CAST") != nullptr; }
+
 static int64_t next_pow2(int64_t n) {
   int64_t p = 1;
   while (p < n) p <<= 1;
@@ -356,7 +359,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {
       ProfScope ps(1, st);
-      rc = launch_ce_rows(ce, dt, st);
+      rc = tc && !getenv("LK_FLCE_FINALIZE_BLOCK") ? launch_ce_ring(ce, dt, st) : LK_UNSUPPORTED;
+      if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dt, st);
     }
     if (rc) return rc;
     if (!want_grad) continue;
@@ -376,13 +380,16 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     // the loop.  fp32 weights accumulate in grad_w itself.
     EpiArgs we{};
     we.kind = EPI_ACCUM; we.out_dtype = dt; we.out = a->grad_w; we.ldo = H; we.M = V; we.N = H; we.alpha = 1.f;
-    (void)last;
     if (dt == LK_F32) {
       we.acc = static_cast<float*>(a->grad_w); we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
     } else if (L.nchunks == 1) {
       we.acc = nullptr; we.ldacc = H; we.beta = 0; we.final_out = 1;
     } else {
-      we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
+      // last chunk: grad_w = dtype(acc + tile) straight from the epilogue (register path),
+      // instead of a TMA reduce-add into acc and a separate cast pass: -3.15 GB of HBM
+      // traffic at cfg2 (LK_FLCE_SEPARATE_CAST=1 restores the old order for comparison)
+      const bool fold = last && !separate_cast();
+      we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = fold ? 1 : 0;
     }
     ProfScope ps_bwd(2, st);
     if (tc) {
@@ -418,7 +425,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (rc) return rc;
   }
   ProfScope ps_tail(3, st);
-  if (want_grad && a->grad_w && dt != LK_F32 && L.nchunks > 1) {
+  if (want_grad && a->grad_w && dt != LK_F32 && L.nchunks > 1 && separate_cast()) {
     rc = launch_cast_f32(dwacc, a->grad_w, V * H, dt, st);
     if (rc) return rc;
   }

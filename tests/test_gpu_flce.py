@@ -121,6 +121,28 @@ def test_bf16_ragged_shapes_and_bias():
     assert rel_close(gb.float().cpu().numpy(), rgb, 2e-2)[0]
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(softcap=5.0),
+                                dict(lse_square_scale=1e-4, reduction="sum")])
+@pytest.mark.parametrize("env", ["LK_FLCE_FINALIZE_BLOCK", "LK_FLCE_SEPARATE_CAST"])
+def test_ring_finalize_and_folded_dw_cast_match_reference_paths(kw, env, monkeypatch):
+    """Default path (TMA-ring finalize, dW cast folded into the last chunk's epilogue) vs the
+    one-CTA-per-row finalize / separate cast kernel, and the oracle."""
+    xb, wb, tb, x, w, t = bf16_problem(1000, 256, 4096, seed=11)
+    a = flce(xb, wb, tb, chunk_rows=256, **kw)
+    monkeypatch.setenv(env, "1")
+    b = flce(xb, wb, tb, chunk_rows=256, **kw)
+    monkeypatch.delenv(env)
+    assert rel_err(a[0], b[0]) < 1e-5
+    assert close(a[2], b[2], 1e-2) and close(a[3], b[3], 1e-2)
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, **kw)
+    assert rel_close(a[0].item(), ref_loss, 2e-2)[0]
+    ok, err = rel_close(a[2].float().cpu().numpy(), rgx, 2e-2)
+    assert ok, err
+    ok, err = rel_close(a[3].float().cpu().numpy(), rgw, 2e-2)
+    assert ok, err
+    assert torch.all(a[2][tb == -100] == 0)
+
+
 def test_tcgen05_matches_simt_path():
     xb, wb, tb, *_ = bf16_problem(512, 256, 2048, seed=3)
     a = flce(xb, wb, tb, chunk_rows=256)
