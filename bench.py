@@ -177,7 +177,7 @@ def run_ours(args):
 
     import paper_2410_10989_b200 as lk
     from paper_2410_10989_b200 import _capi, _utils
-    from paper_2410_10989_b200.distributed import token_sharded_flce
+    from paper_2410_10989_b200.distributed import token_sharded_flce, vocab_parallel_flce, vocab_shard
     from paper_2410_10989_b200.fused_linear_cross_entropy import (
         flce_plan,
         flce_workspace_bytes,
@@ -185,22 +185,35 @@ def run_ours(args):
     )
 
     rank, world, local = env_rank()
-    if world > 1:
+    vocab_mode = args.mode == "vocab"
+    if world > 1 or vocab_mode:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world == 1:  # vocab-parallel at N=1: a one-rank group so the same code path runs
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
+            dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     L = _capi.load()
     bt, h, v = args.bt, args.hidden, args.vocab
 
-    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    # token mode: every rank its own BT tokens (weak scaling); vocab mode: one global problem,
+    # W rows sharded over ranks (strong scaling of the GEMM work)
+    g = torch.Generator(device=dev).manual_seed(1000 + (0 if vocab_mode else rank))
     x = (torch.rand(bt, h, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
     w = ((torch.rand(v, h, device=dev, generator=g) * 2 - 1) / 64.0).to(torch.bfloat16)
     t = torch.randint(0, v, (bt,), device=dev, generator=g)
     t[torch.rand(bt, device=dev, generator=g) < IGNORE_FRAC] = -100
     chunk = args.chunk_rows or flce_plan(bt, h, v)[0]
+    if vocab_mode:
+        shard = vocab_shard(v, rank, world)
+        w = w[shard.offset:shard.offset + shard.size].contiguous()
 
     def step():
+        if vocab_mode:
+            return vocab_parallel_flce(x, w, t, shard, chunk_rows=chunk)
         if world > 1:
             return token_sharded_flce(x, w, t, chunk_rows=chunk)
         return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True,
@@ -222,7 +235,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     peak_extra = torch.cuda.max_memory_allocated(dev) - base
     del out
-    out_bytes = bt * h * 2 + v * h * 2
+    out_bytes = bt * h * 2 + w.shape[0] * h * 2
     ws_bytes = flce_workspace_bytes(bt, h, v, torch.bfloat16, chunk, True)
     logits_chunk_bytes = chunk * (-(-v // 64) * 64) * 2
 
@@ -254,8 +267,9 @@ def run_ours(args):
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     ms = float(tmax.item())
-    value = world * bt * args.steps / (ms / 1e3)
-    flop_step = 6.0 * bt * h * v
+    tokens_per_step = bt if vocab_mode else world * bt
+    value = tokens_per_step * args.steps / (ms / 1e3)
+    flop_step = 6.0 * bt * h * v / (world if vocab_mode else 1)  # per rank
 
     # ---- e2e through the public module, host buffers, H2D/D2H inside the timed region ----
     xh = x.cpu().pin_memory()
@@ -266,7 +280,10 @@ def run_ours(args):
     def e2e_step():
         xd = xh.to(dev, non_blocking=True).requires_grad_(True)
         td = th.to(dev, non_blocking=True)
-        if world > 1:
+        if vocab_mode:
+            loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk)
+            val = loss.item()
+        elif world > 1:
             loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk)
             val = loss.item()
         else:
@@ -289,17 +306,20 @@ def run_ours(args):
     ems = torch.tensor([e0.elapsed_time(e1)], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(ems, op=dist.ReduceOp.MAX)
-    e2e_value = world * bt * args.steps / (float(ems.item()) / 1e3)
+    e2e_value = tokens_per_step * args.steps / (float(ems.item()) / 1e3)
 
     peaks, peak_src = measured_peaks()
     gemm_ms = (ms4[0] + ms4[2]) / args.steps
     achieved = flop_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak_sus = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-    traffic = None
-    prof = ROOT / "profiles" / "r01_gemm_ncu_summary.json"
+    # DRAM bytes of the GEMM launches from the committed ncu --set full capture of one step
+    # (scripts/profile_json.py): per launch on average, like `achieved`
+    traffic, traffic_step = None, None
+    prof = ROOT / "profiles" / "r01_flce_step.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get("dram_bytes_per_step")
+            pj = json.loads(prof.read_text())
+            traffic, traffic_step = pj.get("gemm_dram_bytes_per_launch"), pj.get("dram_bytes_per_step")
         except Exception:
             traffic = None
 
@@ -313,18 +333,23 @@ def run_ours(args):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if vocab_mode else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform X, W, 10% ignore_index targets)",
             "config": {
                 "workload": WORKLOAD, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
-                "num_chunks": -(-bt // chunk), "global_tokens": bt * world,
-                "parallelism": f"token-sharded dp{world}" if world > 1 else "single GPU",
+                "num_chunks": -(-bt // chunk), "global_tokens": tokens_per_step,
+                "parallelism": (f"vocab-parallel vp{world}" if vocab_mode else
+                                (f"token-sharded dp{world}" if world > 1 else "single GPU")),
                 "l2": "inputs larger than L2 (W = 1.05 GB bf16 re-streamed every chunk)",
             },
             "roofline": {
                 "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
                 "frac": (achieved / peak_sus) if achieved else None, "traffic": traffic,
-                "kernel": "lk::tc::gemm_kernel<bf16> (logits + backward launches)",
+                "kernel": "tc2::gemm2_kernel<bf16> (CTA-pair tcgen05; logits + backward launches)",
+                "traffic_unit": "DRAM bytes per GEMM launch (avg over one step's launches, ncu)",
+                "traffic_per_step": traffic_step,
+                "algorithmic_flop_per_step": flop_step,
                 "peak_source": f"{peak_src} bf16_tflops_sustained", "peak_burst": float(peaks["bf16_tflops"]),
                 "frac_of_burst": (achieved / float(peaks["bf16_tflops"])) if achieved else None,
                 "step_tflops": flop_step / (ms / args.steps / 1e3) / 1e12,
@@ -343,7 +368,7 @@ def run_ours(args):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or vocab_mode:
         dist.destroy_process_group()
 
 
@@ -357,6 +382,8 @@ def main():
     ap.add_argument("--hidden", type=int, default=H)
     ap.add_argument("--vocab", type=int, default=V)
     ap.add_argument("--chunk-rows", type=int, default=0)
+    ap.add_argument("--mode", choices=["token", "vocab"], default="token",
+                    help="multi-GPU shard mode: token-sharded (default, weak scaling) or vocab-parallel (strong)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")

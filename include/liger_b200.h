@@ -124,7 +124,7 @@ int lk_scale_rows(void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
  * Layout follows Liger: x[BT, H], weight[V, H] (rowfuse stores W as (H, V); the
  * Python adapter transposes for the oracle).  Gradients are produced during the
  * forward: grad_x[BT, H] in x's dtype, grad_w[V, H] in weight's dtype (accumulated
- * in fp32 in the workspace across chunks).  Either grad pointer may be NULL to
+ * across chunks per grad_w_accum below).  Either grad pointer may be NULL to
  * skip that gradient.  chunk_rows <= 0 selects the B200 chunk policy
  * (lk_flce_plan); otherwise any positive row count is honoured (the reference's
  * ChunkPlan.with_chunk_rows override, rowfuse/flce.py:58-66).
@@ -159,13 +159,26 @@ typedef struct {
   /* Token-sharded mode: device int64 holding the GLOBAL non-ignored count used as
    * the MEAN denominator (all-reduced by the caller); NULL = local count. */
   const int64_t* mean_count;
+  /* grad_w accumulation across chunks (Liger's accum_dtype,
+   * LK/ops/fused_linear_cross_entropy.py:64-69): LK_ACCUM_AUTO (0, the zero-initialised
+   * default) = weight dtype when the plan has <= LK_ACCUM_AUTO_MAX_CHUNKS chunks (a bf16
+   * TMA reduce-add in L2, no fp32 workspace, peak memory ~ one logits chunk), else fp32;
+   * LK_ACCUM_FP32 = fp32 workspace accumulator; LK_ACCUM_WEIGHT_DTYPE = always the weight
+   * dtype (Liger's accum_dtype=None semantics). */
+  int grad_w_accum;
 } lk_flce_args;
+
+enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };
+#define LK_ACCUM_AUTO_MAX_CHUNKS 8
 
 /* B200 chunk policy.  Writes the chunk row count and number of chunks. */
 int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t* chunk_rows,
                  int64_t* num_chunks);
 size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
                                int64_t chunk_rows, int has_grad_w);
+/* Same, for an explicit grad_w_accum mode (lk_flce_workspace_bytes assumes LK_ACCUM_AUTO). */
+size_t lk_flce_workspace_bytes_ex(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
+                                  int64_t chunk_rows, int has_grad_w, int grad_w_accum);
 int lk_flce_forward_backward(const lk_flce_args* args);
 
 /*
@@ -230,6 +243,11 @@ int lk_geglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* s
 int lk_gemm_test(const void* a, const void* b, float* d, int64_t m, int64_t n, int64_t k,
                  int layout, int dtype, int use_tcgen05, void* workspace, size_t workspace_bytes,
                  void* stream);
+/* Test hook for the 16-bit accumulate epilogue: d16[m, n] (weight dtype) = A.B^T
+ * (beta = 0, TMA store) or d16 += A.B^T (beta = 1, TMA reduce-add in L2; reduce = 0
+ * selects the register read-add-round path), K-major operands, tcgen05. */
+int lk_gemm_test_accum16(const void* a, const void* b, void* d16, int64_t m, int64_t n, int64_t k, int dtype,
+                         int beta, int use_tma_reduce, void* workspace, size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -28,6 +28,7 @@ c_fp = C.POINTER(C.c_float)
 LK_F32, LK_BF16, LK_F16 = 0, 1, 2
 REDUCTIONS = {"none": 0, "mean": 1, "sum": 2}
 CASTING = {"llama": 0, "gemma": 1, "none": 2}
+LK_ACCUM_AUTO, LK_ACCUM_FP32, LK_ACCUM_WEIGHT_DTYPE = 0, 1, 2
 
 
 class FlceArgs(C.Structure):
@@ -61,6 +62,7 @@ class FlceArgs(C.Structure):
         ("stream", c_void),
         ("force_simt", c_int),
         ("mean_count", c_void),
+        ("grad_w_accum", c_int),
     ]
 
 
@@ -73,6 +75,7 @@ SIGNATURES: dict[str, tuple] = {
     "lk_profile_collect": (c_int, [C.POINTER(C.c_double), c_i64p]),
     "lk_launch_count": (c_i64, []),
     "lk_cross_entropy_workspace_bytes": (c_size, [c_i64]),
+    "lk_flce_workspace_bytes_ex": (c_size, [c_i64, c_i64, c_i64, c_int, c_i64, c_int, c_int]),
     "lk_cross_entropy_fwd": (
         c_int,
         [c_void, c_i64, c_void, c_i64, c_i64, c_int, c_i64, c_float, c_float, c_float, c_int, c_int,
@@ -113,6 +116,8 @@ SIGNATURES: dict[str, tuple] = {
     "lk_swiglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_geglu_fwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_geglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
+    "lk_gemm_test_accum16": (c_int, [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_void, c_size,
+                                     c_void]),
     "lk_gemm_test": (
         c_int, [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_void, c_size, c_void]
     ),

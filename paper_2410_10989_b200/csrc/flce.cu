@@ -234,8 +234,15 @@ static bool use_tc_path(int dtype, int64_t hidden, const void* x, const void* w,
 #endif
 }
 
+// Weight-dtype grad_w accumulation across chunks (LK_ACCUM_* in include/liger_b200.h).
+static bool wdtype_accum(int mode, int dtype, int64_t nchunks, bool tc) {
+  if (dtype == LK_F32 || nchunks <= 1 || !tc) return false;  // SIMT path keeps the fp32 accumulator
+  if (mode == LK_ACCUM_WEIGHT_DTYPE) return true;
+  return mode == LK_ACCUM_AUTO && nchunks <= LK_ACCUM_AUTO_MAX_CHUNKS;
+}
+
 static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t chunk_rows,
-                              bool has_grad_w, bool has_bias_grad, bool tc) {
+                              bool has_grad_w, bool has_bias_grad, bool tc, int accum_mode) {
   FlceLayout L{};
   L.C = chunk_rows > 0 ? chunk_rows : b200_chunk_rows(bt, hidden, vocab, dtype);
   L.C = std::max<int64_t>(1, std::min<int64_t>(L.C, std::max<int64_t>(bt, 1)));
@@ -243,7 +250,7 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   L.ldz = ld_logits(vocab);
   L.nparts = (vocab + tc::BN - 1) / tc::BN;
   L.tc = tc;
-  L.need_acc = has_grad_w && dtype != LK_F32 && L.nchunks > 1;
+  L.need_acc = has_grad_w && dtype != LK_F32 && L.nchunks > 1 && !wdtype_accum(accum_mode, dtype, L.nchunks, tc);
   L.need_bias_acc = has_bias_grad;
   size_t off = 0;
   auto take = [&](size_t bytes) { off = align_up(off, 1024); size_t o = off; off += bytes; return o; };
@@ -275,7 +282,13 @@ extern "C" int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype
 extern "C" size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
                                           int64_t chunk_rows, int has_grad_w) {
   bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
-  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc).total;
+  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, LK_ACCUM_AUTO).total;
+}
+
+extern "C" size_t lk_flce_workspace_bytes_ex(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
+                                             int64_t chunk_rows, int has_grad_w, int grad_w_accum) {
+  bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
+  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, grad_w_accum).total;
 }
 
 extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
@@ -292,7 +305,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   cudaStream_t st = as_stream(a->stream);
   const bool tc = use_tc_path(dt, H, a->x, a->weight, a->force_simt);
   const bool want_grad = a->grad_x || a->grad_w || a->grad_bias;
-  FlceLayout L = flce_layout(BT, H, V, dt, a->chunk_rows, a->grad_w != nullptr, a->grad_bias != nullptr, tc);
+  LK_REQUIRE(a->grad_w_accum >= LK_ACCUM_AUTO && a->grad_w_accum <= LK_ACCUM_WEIGHT_DTYPE, LK_INVALID_ARGUMENT,
+             "bad grad_w_accum");
+  FlceLayout L = flce_layout(BT, H, V, dt, a->chunk_rows, a->grad_w != nullptr, a->grad_bias != nullptr, tc,
+                             a->grad_w_accum);
+  const bool wacc = a->grad_w && wdtype_accum(a->grad_w_accum, dt, L.nchunks, tc);
   LK_REQUIRE(a->workspace && a->workspace_bytes >= L.total, LK_INVALID_ARGUMENT,
              "workspace too small: need " + std::to_string(L.total) + " bytes");
   char* ws = static_cast<char*>(a->workspace);
@@ -384,6 +401,10 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
       we.acc = static_cast<float*>(a->grad_w); we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
     } else if (L.nchunks == 1) {
       we.acc = nullptr; we.ldacc = H; we.beta = 0; we.final_out = 1;
+    } else if (wacc) {
+      // accumulate in the weight dtype inside grad_w: first chunk stores, later chunks
+      // TMA reduce-add (bf16/fp16 add in L2) -- Liger's accum_dtype=None order
+      we.acc = nullptr; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = 0;
     } else {
       // last chunk: grad_w = dtype(acc + tile) straight from the epilogue (register path),
       // instead of a TMA reduce-add into acc and a separate cast pass: -3.15 GB of HBM
@@ -425,7 +446,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (rc) return rc;
   }
   ProfScope ps_tail(3, st);
-  if (want_grad && a->grad_w && dt != LK_F32 && L.nchunks > 1 && separate_cast()) {
+  if (want_grad && a->grad_w && dt != LK_F32 && L.nchunks > 1 && !wacc && separate_cast()) {
     rc = launch_cast_f32(dwacc, a->grad_w, V * H, dt, st);
     if (rc) return rc;
   }
@@ -498,7 +519,6 @@ extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, cons
                                    void* grad_x_partial_f32, float* grad_w_accum, int accumulate, void* workspace,
                                    size_t workspace_bytes, void* stream) {
   LK_REQUIRE(rows >= 0 && hidden >= 1 && vocab_local >= 1, LK_SIZE_MISMATCH, "bad sizes");
-  (void)workspace; (void)workspace_bytes;
   if (rows == 0) return LK_OK;
   cudaStream_t st = as_stream(stream);
   const int64_t ldz = ld_logits(vocab_local);
@@ -517,8 +537,33 @@ extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, cons
   EpiArgs we{};
   we.kind = EPI_ACCUM; we.out_dtype = LK_F32; we.acc = grad_w_accum; we.ldacc = hidden;
   we.beta = accumulate ? 1 : 0; we.M = vocab_local; we.N = hidden;
-  // The fp32 dX-partial store uses the SIMT epilogue contract; both GEMMs run through
-  // the generic launcher so the partial stays fp32 for the all-reduce.
+  const bool tc = use_tc_path(dtype, hidden, x, weight_shard, 0) && workspace && workspace_bytes >= 64;
+  if (tc) {
+    // both GEMMs in one persistent tcgen05 launch, as in the token-local FLCE backward:
+    // dX partial (fp32, all-reduced by the caller) = dZ W_shard; dW_shard (+)= dZ^T X (fp32)
+    tc::TmaOperand As[2], Bs[2];
+    tc::Problem Ps[2];
+    int np = 0;
+    if (grad_x_partial_f32) {
+      xe.kind = EPI_F32;
+      As[np] = {logits_buf, vocab_local, rows, ldz, 0};
+      Bs[np] = {weight_shard, hidden, vocab_local, hidden, 1};
+      Ps[np] = tc::Problem{};
+      Ps[np].M = rows; Ps[np].N = hidden; Ps[np].K = vocab_local; Ps[np].n_fast = 0; Ps[np].epi = xe;
+      ++np;
+    }
+    if (grad_w_accum) {
+      As[np] = {logits_buf, vocab_local, rows, ldz, 1};
+      Bs[np] = {x, hidden, rows, hidden, 1};
+      Ps[np] = tc::Problem{};
+      Ps[np].M = vocab_local; Ps[np].N = hidden; Ps[np].K = rows; Ps[np].n_fast = 1; Ps[np].epi = we;
+      ++np;
+    }
+    if (!np) return LK_OK;
+    int* sched = static_cast<int*>(workspace);
+    LK_CUDA(cudaMemsetAsync(sched, 0, 64, st));
+    return tc::launch_tc_gemm(As, Bs, Ps, np, dtype, sched, st);
+  }
   if (grad_x_partial_f32) {
     Operand A{logits_buf, ldz, 1}, B{weight_shard, 1, hidden};
     rc = launch_simt_gemm(A, B, rows, hidden, vocab_local, dtype, xe, st);
@@ -560,4 +605,26 @@ extern "C" int lk_gemm_test(const void* a, const void* b, float* d, int64_t m, i
   else if (layout == 1) { A = {a, k, 1}; B = {b, 1, n}; }
   else { A = {a, 1, m}; B = {b, 1, n}; }
   return launch_simt_gemm(A, B, m, n, k, dtype, e, st);
+}
+
+extern "C" int lk_gemm_test_accum16(const void* a, const void* b, void* d16, int64_t m, int64_t n, int64_t k,
+                                    int dtype, int beta, int use_tma_reduce, void* workspace,
+                                    size_t workspace_bytes, void* stream) {
+#ifdef LK_HAS_TCGEN05
+  LK_REQUIRE(a && b && d16 && workspace && workspace_bytes >= 64, LK_INVALID_ARGUMENT, "null pointer / workspace");
+  cudaStream_t st = as_stream(stream);
+  LK_CUDA(cudaMemsetAsync(workspace, 0, 64, st));
+  EpiArgs e{};
+  e.kind = EPI_ACCUM; e.out_dtype = dtype; e.out = d16; e.ldo = n; e.M = m; e.N = n; e.alpha = 1.f;
+  e.acc = nullptr; e.ldacc = n; e.beta = beta; e.final_out = 0;
+  tc::TmaOperand A{a, k, m, k, 0}, B{b, k, n, k, 0};
+  tc::Problem P{};
+  P.M = m; P.N = n; P.K = k; P.n_fast = 0; P.epi = e;
+  if (!use_tma_reduce) setenv("LK_NO_TMA_EPILOGUE", "1", 1);
+  int rc = tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st);
+  if (!use_tma_reduce) unsetenv("LK_NO_TMA_EPILOGUE");
+  return rc;
+#else
+  return fail(LK_UNSUPPORTED, "built without tcgen05");
+#endif
 }

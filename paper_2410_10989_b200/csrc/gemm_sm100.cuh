@@ -301,6 +301,22 @@ __device__ __forceinline__ void epi_store(const EpiArgs& e, int64_t grow, int64_
 template <typename T>
 __device__ __forceinline__ void epi_accum(const EpiArgs& e, int64_t grow, int64_t n0, uint32_t taddr) {
   const bool row_ok = grow < e.M;
+  if (!e.acc) {  // weight-dtype accumulation directly in `out` (register fallback of the TMA reduce-add)
+    T* orow = static_cast<T*>(e.out) + grow * e.ldo;
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      tmem_ld32(taddr + c * 32, r);
+      tmem_wait_ld();
+      if (!row_ok) continue;
+      const int64_t col0 = n0 + c * 32;
+      for (int j = 0; j < 32 && col0 + j < e.N; ++j) {
+        const float a = e.beta ? to_f<T>(orow[col0 + j]) : 0.f;
+        orow[col0 + j] = from_f<T>(a + e.alpha * __uint_as_float(r[j]));
+      }
+    }
+    return;
+  }
   float* arow = e.acc + grow * e.ldacc;
   T* orow = static_cast<T*>(e.out) + grow * e.ldo;
   const bool vec_ok = (e.ldacc % 4) == 0 && (!e.final_out || (e.ldo % 8) == 0);
@@ -531,7 +547,8 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
     }
     const uint32_t buf = sg.acquire(lane);
     stage_row(buf, lane, w);
-    sg.flush(omap, buf, (int)col0, row0, false, lane);
+    // EPI_ACCUM into a 16-bit grad_w (weight-dtype accumulation): later chunks reduce-add
+    sg.flush(omap, buf, (int)col0, row0, !LOGITS && e.kind == EPI_ACCUM && e.beta != 0, lane);
   }
   if (LOGITS && row_ok) e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
 }

@@ -40,9 +40,11 @@ def flce_plan(bt: int, hidden: int, vocab: int, dtype: torch.dtype = torch.bfloa
     return int(c.value), int(n.value)
 
 
-def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=None, has_grad_w=True) -> int:
+def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=None, has_grad_w=True,
+                         accum=0) -> int:
     code = {torch.float32: 0, torch.bfloat16: 1, torch.float16: 2}[dtype]
-    return int(lib().lk_flce_workspace_bytes(bt, hidden, vocab, code, int(chunk_rows or 0), int(has_grad_w)))
+    return int(lib().lk_flce_workspace_bytes_ex(bt, hidden, vocab, code, int(chunk_rows or 0), int(has_grad_w),
+                                                int(accum)))
 
 
 def fused_linear_cross_entropy_forward(
@@ -69,10 +71,14 @@ def fused_linear_cross_entropy_forward(
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
-    Same return tuple as LK/ops/fused_linear_cross_entropy.py:17-244.  grad_weight is
-    accumulated in fp32 across chunks regardless of accum_dtype (>= Liger precision) and
-    returned in weight.dtype, as Liger does.  `mean_count` (CUDA int64 scalar) overrides
-    the MEAN denominator with a global non-ignored count (token-sharded mode).
+    Same return tuple as LK/ops/fused_linear_cross_entropy.py:17-244.  grad_weight across
+    chunks (LK/ops/fused_linear_cross_entropy.py:64-69): accum_dtype=torch.float32 -> fp32
+    workspace accumulator; accum_dtype=weight.dtype -> accumulated in the weight dtype
+    (Liger's accum_dtype=None order, a TMA reduce-add in L2); accum_dtype=None -> the
+    weight dtype when the plan has <= 8 chunks (no fp32 workspace: peak memory ~ one
+    logits chunk), fp32 beyond that.  Returned in weight.dtype, as Liger does.
+    `mean_count` (CUDA int64 scalar) overrides the MEAN denominator with a global
+    non-ignored count (token-sharded mode).
     """
     if ce_weight is not None:
         raise errors.UnsupportedOption("ce_weight is not implemented in the B200 build")
@@ -116,7 +122,17 @@ def fused_linear_cross_entropy_forward(
     L = lib()
     dt = dtype_code(x)
     cr = int(chunk_rows or 0)
-    ws = workspace(L.lk_flce_workspace_bytes(bt, h, v, dt, cr, int(grad_w is not None)), dev)
+    if force_simt:
+        accum = _capi.LK_ACCUM_FP32  # the SIMT (fp32 parity) GEMM accumulates dW in an fp32 workspace
+    elif accum_dtype is None:
+        accum = _capi.LK_ACCUM_AUTO
+    elif accum_dtype == torch.float32:
+        accum = _capi.LK_ACCUM_FP32
+    elif accum_dtype == weight.dtype:
+        accum = _capi.LK_ACCUM_WEIGHT_DTYPE
+    else:
+        raise errors.UnsupportedOption(f"accum_dtype {accum_dtype}: use None, torch.float32 or the weight dtype")
+    ws = workspace(L.lk_flce_workspace_bytes_ex(bt, h, v, dt, cr, int(grad_w is not None), accum), dev)
     args = _capi.FlceArgs(
         x=ptr(x), weight=ptr(w), target=ptr(t), bias=ptr(b), bt=bt, hidden=h, vocab=v, dtype=dt,
         ignore_index=int(ignore_index), label_smoothing=float(label_smoothing),
@@ -125,7 +141,7 @@ def fused_linear_cross_entropy_forward(
         z_loss_rows=ptr(z_rows), z_loss_sum=ptr(z_sum), grad_x=ptr(grad_x), grad_w=ptr(grad_w),
         grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=ptr(ws), workspace_bytes=ws.numel(),
         stream=stream_of(x), force_simt=int(bool(force_simt)),
-        mean_count=ptr(mean_count) if mean_count is not None else None,
+        mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
     )
     if mean_count is not None and (mean_count.dtype != torch.int64 or not mean_count.is_cuda):
         raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")

@@ -52,10 +52,17 @@ def test_plan_and_workspace_queries():
     assert lib.lk_flce_plan(1024, 512, 4096, 0, C.byref(c), C.byref(n)) == 0
     assert (c.value, n.value) == (1024, 1)
     assert lib.lk_flce_plan(0, 4096, 128256, 1, C.byref(c), C.byref(n)) == 3  # SIZE_MISMATCH
-    ws = lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 0, 1)
     chunk = 2048 * 128256 * 2
     dw_acc = 128256 * 4096 * 4
-    assert chunk + dw_acc < ws < chunk + dw_acc + 64 * 2**20
+    # default (LK_ACCUM_AUTO, 4 chunks): grad_w accumulates in bf16 -> workspace ~ one logits chunk
+    ws = lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 0, 1)
+    assert chunk < ws < chunk + 64 * 2**20
+    assert lib.lk_flce_workspace_bytes_ex(8192, 4096, 128256, 1, 0, 1, _capi.LK_ACCUM_AUTO) == ws
+    assert lib.lk_flce_workspace_bytes_ex(8192, 4096, 128256, 1, 0, 1, _capi.LK_ACCUM_WEIGHT_DTYPE) == ws
+    ws32 = lib.lk_flce_workspace_bytes_ex(8192, 4096, 128256, 1, 0, 1, _capi.LK_ACCUM_FP32)
+    assert chunk + dw_acc < ws32 < chunk + dw_acc + 64 * 2**20
+    # more than 8 chunks: auto falls back to the fp32 accumulator
+    assert lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 512, 1) > dw_acc
     assert lk.flce_plan(8192, 4096, 128256) == (2048, 4)
 
 

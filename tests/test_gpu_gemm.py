@@ -68,3 +68,32 @@ def test_tcgen05_gemm_random_bf16_large():
     ref = A.float() @ B.float().t()
     err = (d - ref).abs().max().item() / ref.abs().max().item()
     assert err < 1e-5, err
+
+
+@pytest.mark.parametrize("tma_reduce", [1, 0])
+def test_accum16_epilogue_rounding(tma_reduce):
+    """16-bit grad_w accumulation (weight-dtype accum_dtype): store, then add a second product.
+    TMA reduce-add path: the tile is staged in bf16 and added in L2 -> bf16(acc + bf16(p2)),
+    exactly Liger's `grad_weight += torch.mm(...).float()` order with a bf16 grad_weight
+    (LK/ops/fused_linear_cross_entropy.py:211).  Register path: bf16(acc + p2)."""
+    lib = _capi.load()
+    g = torch.Generator(device="cuda").manual_seed(5)
+    m, n, k = 512, 512, 256
+    a1 = torch.randn(m, k, device="cuda", generator=g).to(torch.bfloat16)
+    b1 = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    a2 = (torch.randn(m, k, device="cuda", generator=g) * 0.37).to(torch.bfloat16)
+    b2 = torch.randn(n, k, device="cuda", generator=g).to(torch.bfloat16)
+    d = torch.empty(m, n, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(256, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for beta, (a, b) in enumerate(((a1, b1), (a2, b2))):
+        _capi.check(lib.lk_gemm_test_accum16(a.data_ptr(), b.data_ptr(), d.data_ptr(), m, n, k, 1, beta, tma_reduce,
+                                             ws.data_ptr(), ws.numel(), st))
+    torch.cuda.synchronize()
+    p1 = (a1.float() @ b1.float().T).to(torch.bfloat16).float()
+    p2 = a2.float() @ b2.float().T
+    want = (p1 + (p2.to(torch.bfloat16).float() if tma_reduce else p2)).to(torch.bfloat16).float()
+    got = d.float()
+    # fp32 summation order inside the MMA differs from torch's: allow rare one-ulp ties
+    assert (got == want).float().mean().item() > 0.99
+    assert torch.allclose(got, want, rtol=2**-7, atol=2**-7 * want.abs().mean().item())
