@@ -120,6 +120,24 @@ def main():
                 "steady_frac": bb / (sm_ / 1e3) / 1e9 / hbm})
         del sets
 
+    # ---- LayerNorm (x: 8192 x 4096) ----
+    if want("layernorm"):
+        x = torch.randn(BT, H, device=dev, generator=g).to(bf)
+        w = (torch.rand(H, device=dev, generator=g) + 0.5).to(bf)
+        b = torch.randn(H, device=dev, generator=g).to(bf)
+        y, dy, dx = torch.empty_like(x), torch.randn(BT, H, device=dev, generator=g).to(bf), torch.empty_like(x)
+        mu, rs = torch.empty(BT, device=dev), torch.empty(BT, device=dev)
+        dw, db = torch.empty_like(w), torch.empty_like(b)
+        ws = torch.empty(L.lk_layernorm_bwd_workspace_bytes(BT, H), dtype=torch.uint8, device=dev)
+        f = lambda: _capi.check(L.lk_layernorm_fwd(x.data_ptr(), w.data_ptr(), b.data_ptr(), y.data_ptr(),  # noqa: E731
+                                                   mu.data_ptr(), rs.data_ptr(), BT, H, 1e-6, 1, st()))
+        bb = lambda: _capi.check(L.lk_layernorm_bwd(dy.data_ptr(), x.data_ptr(), w.data_ptr(), mu.data_ptr(),  # noqa: E731
+                                                    rs.data_ptr(), dx.data_ptr(), dw.data_ptr(), db.data_ptr(), BT, H,
+                                                    1, ws.data_ptr(), ws.numel(), st()))
+        report("layernorm_fwd", 2 * BT * H * 2 + 2 * H * 2 + 2 * BT * 4, timed(f, args.reps, flush))
+        report("layernorm_bwd", 3 * BT * H * 2 + 3 * H * 2 + 2 * BT * 4, timed(bb, args.reps, flush))
+        del x, y, dy, dx
+
     # ---- RoPE (q: 4 x 2048 x 32 x 128, k: 4 x 2048 x 8 x 128) ----
     if want("rope"):
         B, T = 4, 2048

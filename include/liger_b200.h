@@ -217,6 +217,19 @@ int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight, const void
                    void* dw, int64_t rows, int64_t cols, float offset, int casting_mode, int dtype,
                    void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- LayerNorm ------------------------------------------ */
+/* rowfuse/ops.py:248-311 and LK/ops/layer_norm.py (forward 169-227, backward 230-304).
+ * y = (x - mean) * rstd * w + b with rstd = 1/sqrt(mean((x - mean)^2) + eps); mean[rows]
+ * and rstd[rows] are fp32.  bias may be NULL (no shift; db then not computed).  cols must be
+ * a multiple of 16 bytes.  dw/db are sums over rows in the weight dtype (deterministic two-
+ * stage reduction through the caller workspace of lk_layernorm_bwd_workspace_bytes()). */
+int lk_layernorm_fwd(const void* x, const void* weight, const void* bias, void* y, float* mean, float* rstd,
+                     int64_t rows, int64_t cols, float eps, int dtype, void* stream);
+size_t lk_layernorm_bwd_workspace_bytes(int64_t rows, int64_t cols);
+int lk_layernorm_bwd(const void* dy, const void* x, const void* weight, const float* mean, const float* rstd,
+                     void* dx, void* dw, void* db, int64_t rows, int64_t cols, int dtype, void* workspace,
+                     size_t workspace_bytes, void* stream);
+
 /* ---- RoPE -------------------------------------------------------------- */
 /* rowfuse/ops.py:344-382 and LK/ops/rope.py:6-112.  q[B, T, nq, d] and
  * k[B, T, nk, d] are rotated in place (half-split HF layout); cos/sin are

@@ -156,6 +156,27 @@ def rmsnorm_backward(dy: np.ndarray, x: np.ndarray, r: np.ndarray, gamma: np.nda
     return dx, tree_sum(dy * xhat)
 
 
+# --------------------------------------------------------------- LayerNorm --
+def layernorm_forward(x: np.ndarray, gamma: np.ndarray, beta: np.ndarray, eps: float = 1e-6):
+    """rowfuse/ops.py:248-275: centred, r = 1/sqrt(mean((x-mu)^2) + eps); caches (mu, r)."""
+    n = x.shape[1]
+    mu = x.mean(axis=1)
+    v = x - mu[:, None]
+    r = 1.0 / np.sqrt(np.einsum("ij,ij->i", v, v) / n + eps)
+    return v * r[:, None] * gamma + beta, mu.astype(x.dtype), r.astype(x.dtype)
+
+
+def layernorm_backward(dy: np.ndarray, x: np.ndarray, mu: np.ndarray, r: np.ndarray, gamma: np.ndarray):
+    """rowfuse/ops.py:278-311: dx = r (gy - (xt.gy/n) xt - sum(gy)/n); dgamma, dbeta tree sums."""
+    n = x.shape[1]
+    xt = (x - mu[:, None]) * r[:, None]
+    gy = dy * gamma
+    proj = np.einsum("ij,ij->i", xt, gy) / n
+    shift = gy.sum(axis=1) / n
+    dx = (gy - proj[:, None] * xt - shift[:, None]) * r[:, None]
+    return dx, tree_sum(dy * xt), tree_sum(dy)
+
+
 # -------------------------------------------------------------------- RoPE --
 def rotation_thetas(head_dim: int, base: float = 10000.0) -> np.ndarray:
     """rowfuse/ops.py:85-89: base^(-2i/d)."""

@@ -15,6 +15,7 @@ from .fused_linear_cross_entropy import (
     flce_plan,
     fused_linear_cross_entropy_forward,
 )
+from .layer_norm import LigerLayerNorm, LigerLayerNormFunction, liger_layer_norm
 from .rms_norm import LigerRMSNorm, LigerRMSNormFunction
 from .rope import LigerRopeFunction, liger_rotary_pos_emb
 from .swiglu import (
@@ -58,7 +59,7 @@ __all__ = [
     "CrossEntropyOutput", "LigerCrossEntropyFunction", "LigerCrossEntropyLoss",
     "LigerFusedLinearCrossEntropyFunction", "LigerFusedLinearCrossEntropyLoss",
     "fused_linear_cross_entropy_forward",
-    "LigerRMSNorm", "LigerRMSNormFunction", "LigerRopeFunction", "liger_rotary_pos_emb",
+    "LigerRMSNorm", "LigerRMSNormFunction", "LigerLayerNorm", "LigerLayerNormFunction", "liger_layer_norm", "LigerRopeFunction", "liger_rotary_pos_emb",
     "LigerSiLUMulFunction", "LigerGELUMulFunction", "LigerSwiGLUMLP", "LigerGEGLUMLP",
     "liger_swiglu", "liger_geglu", "liger_cross_entropy", "liger_fused_linear_cross_entropy", "liger_rms_norm",
 ]

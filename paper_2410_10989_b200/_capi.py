@@ -116,6 +116,11 @@ SIGNATURES: dict[str, tuple] = {
     "lk_swiglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_geglu_fwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_geglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
+    "lk_layernorm_fwd": (c_int, [c_void, c_void, c_void, c_void, c_void, c_void, c_i64, c_i64, c_float, c_int,
+                                 c_void]),
+    "lk_layernorm_bwd_workspace_bytes": (c_size, [c_i64, c_i64]),
+    "lk_layernorm_bwd": (c_int, [c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_i64, c_i64, c_int,
+                                 c_void, c_size, c_void]),
     "lk_gemm_test_accum16": (c_int, [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_int, c_int, c_int, c_void, c_size,
                                      c_void]),
     "lk_gemm_test": (

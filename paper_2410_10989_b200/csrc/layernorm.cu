@@ -1,0 +1,272 @@
+// LayerNorm forward / backward.
+//
+// Forward (rowfuse/ops.py:248-275; Liger LK/ops/layer_norm.py:169-227):
+//   mu = mean(x), r = 1/sqrt(mean((x - mu)^2) + eps), y = (x - mu) * r * w + b,
+//   per-row mean and r cached in fp32.  One CTA per row, the row in registers, two
+//   reductions (centred variance, as the reference computes it), packed fp32x2 math.
+// Backward (rowfuse/ops.py:278-311; LK/ops/layer_norm.py:230-304):
+//   xt = (x - mu) r, gy = dy w, dx = r (gy - (xt . gy / n) xt - sum(gy) / n),
+//   dw = sum_rows dy xt, db = sum_rows dy.  Persistent CTAs over contiguous row ranges,
+//   next row prefetched into registers, both row reductions in one CTA barrier, dw/db
+//   partials in registers -> one partial row each per CTA -> fixed-order column sums
+//   (rowfuse's _tree_sum role, ops.py:138-152): bitwise deterministic for a given grid.
+#include "norm_cta.cuh"
+
+namespace lk {
+namespace ln {
+
+using rc::cta_sum;
+using rc::ldg_stream;
+
+// Two sums over the CTA's warps at once (one barrier); sh holds >= 2 x 64 floats.
+__device__ __forceinline__ float2 cta_sum2(float a, float b, float* sh, int par) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (lane == 0) { sh[par * 64 + warp] = a; sh[par * 64 + 32 + warp] = b; }
+  __syncthreads();
+  float ta = lane < nw ? sh[par * 64 + lane] : 0.f;
+  float tb = lane < nw ? sh[par * 64 + 32 + lane] : 0.f;
+  return make_float2(warp_sum(ta), warp_sum(tb));  // fixed trees: deterministic
+}
+
+template <typename T, int VPT>
+__global__ void __launch_bounds__(256) layernorm_fwd_cta(const T* __restrict__ x, const T* __restrict__ w,
+                                                         const T* __restrict__ b, T* __restrict__ y,
+                                                         float* __restrict__ mean, float* __restrict__ rstd,
+                                                         int rows, int cols, float eps) {
+  using P = ring::Pairs<T>;
+  constexpr int NP = P::NP, NV = 16 / sizeof(T);
+  __shared__ float sh[64];
+  const int nvec = cols / NV, row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
+  const T* xr = x + (int64_t)row * cols;
+  float2 f[VPT][NP];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = tid + k * nt;
+    P::unpack(v < nvec ? ldg_stream(xr + v * NV) : make_uint4(0, 0, 0, 0), f[k]);
+  }
+  float2 s = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k)
+#pragma unroll
+    for (int e = 0; e < NP; ++e) s = __fadd2_rn(s, f[k][e]);
+  const float mu = cta_sum(s.x + s.y, sh, 0) / (float)cols;
+  const float2 nmu = make_float2(-mu, -mu);
+  float2 q = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const bool in = tid + k * nt < nvec;
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      f[k][e] = in ? __fadd2_rn(f[k][e], nmu) : make_float2(0.f, 0.f);  // centred; padding stays 0
+      q = __ffma2_rn(f[k][e], f[k][e], q);
+    }
+  }
+  const float r = rsqrtf(cta_sum(q.x + q.y, sh, 1) / (float)cols + eps);
+  if (tid == 0) { mean[row] = mu; rstd[row] = r; }
+  const float2 r2 = make_float2(r, r);
+  T* yr = y + (int64_t)row * cols;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = tid + k * nt;
+    if (v < nvec) {
+      float2 wv[NP], bv[NP];
+      P::unpack(__ldg(reinterpret_cast<const uint4*>(w) + v), wv);
+      if (b) P::unpack(__ldg(reinterpret_cast<const uint4*>(b) + v), bv);
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        const float2 t = __fmul2_rn(__fmul2_rn(f[k][e], r2), wv[e]);
+        f[k][e] = b ? __fadd2_rn(t, bv[e]) : t;
+      }
+      ring::stg128(yr + v * NV, P::pack(f[k]));
+    }
+  }
+}
+
+template <typename T, int VPT>
+__global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* __restrict__ x,
+                                                         const T* __restrict__ w, const float* __restrict__ mean,
+                                                         const float* __restrict__ rstd, T* dx,
+                                                         float* __restrict__ dw_part, float* __restrict__ db_part,
+                                                         int rows, int cols) {
+  using P = ring::Pairs<T>;
+  constexpr int NP = P::NP, NV = 16 / sizeof(T);
+  __shared__ float sh[128];
+  const int nvec = cols / NV, tid = threadIdx.x, nt = blockDim.x;
+  const int per = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float2 aw[VPT][NP], ab[VPT][NP], wv[VPT][NP];
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = tid + k * nt;
+    if (v < nvec) P::unpack(__ldg(reinterpret_cast<const uint4*>(w) + v), wv[k]);
+#pragma unroll
+    for (int e = 0; e < NP; ++e) {
+      aw[k][e] = ab[k][e] = make_float2(0.f, 0.f);
+      if (v >= nvec) wv[k][e] = make_float2(0.f, 0.f);
+    }
+  }
+  uint4 gn[VPT], xn[VPT];
+  auto load = [&](int row) {
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int v = tid + k * nt;
+      const bool ok = row < r1 && v < nvec;
+      const int64_t off = (int64_t)row * cols + v * NV;
+      gn[k] = ok ? ldg_stream(dy + off) : make_uint4(0, 0, 0, 0);
+      xn[k] = ok ? ldg_stream(x + off) : make_uint4(0, 0, 0, 0);
+    }
+  };
+  load(r0);
+  int par = 0;
+  for (int row = r0; row < r1; ++row, par ^= 1) {
+    const float mu = mean[row], r = rstd[row];
+    const float2 nmu = make_float2(-mu, -mu), r2 = make_float2(r, r);
+    float2 xt[VPT][NP], gy[VPT][NP];
+    float2 pj = make_float2(0.f, 0.f), sf = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      float2 g[NP], xv[NP];
+      P::unpack(gn[k], g);
+      P::unpack(xn[k], xv);
+#pragma unroll
+      for (int e = 0; e < NP; ++e) {
+        xt[k][e] = __fmul2_rn(__fadd2_rn(xv[e], nmu), r2);
+        if (tid + k * nt >= nvec) xt[k][e] = make_float2(0.f, 0.f);
+        gy[k][e] = __fmul2_rn(g[e], wv[k][e]);
+        pj = __ffma2_rn(xt[k][e], gy[k][e], pj);
+        sf = __fadd2_rn(sf, gy[k][e]);
+        aw[k][e] = __ffma2_rn(g[e], xt[k][e], aw[k][e]);
+        ab[k][e] = __fadd2_rn(ab[k][e], g[e]);
+      }
+    }
+    load(row + 1);  // next row in flight during the reduction and the write
+    const float2 t = cta_sum2(pj.x + pj.y, sf.x + sf.y, sh, par);
+    const float proj = t.x / (float)cols, shift = t.y / (float)cols;
+    const float2 np2 = make_float2(-proj, -proj), ns2 = make_float2(-shift, -shift);
+#pragma unroll
+    for (int k = 0; k < VPT; ++k) {
+      const int v = tid + k * nt;
+      if (v < nvec) {
+        float2 o[NP];
+#pragma unroll
+        for (int e = 0; e < NP; ++e)
+          o[e] = __fmul2_rn(__fadd2_rn(__ffma2_rn(np2, xt[k][e], gy[k][e]), ns2), r2);
+        ring::stg128(dx + (int64_t)row * cols + v * NV, P::pack(o));
+      }
+    }
+  }
+  float* pw = dw_part + (int64_t)blockIdx.x * cols;
+  float* pb = db_part ? db_part + (int64_t)blockIdx.x * cols : nullptr;
+#pragma unroll
+  for (int k = 0; k < VPT; ++k) {
+    const int v = tid + k * nt;
+    if (v < nvec) {
+#pragma unroll
+      for (int e = 0; e < NP; e += 2) {
+        reinterpret_cast<float4*>(pw + v * NV)[e / 2] =
+            make_float4(aw[k][e].x, aw[k][e].y, aw[k][e + 1].x, aw[k][e + 1].y);
+        if (pb)
+          reinterpret_cast<float4*>(pb + v * NV)[e / 2] =
+              make_float4(ab[k][e].x, ab[k][e].y, ab[k][e + 1].x, ab[k][e + 1].y);
+      }
+    }
+  }
+}
+
+static int vpt_for(int64_t nvec, int* threads) {
+  int v = 1;
+  while (v < 8 && (nvec + v - 1) / v > 256) v *= 2;
+  if ((nvec + v - 1) / v > 256) return 0;
+  *threads = (int)(((nvec + v - 1) / v + 31) / 32 * 32);
+  return v;
+}
+static int64_t bwd_grid(int64_t rows) { return std::max<int64_t>(1, std::min<int64_t>(rows, 8 * (int64_t)sm_count())); }
+
+}  // namespace ln
+
+// defined in norm.cu
+int launch_colsum_partials(const float* part, int64_t g, int64_t cols, void* out, int dtype, cudaStream_t st);
+
+}  // namespace lk
+
+using namespace lk;
+
+#define LK_LN_VPT(vpt, VPT, ...)                            \
+  switch (vpt) {                                            \
+    case 1: { constexpr int VPT = 1; __VA_ARGS__; break; }  \
+    case 2: { constexpr int VPT = 2; __VA_ARGS__; break; }  \
+    case 4: { constexpr int VPT = 4; __VA_ARGS__; break; }  \
+    default: { constexpr int VPT = 8; __VA_ARGS__; break; } \
+  }
+
+extern "C" int lk_layernorm_fwd(const void* x, const void* weight, const void* bias, void* y, float* mean,
+                                float* rstd, int64_t rows, int64_t cols, float eps, int dtype, void* stream) {
+  LK_REQUIRE(rows >= 0 && cols >= 1, LK_SIZE_MISMATCH, "rows >= 0 and cols >= 1 required");
+  if (rows == 0) return LK_OK;
+  LK_REQUIRE(x && weight && y && mean && rstd, LK_INVALID_ARGUMENT, "null pointer");
+  LK_REQUIRE(rows <= 0x7fffffff, LK_SIZE_MISMATCH, "too many rows");
+  const int64_t nv = dtype == LK_F32 ? 4 : 8;
+  LK_REQUIRE(cols % nv == 0, LK_SIZE_MISMATCH, "hidden size must be a multiple of 16 bytes");
+  LK_REQUIRE(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(weight) |
+               reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(y)) & 15) == 0,
+             LK_NON_CONTIGUOUS, "buffers must be 16-byte aligned");
+  int threads = 0;
+  const int vpt = ln::vpt_for(cols / nv, &threads);
+  LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
+  cudaStream_t st = as_stream(stream);
+  LK_DISPATCH_FLOAT(dtype, T, {
+    LK_LN_VPT(vpt, VPT, {
+      ln::layernorm_fwd_cta<T, VPT><<<(unsigned)rows, threads, 0, st>>>(
+          static_cast<const T*>(x), static_cast<const T*>(weight), static_cast<const T*>(bias), static_cast<T*>(y),
+          mean, rstd, (int)rows, (int)cols, eps);
+    });
+  });
+  return check_launch("layernorm_fwd_cta");
+}
+
+extern "C" size_t lk_layernorm_bwd_workspace_bytes(int64_t rows, int64_t cols) {
+  return (size_t)2 * ln::bwd_grid(rows) * (size_t)cols * sizeof(float) + 256;
+}
+
+extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weight, const float* mean,
+                                const float* rstd, void* dx, void* dw, void* db, int64_t rows, int64_t cols,
+                                int dtype, void* workspace, size_t workspace_bytes, void* stream) {
+  LK_REQUIRE(rows >= 0 && cols >= 1, LK_SIZE_MISMATCH, "rows >= 0 and cols >= 1 required");
+  LK_REQUIRE(rows <= 0x7fffffff, LK_SIZE_MISMATCH, "too many rows");
+  LK_REQUIRE(weight && dw, LK_INVALID_ARGUMENT, "null weight / dw");
+  LK_REQUIRE(workspace && workspace_bytes >= lk_layernorm_bwd_workspace_bytes(rows, cols), LK_INVALID_ARGUMENT,
+             "workspace too small");
+  LK_REQUIRE(rows == 0 || (dy && x && mean && rstd && dx), LK_INVALID_ARGUMENT, "null pointer");
+  const int64_t nv = dtype == LK_F32 ? 4 : 8;
+  LK_REQUIRE(cols % nv == 0, LK_SIZE_MISMATCH, "hidden size must be a multiple of 16 bytes");
+  cudaStream_t st = as_stream(stream);
+  float* pw = static_cast<float*>(workspace);
+  const int64_t gmax = ln::bwd_grid(rows);
+  float* pb = pw + gmax * cols;
+  int threads = 0;
+  const int vpt = ln::vpt_for(cols / nv, &threads);
+  LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
+  int64_t grid = 1;
+  if (rows == 0) {
+    LK_CUDA(cudaMemsetAsync(pw, 0, (size_t)2 * gmax * cols * sizeof(float), st));
+  } else {
+    LK_DISPATCH_FLOAT(dtype, T, {
+      LK_LN_VPT(vpt, VPT, {
+        auto kern = ln::layernorm_bwd_cta<T, VPT>;
+        int per_sm = 0;
+        LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+        grid = std::max<int64_t>(1, std::min<int64_t>({rows, gmax, (int64_t)std::max(1, per_sm) * sm_count()}));
+        kern<<<(unsigned)grid, threads, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
+                                                 static_cast<const T*>(weight), mean, rstd, static_cast<T*>(dx), pw,
+                                                 db ? pb : nullptr, (int)rows, (int)cols);
+      });
+    });
+    int rc = check_launch("layernorm_bwd_cta");
+    if (rc) return rc;
+  }
+  int rc = launch_colsum_partials(pw, grid, cols, dw, dtype, st);
+  if (rc || !db) return rc;
+  return launch_colsum_partials(pb, grid, cols, db, dtype, st);
+}

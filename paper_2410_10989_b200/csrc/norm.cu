@@ -247,6 +247,13 @@ __global__ void __launch_bounds__(1024) colsum_partials_kernel(const float* __re
   }
 }
 
+int launch_colsum_partials(const float* part, int64_t g, int64_t cols, void* out, int dtype, cudaStream_t st) {
+  LK_DISPATCH_FLOAT(dtype, T, {
+    colsum_partials_kernel<T><<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(part, g, cols, static_cast<T*>(out));
+  });
+  return check_launch("colsum_partials_kernel");
+}
+
 struct NormCfg {
   bool reg;
   int kv;

@@ -14,8 +14,9 @@ rng.uniform(-1, 1), W scaled by 1/sqrt(H), tests/test_flce.py:30-35):
   flce_mid         BT=128, H=64, V=512, f64, reference plan
   flce_cfg1        cfg1 (BT=1024, H=512, V=4096, seed 0, f64): loss + checksums + sampled entries
   flce_scalar      BT=6, H=5, V=7 through the scalar oracle ref_linear_cross_entropy
-  rms_*, rope_*, swiglu_*, geglu_*  row ops at f64
+  rms_*, ln_*, rope_*, swiglu_*, geglu_*  row ops at f64
   plan_table       chunk-size table of tests/test_flce.py:40-53
+  converge_*       loss curves of rowfuse.converge.converge() (100 SGD steps, f32, fused and baseline)
 """
 
 from __future__ import annotations
@@ -44,6 +45,8 @@ def main() -> None:
         cross_entropy,
         geglu_backward,
         geglu_forward,
+        layernorm_backward,
+        layernorm_forward,
         rmsnorm_backward,
         rmsnorm_forward,
         rope_backward,
@@ -133,6 +136,18 @@ def main() -> None:
     g["rms_y"], g["rms_rstd"], g["rms_dx"], g["rms_dgamma"] = y.view2d.copy(), res.inv_rms.copy(), dx.view2d.copy(), dgam.data.copy()
     g["rms_kat_y"] = rmsnorm_forward(Matrix2D.from_array(np.array([[3.0, 4.0]])), Vector(np.ones(2), DType.F64), eps=0.0)[0].view2d.copy()
 
+    # ---- LayerNorm ----
+    rng = np.random.default_rng(14)
+    x = rng.uniform(-1, 1, (16, 40)) + 0.3
+    gam = np.abs(rng.uniform(-1, 1, 40)) + 0.5
+    bet = rng.uniform(-0.5, 0.5, 40)
+    dy = rng.uniform(-1, 1, (16, 40))
+    y, res = layernorm_forward(Matrix2D.from_array(x), Vector(gam, DType.F64), Vector(bet, DType.F64), eps=1e-6)
+    dx, dgam, dbet = layernorm_backward(Matrix2D.from_array(dy), res, Vector(gam, DType.F64))
+    g["ln_x"], g["ln_gamma"], g["ln_beta"], g["ln_dy"] = x, gam, bet, dy
+    g["ln_y"], g["ln_mean"], g["ln_rstd"] = y.view2d.copy(), res.mean.copy(), res.inv_rms.copy()
+    g["ln_dx"], g["ln_dgamma"], g["ln_dbeta"] = dx.view2d.copy(), dgam.data.copy(), dbet.data.copy()
+
     # ---- RoPE (per-row positions + thetas) ----
     rng = np.random.default_rng(12)
     d = 8
@@ -156,6 +171,14 @@ def main() -> None:
     g["geglu_y"] = geglu_forward(gi).view2d.copy()
     a, b = geglu_backward(Matrix2D.from_array(dy), gi)
     g["geglu_dx1"], g["geglu_dx2"] = a.view2d.copy(), b.view2d.copy()
+
+    # ---- training parity harness (rowfuse/converge.py): the reference's own loss curves ----
+    from rowfuse.converge import ConvergeConfig, converge  # noqa: E402
+
+    rep = converge(ConvergeConfig())
+    assert rep.passed
+    g["converge_losses_fused"] = np.array(rep.losses_a, dtype=np.float64)
+    g["converge_losses_reference"] = np.array(rep.losses_b, dtype=np.float64)
 
     # ---- chunk plan table ----
     table = [(4096, 131072, 4096), (4096, 32000, 4096), (4096, 40960, 512), (1, 50000, 768), (100, 768, 768),

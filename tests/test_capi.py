@@ -98,6 +98,8 @@ def test_no_cpu_fallback():
         lk.LigerRMSNorm(8)(x)
     with pytest.raises(errors.ExtensionMissing):
         lk.liger_swiglu(x, x)
+    with pytest.raises(errors.ExtensionMissing):
+        lk.LigerLayerNorm(8)(x)
 
 
 def _params(obj):
@@ -118,6 +120,10 @@ def _params(obj):
         ("LigerSwiGLUMLP.__init__", "liger_kernel.transformers.swiglu.LigerSwiGLUMLP.__init__"),
         ("LigerGEGLUMLP.__init__", "liger_kernel.transformers.geglu.LigerGEGLUMLP.__init__"),
         ("LigerCrossEntropyFunction.forward", "liger_kernel.ops.cross_entropy.LigerCrossEntropyFunction.forward"),
+        ("LigerLayerNorm.__init__", "liger_kernel.transformers.layer_norm.LigerLayerNorm.__init__"),
+        ("LigerLayerNorm.forward", "liger_kernel.transformers.layer_norm.LigerLayerNorm.forward"),
+        ("LigerLayerNormFunction.forward", "liger_kernel.ops.layer_norm.LigerLayerNormFunction.forward"),
+        ("liger_layer_norm", "liger_kernel.transformers.functional.liger_layer_norm"),
     ],
 )
 def test_signatures_match_liger(ours, theirs):

@@ -94,6 +94,8 @@ def test_accum16_epilogue_rounding(tma_reduce):
     p2 = a2.float() @ b2.float().T
     want = (p1 + (p2.to(torch.bfloat16).float() if tma_reduce else p2)).to(torch.bfloat16).float()
     got = d.float()
-    # fp32 summation order inside the MMA differs from torch's: allow rare one-ulp ties
+    # fp32 summation order inside the MMA differs from torch's, so a rounding of p1 / p2 can land
+    # one ulp apart at ties: equal almost everywhere, and never more than a few bf16 ulps apart
     assert (got == want).float().mean().item() > 0.99
-    assert torch.allclose(got, want, rtol=2**-7, atol=2**-7 * want.abs().mean().item())
+    ulp = torch.clamp(want.abs(), min=1e-3) * 2.0**-7
+    assert torch.all((got - want).abs() <= 4 * ulp)

@@ -110,6 +110,63 @@ def test_rmsnorm_dw_deterministic_and_batch_linear():
     assert torch.equal(outs[0], outs[1])  # fixed-order two-stage reduction
 
 
+# ---------------------------------------------------------------- LayerNorm
+def test_layernorm_fp32_vs_reference_golden(golden):
+    x = cuda(golden["ln_x"]).requires_grad_(True)
+    m = lk.LigerLayerNorm(40, eps=1e-6, bias=True).cuda()
+    with torch.no_grad():
+        m.weight.copy_(cuda(golden["ln_gamma"]))
+        m.bias.copy_(cuda(golden["ln_beta"]))
+    y = m(x)
+    y.backward(cuda(golden["ln_dy"]))
+    for name, a, b in (("y", y.detach(), golden["ln_y"]), ("dx", x.grad, golden["ln_dx"]),
+                       ("dgamma", m.weight.grad, golden["ln_dgamma"]), ("dbeta", m.bias.grad, golden["ln_dbeta"])):
+        ok, err = rel_close(a.cpu().numpy(), b, 1e-4)
+        assert ok, (name, err)
+
+
+@pytest.mark.parametrize("shape,dtype", [((8192, 4096), torch.bfloat16), ((300, 1000), torch.bfloat16),
+                                         ((37, 2048), torch.float32), ((5, 64), torch.float16)])
+def test_layernorm_vs_oracle_and_torch(shape, dtype):
+    rows, cols = shape
+    g = torch.Generator(device="cuda").manual_seed(rows + 3 * cols)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 0.7).to(dtype)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(dtype)
+    b = (torch.rand(cols, device="cuda", generator=g) - 0.5).to(dtype)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(dtype)
+    xr, wr, br = x.clone().requires_grad_(True), w.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    y = lk.liger_layer_norm(xr, wr, br, 1e-6)
+    y.backward(dy)
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    sel = slice(0, min(rows, 256))
+    xs = x[sel].double().cpu().numpy()
+    ry, mu, r = rp.layernorm_forward(xs, w.double().cpu().numpy(), b.double().cpu().numpy())
+    rdx, _, _ = rp.layernorm_backward(dy[sel].double().cpu().numpy(), xs, mu, r, w.double().cpu().numpy())
+    ok, err = rel_close(y[sel].detach().float().cpu().numpy(), ry, tol)
+    assert ok, ("y", err)
+    ok, err = rel_close(xr.grad[sel].float().cpu().numpy(), rdx, tol)
+    assert ok, ("dx", err)
+    # dgamma / dbeta over all rows against torch fp32 autograd
+    xf = x.float().requires_grad_(True)
+    wf, bf = w.float().requires_grad_(True), b.float().requires_grad_(True)
+    torch.nn.functional.layer_norm(xf, (cols,), wf, bf, eps=1e-6).backward(dy.float())
+    assert close(wr.grad, wf.grad, tol) and close(br.grad, bf.grad, tol)
+
+
+def test_layernorm_grads_deterministic():
+    g = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(4096, 1024, device="cuda", generator=g).to(torch.bfloat16)
+    w = torch.randn(1024, device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn(1024, device="cuda", generator=g).to(torch.bfloat16)
+    dy = torch.randn(4096, 1024, device="cuda", generator=g).to(torch.bfloat16)
+    outs = []
+    for _ in range(2):
+        xr, wr, br = x.clone().requires_grad_(True), w.clone().requires_grad_(True), b.clone().requires_grad_(True)
+        lk.liger_layer_norm(xr, wr, br, 1e-6).backward(dy)
+        outs.append((xr.grad.clone(), wr.grad.clone(), br.grad.clone()))
+    assert all(torch.equal(p, q) for p, q in zip(*outs))
+
+
 # --------------------------------------------------------------------- RoPE
 def test_rope_fp32_vs_reference_golden(golden):
     q, k, th, pos = golden["rope_q"], golden["rope_k"], golden["rope_thetas"], golden["rope_pos"]

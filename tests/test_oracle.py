@@ -132,6 +132,23 @@ def test_liger_ref_z_loss_gradient():
     np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
 
 
+def test_layernorm_port_vs_reference(golden):
+    y, mu, r = rp.layernorm_forward(golden["ln_x"], golden["ln_gamma"], golden["ln_beta"])
+    np.testing.assert_allclose(y, golden["ln_y"], **STRICT)
+    np.testing.assert_allclose(mu, golden["ln_mean"], **STRICT)
+    np.testing.assert_allclose(r, golden["ln_rstd"], **STRICT)
+    dx, dg, db = rp.layernorm_backward(golden["ln_dy"], golden["ln_x"], mu, r, golden["ln_gamma"])
+    np.testing.assert_allclose(dx, golden["ln_dx"], **STRICT)
+    np.testing.assert_array_equal(dg, golden["ln_dgamma"])  # same fixed-order tree: bitwise
+    np.testing.assert_array_equal(db, golden["ln_dbeta"])
+    # the centred form equals torch's layer_norm (biased variance, eps inside the root)
+    import torch
+
+    t = torch.nn.functional.layer_norm(torch.tensor(golden["ln_x"]), (golden["ln_x"].shape[1],),
+                                       torch.tensor(golden["ln_gamma"]), torch.tensor(golden["ln_beta"]), eps=1e-6)
+    np.testing.assert_allclose(t.numpy(), golden["ln_y"], **STRICT)
+
+
 def test_rmsnorm_port_vs_reference(golden):
     y, r = rp.rmsnorm_forward(golden["rms_x"], golden["rms_gamma"])
     np.testing.assert_allclose(y, golden["rms_y"], **STRICT)
