@@ -158,3 +158,47 @@ def test_flce_module_signature_is_liger_plus_chunk_override():
     ours = _params(lk.LigerFusedLinearCrossEntropyLoss.__init__)
     assert ours[:-1] == _params(Ref.__init__)
     assert ours[-1] == ("chunk_rows", None)
+
+
+def test_benchrecord_schema_round_trip(tmp_path):
+    """GPU bench results use rowfuse's BenchRecord CSV schema (rowfuse/bench.py:84-159), so
+    `rowfuse report` can merge them with CPU runs."""
+    from paper_2410_10989_b200 import benchrecord as br
+
+    assert br.FIELDS == ("op", "variant", "rows", "cols", "hidden", "dtype", "repeats", "workers", "median_s",
+                         "q20_s", "q80_s", "peak_bytes")
+    recs = [br.BenchRecord("linear_ce", "fused", 128, 40960, 256, "bf16", 10, 0, 1.25e-4, 1.2e-4, 1.3e-4, 12345)]
+    p = tmp_path / "r.csv"
+    br.write_records(p, recs)
+    assert br.read_records(p) == recs
+    assert p.read_text().splitlines()[0] == ",".join(br.FIELDS)
+    bad = tmp_path / "bad.csv"
+    bad.write_text("op,variant\nx,y\n")
+    with pytest.raises(br.SchemaMismatch):
+        br.read_records(bad)
+    assert br.default_shapes("rmsnorm")[0] == (256, 4096, 0)
+    assert br.default_shapes("linear_ce")[-1] == (128, 163840, 256)
+
+
+def test_benchrecord_csv_reads_with_the_reference_reader(tmp_path):
+    """Where the reference tree exists (the build container), its own reader accepts our CSV."""
+    import os
+    import sys
+
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference tree not present (GPU box)")
+    from paper_2410_10989_b200 import benchrecord as br
+
+    p = tmp_path / "r.csv"
+    br.write_records(p, [br.BenchRecord("rmsnorm", "fused", 256, 4096, 0, "bf16", 10, 0, 2e-5, 1.9e-5, 2.2e-5, 4096)])
+    sys.path.insert(0, src)
+    os.environ["PYTHONDONTWRITEBYTECODE"] = "1"
+    sys.dont_write_bytecode = True
+    try:
+        from rowfuse.bench import read_records, summarize
+    finally:
+        sys.path.remove(src)
+    recs = read_records(p)
+    assert recs[0].op == "rmsnorm" and recs[0].median_s == 2e-5
+    assert summarize(recs)[0]["fused_median_s"] == 2e-5

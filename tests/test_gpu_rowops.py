@@ -272,3 +272,15 @@ def test_swiglu_mlp_module_matches_torch():
     gx = torch.autograd.grad(y, x, gy)[0]
     gx_ref = torch.autograd.grad(ref, x, gy)[0]
     torch.testing.assert_close(gx, gx_ref, rtol=1e-4, atol=1e-5)
+
+
+def test_benchrecord_gpu_rows(tmp_path):
+    """One GPU record per op at a reference default shape, readable back through the schema."""
+    from paper_2410_10989_b200 import benchrecord as br
+
+    recs = [br.bench_op(op, *br.default_shapes(op)[0], repeats=3) for op in br.OPS]
+    p = tmp_path / "gpu.csv"
+    br.write_records(p, recs)
+    back = br.read_records(p)
+    assert [r.op for r in back] == list(br.OPS)
+    assert all(r.variant == "fused" and r.median_s > 0 and r.q20_s <= r.q80_s for r in back)
