@@ -101,6 +101,14 @@ int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* targets, int64
                          float lse_square_scale, float softcap, int reduction, int compute_grad,
                          float* loss_rows, float* loss_sum, float* z_loss_rows, float* z_loss_sum,
                          void* workspace, size_t workspace_bytes, void* stream);
+/* Same, plus Liger's return_token_accuracy / return_predicted_tokens outputs: per row
+ * 1.0 if argmax == target else 0.0 (correct_rows) and the argmax (pred_rows); ignored rows
+ * -> 0.0 / -1; either may be NULL (LK/ops/cross_entropy.py:131-163, 294-299). */
+int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* targets, int64_t rows, int64_t vocab,
+                            int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
+                            float softcap, int reduction, int compute_grad, float* loss_rows, float* loss_sum,
+                            float* z_loss_rows, float* z_loss_sum, float* correct_rows, int64_t* pred_rows,
+                            void* workspace, size_t workspace_bytes, void* stream);
 
 /* Count of targets != ignore_index and the out-of-range flag, on device.
  * out[0] = n_non_ignore (as int64), out[1] = number of out-of-range targets. */
@@ -166,6 +174,12 @@ typedef struct {
    * LK_ACCUM_FP32 = fp32 workspace accumulator; LK_ACCUM_WEIGHT_DTYPE = always the weight
    * dtype (Liger's accum_dtype=None semantics). */
   int grad_w_accum;
+  /* Liger return_token_accuracy / return_predicted_tokens (LK/ops/fused_linear_cross_entropy.py:
+   * 119-125, 148-160): per row 1.0 if argmax(logits) == target else 0.0, and the argmax
+   * (first column of the max of the softcapped, rounded logits); ignored rows -> 0.0 / -1.
+   * NULL = not computed (the epilogue then skips the argmax search). */
+  float* token_correct_rows;  /* [BT] fp32 or NULL */
+  int64_t* predicted_tokens;  /* [BT] or NULL      */
 } lk_flce_args;
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };

@@ -63,6 +63,8 @@ class FlceArgs(C.Structure):
         ("force_simt", c_int),
         ("mean_count", c_void),
         ("grad_w_accum", c_int),
+        ("token_correct_rows", c_void),
+        ("predicted_tokens", c_void),
     ]
 
 
@@ -75,6 +77,9 @@ SIGNATURES: dict[str, tuple] = {
     "lk_profile_collect": (c_int, [C.POINTER(C.c_double), c_i64p]),
     "lk_launch_count": (c_i64, []),
     "lk_cross_entropy_workspace_bytes": (c_size, [c_i64]),
+    "lk_cross_entropy_fwd_ex": (c_int, [c_void, c_i64, c_void, c_i64, c_i64, c_int, c_i64, c_float, c_float, c_float,
+                                        c_int, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_size,
+                                        c_void]),
     "lk_flce_workspace_bytes_ex": (c_size, [c_i64, c_i64, c_i64, c_int, c_i64, c_int, c_int]),
     "lk_cross_entropy_fwd": (
         c_int,

@@ -64,8 +64,6 @@ def cross_entropy_forward(
     _validate(label_smoothing, reduction, softcap)
     if weight is not None:
         raise errors.UnsupportedOption("class weights (ce_weight) are not implemented in the B200 build")
-    if return_token_accuracy or return_predicted_tokens:
-        raise errors.UnsupportedOption("token accuracy / predicted tokens are not implemented in the B200 build")
     require_cuda(_input, target)
     if _input.dim() != 2:
         raise errors.ShapeMismatch(f"input must be (BT, V), got {tuple(_input.shape)}")
@@ -81,25 +79,31 @@ def cross_entropy_forward(
     loss_sum = torch.empty((), dtype=torch.float32, device=dev)
     z_rows = torch.empty(bt, dtype=torch.float32, device=dev) if return_z_loss else None
     z_sum = torch.empty((), dtype=torch.float32, device=dev) if return_z_loss else None
+    correct = torch.empty(bt, dtype=torch.float32, device=dev) if return_token_accuracy else None
+    pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None
     L = lib()
     ws = workspace(L.lk_cross_entropy_workspace_bytes(bt), dev)
     check(
-        L.lk_cross_entropy_fwd(
+        L.lk_cross_entropy_fwd_ex(
             _input.data_ptr(), _input.stride(0) if bt > 0 else v, ptr(t), bt, v, dtype_code(_input),
             int(ignore_index), float(label_smoothing), float(lse_square_scale),
             float(softcap) if softcap is not None else 0.0, _capi.REDUCTIONS[reduction], int(bool(grad)),
-            loss_rows.data_ptr(), loss_sum.data_ptr(), ptr(z_rows), ptr(z_sum), ws.data_ptr(), ws.numel(),
-            stream_of(_input),
+            loss_rows.data_ptr(), loss_sum.data_ptr(), ptr(z_rows), ptr(z_sum), ptr(correct), ptr(pred),
+            ws.data_ptr(), ws.numel(), stream_of(_input),
         )
     )
-    raise_if_out_of_range(ws[:16].view(torch.int64), v)
+    counts = ws[:16].view(torch.int64)
+    raise_if_out_of_range(counts, v)
     if reduction == "none":
         loss = loss_rows.to(_input.dtype)
         z_loss = z_rows.to(_input.dtype) if return_z_loss else None
+        acc = correct
     else:
         loss = loss_sum.to(_input.dtype)
         z_loss = z_sum.to(_input.dtype) if return_z_loss else None
-    return loss, z_loss, None, None, _input
+        # mean over the non-ignored tokens for both 'mean' and 'sum' (LK/ops/cross_entropy.py:419-420)
+        acc = correct.sum() / counts[0].clamp(min=1) if return_token_accuracy else None
+    return loss, z_loss, acc, pred, _input
 
 
 def cross_entropy_backward(_input: torch.Tensor, grad_output: torch.Tensor) -> torch.Tensor:

@@ -156,6 +156,17 @@ extern "C" int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* tar
                                     int reduction, int compute_grad, float* loss_rows,
                                     float* loss_sum, float* z_loss_rows, float* z_loss_sum,
                                     void* workspace, size_t workspace_bytes, void* stream) {
+  return lk_cross_entropy_fwd_ex(logits, ld, targets, rows, vocab, dtype, ignore_index, label_smoothing,
+                                 lse_square_scale, softcap, reduction, compute_grad, loss_rows, loss_sum,
+                                 z_loss_rows, z_loss_sum, nullptr, nullptr, workspace, workspace_bytes, stream);
+}
+
+extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* targets, int64_t rows,
+                                       int64_t vocab, int dtype, int64_t ignore_index, float label_smoothing,
+                                       float lse_square_scale, float softcap, int reduction, int compute_grad,
+                                       float* loss_rows, float* loss_sum, float* z_loss_rows, float* z_loss_sum,
+                                       float* correct_rows, int64_t* pred_rows, void* workspace,
+                                       size_t workspace_bytes, void* stream) {
   LK_REQUIRE(rows >= 0 && vocab >= 1, LK_SIZE_MISMATCH, "rows must be >= 0 and vocab >= 1");
   LK_REQUIRE(ld >= vocab, LK_NON_CONTIGUOUS, "row stride smaller than vocab");
   LK_REQUIRE(rows == 0 || (logits && targets), LK_INVALID_ARGUMENT, "null logits/targets");
@@ -175,6 +186,7 @@ extern "C" int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* tar
   a.label_smoothing = label_smoothing; a.lse_square_scale = lse_square_scale; a.softcap = softcap;
   a.input_capped = 0; a.reduction = reduction; a.compute_grad = compute_grad; a.n_valid = counts;
   a.loss_rows = loss_rows; a.z_loss_rows = z_loss_rows;
+  a.correct_rows = correct_rows; a.pred_rows = pred_rows;
   // LK_CE_IMPL = ring (default) | cluster | block (one CTA per row, ce_rows_kernel)
   const char* impl_env = getenv("LK_CE_IMPL");  // read per call so tests can switch paths
   const char impl = impl_env ? impl_env[0] : 'r';

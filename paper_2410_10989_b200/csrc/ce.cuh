@@ -40,7 +40,25 @@ struct CeRowArgs {
   int64_t n_parts;
   const float* tgt_logit;  // [rows] capped target logit (with partials)
   const float4* row_stats; // [rows] global (max, sumexp, sum_logits, target_logit) (vocab-parallel)
+  // Liger return_token_accuracy / return_predicted_tokens (LK/ops/cross_entropy.py:131-163, 294-299):
+  // argmax = first column of the (softcapped) row max; ignored rows -> 0 / -1.  With
+  // partials, the argmax comes from partials[].w (int bits) written by the logits epilogue.
+  float* correct_rows;     // [rows] 1.0 if argmax == target else 0.0, or null
+  int64_t* pred_rows;      // [rows] argmax (global column), -1 for ignored rows, or null
 };
+
+// (value, index) argmax merge: larger value wins, ties keep the smaller index.
+__device__ __forceinline__ void am_merge(float& v, int& i, float v2, int i2) {
+  if (v2 > v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+}
+__device__ __forceinline__ void warp_am(float& v, int& i) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, i, o);
+    am_merge(v, i, v2, i2);
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ float cap_val(float z, float cap, bool accurate) {
@@ -52,8 +70,13 @@ template <typename T, int BLOCK>
 __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
   constexpr int NV = Vec16<T>::N;
   constexpr bool ACCURATE = sizeof(T) == 4;
-  __shared__ float red_m[BLOCK / 32], red_s[BLOCK / 32], red_z[BLOCK / 32];
+  __shared__ float red_m[BLOCK / 32], red_s[BLOCK / 32], red_z[BLOCK / 32], red_av[BLOCK / 32];
+  __shared__ int red_ai[BLOCK / 32];
   __shared__ float bcast[4];
+  __shared__ int bcast_arg;
+  const bool want_arg = a.correct_rows || a.pred_rows;
+  float av = -INFINITY;
+  int ai = 0x7fffffff;
 
   const int64_t row = blockIdx.x;
   if (row >= a.rows) return;
@@ -71,6 +94,8 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
     if (tid == 0) {
       if (a.loss_rows) a.loss_rows[row] = 0.f;
       if (a.z_loss_rows) a.z_loss_rows[row] = 0.f;
+      if (a.correct_rows) a.correct_rows[row] = 0.f;
+      if (a.pred_rows) a.pred_rows[row] = -1;
     }
     return;
   }
@@ -89,13 +114,15 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
         float4 q = p[j];
         ms_combine(lm, ls, q.x, q.y);
         lz += q.z;
+        if (want_arg) am_merge(av, ai, q.x, __float_as_int(q.w));
       }
     } else {
-      auto upd = [&](float* v, int cnt) {
+      auto upd = [&](float* v, int cnt, int64_t col) {
         float cm = -INFINITY;
         for (int i = 0; i < cnt; ++i) {
           if (has_cap && !a.input_capped) v[i] = cap_val<T>(v[i], cap, ACCURATE);
           cm = fmaxf(cm, v[i]);
+          if (want_arg) am_merge(av, ai, v[i], (int)(col + i));
         }
         float mn = fmaxf(lm, cm);
         float acc = 0.f;
@@ -108,29 +135,36 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
         for (int64_t i = tid; i < nvec; i += BLOCK) {
           Vec16<T> v;
           v.load(x + i * NV);
-          upd(v.v, NV);
+          upd(v.v, NV, i * NV);
         }
         for (int64_t i = nvec * NV + tid; i < n; i += BLOCK) {
           float v = to_f<T>(x[i]);
-          upd(&v, 1);
+          upd(&v, 1, i);
         }
       } else {
         for (int64_t i = tid; i < n; i += BLOCK) {
           float v = to_f<T>(x[i]);
-          upd(&v, 1);
+          upd(&v, 1, i);
         }
       }
     }
     warp_ms(lm, ls);
     lz = warp_sum(lz);
-    if (lane == 0) { red_m[warp] = lm; red_s[warp] = ls; red_z[warp] = lz; }
+    if (want_arg) warp_am(av, ai);
+    if (lane == 0) { red_m[warp] = lm; red_s[warp] = ls; red_z[warp] = lz; red_av[warp] = av; red_ai[warp] = ai; }
     __syncthreads();
     if (warp == 0) {
       float wm = lane < BLOCK / 32 ? red_m[lane] : -INFINITY;
       float ws = lane < BLOCK / 32 ? red_s[lane] : 0.f;
       float wz = lane < BLOCK / 32 ? red_z[lane] : 0.f;
+      float wav = lane < BLOCK / 32 ? red_av[lane] : -INFINITY;
+      int wai = lane < BLOCK / 32 ? red_ai[lane] : 0x7fffffff;
       warp_ms(wm, ws);
       wz = warp_sum(wz);
+      if (want_arg) {
+        warp_am(wav, wai);
+        if (lane == 0) bcast_arg = wai;
+      }
       if (lane == 0) {
         float zt = 0.f;
         if (yl >= 0 && yl < n) {
@@ -154,6 +188,11 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
     scale = 1.f / (float)(nv > 0 ? nv : 1);
   }
   if (tid == 0) {
+    if (want_arg) {  // global column; the finalize of a vocab shard is not supported (row_stats path)
+      const int64_t am = a.row_stats ? -1 : (int64_t)bcast_arg + a.col_offset;
+      if (a.pred_rows) a.pred_rows[row] = am;
+      if (a.correct_rows) a.correct_rows[row] = am == y ? 1.f : 0.f;
+    }
     // LK/ops/cross_entropy.py:259-289
     float loss = lse - zy;
     if (lsm > 0.f) loss = loss * (1.f - lsm) + (-eps * sz + lsm * lse);

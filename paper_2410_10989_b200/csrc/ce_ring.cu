@@ -44,6 +44,7 @@ using ring::Pairs;
 
 struct Smem {
   float4 red[2][NC];
+  float2 am[2][NC];  // per-warp argmax (value, index bits) for token accuracy / predicted tokens
   float zt[2];
 };
 
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   }
   const int tid = threadIdx.x;
   const float2 l2e2 = make_float2(L2E, L2E);
+  const bool want_arg = a.correct_rows || a.pred_rows;
   ring::Cursor cur(stages);
   int par = 0;
   for (int64_t i = 0; i < n_local; ++i) {
@@ -128,6 +130,8 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       if (tid == 0) {
         if (a.loss_rows) a.loss_rows[row] = 0.f;
         if (a.z_loss_rows) a.z_loss_rows[row] = 0.f;
+        if (a.correct_rows) a.correct_rows[row] = 0.f;
+        if (a.pred_rows) a.pred_rows[row] = -1;
       }
       continue;
     }
@@ -143,12 +147,15 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     // ---- pass 1: online (max, sumexp[, sum]) ----
     float m = -INFINITY, se = 0.f;
     float2 sz2 = make_float2(0.f, 0.f);
+    float av = -INFINITY;  // argmax (option): value, first column
+    int ai = 0x7fffffff;
     if constexpr (PART) {
       const float4* pp = a.partials + row * a.n_parts;
       for (int64_t jp = tid; jp < a.n_parts; jp += NC * 32) {
         const float4 q = pp[jp];
         ms_combine(m, se, q.x, q.y);
         sz2.x += q.z;
+        if (want_arg) am_merge(av, ai, q.x, __float_as_int(q.w));
       }
     }
     for (int64_t j = 0; j < (PART ? 0 : npc); ++j, cur.next()) {
@@ -186,6 +193,18 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
           }
         se = se * ex2((m - mn) * L2E) + (acc.x + acc.y);  // m = -inf: ex2(-inf) = 0, se = 0
         m = mn;
+        if (want_arg && lmax > av) {  // option; strict: earlier columns keep ties
+          const int cbase = (int)(j * (int64_t)(PIECE / sizeof(T)));
+#pragma unroll
+          for (int k = KPL - 1; k >= 0; --k)
+#pragma unroll
+            for (int e = NP - 1; e >= 0; --e) {
+              const int c = cbase + (v0 + 32 * k) * NV + 2 * e;
+              if (z[k][e].y == lmax) ai = c + 1;
+              if (z[k][e].x == lmax) ai = c;
+            }
+          av = lmax;
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < KPL; ++k) {
@@ -212,12 +231,28 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         }
         se = (m == -INFINITY ? 0.f : se * ex2((m - mn) * L2E)) + (acc.x + acc.y);
         m = mn;
+        if (want_arg && lmax > av) {
+          const int cbase = (int)(j * (int64_t)(PIECE / sizeof(T)));
+#pragma unroll
+          for (int k = KPL - 1; k >= 0; --k)
+#pragma unroll
+            for (int e = NP - 1; e >= 0; --e) {
+              const int c = cbase + (v0 + 32 * k) * NV + 2 * e;
+              if (z[k][e].y == lmax) ai = c + 1;
+              if (z[k][e].x == lmax) ai = c;
+            }
+          av = lmax;
+        }
       }
     }
     float sz = sz2.x + sz2.y;
     warp_ms(m, se);
     if (LS) sz = warp_sum(sz);
-    if (lane == 0) sh->red[par][warp] = make_float4(m, se, sz, 0.f);
+    if (want_arg) warp_am(av, ai);
+    if (lane == 0) {
+      sh->red[par][warp] = make_float4(m, se, sz, 0.f);
+      sh->am[par][warp] = make_float2(av, __int_as_float(ai));
+    }
     ring::consumers_sync(1, NC * 32);
     m = -INFINITY; se = 0.f; sz = 0.f;
 #pragma unroll
@@ -227,6 +262,14 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       sz += r.z;
     }
     const float zy = sh->zt[par];
+    if (want_arg && tid == 0) {
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int c = 0; c < NC; ++c) am_merge(bv, bi, sh->am[par][c].x, __float_as_int(sh->am[par][c].y));
+      const int64_t am = (int64_t)bi + a.col_offset;
+      if (a.pred_rows) a.pred_rows[row] = am;
+      if (a.correct_rows) a.correct_rows[row] = am == y ? 1.f : 0.f;
+    }
     par ^= 1;
     const float lse = m + logf(se);
     if (tid == 0) {  // LK/ops/cross_entropy.py:259-289

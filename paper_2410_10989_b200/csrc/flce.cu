@@ -351,6 +351,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     le.bias = a->bias; le.softcap = a->softcap; le.target = a->target + lo; le.col_offset = 0;
     le.ignore_index = a->ignore_index; le.partials = parts; le.n_parts = L.nparts; le.tgt_logit = tgt;
     le.M = r; le.N = V; le.want_sum = a->label_smoothing > 0.f ? 1 : 0;
+    le.want_argmax = (a->token_correct_rows || a->predicted_tokens) ? 1 : 0;
     {
       ProfScope ps(0, st);
       if (tc) {
@@ -373,6 +374,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     ce.reduction = a->reduction; ce.compute_grad = want_grad ? 1 : 0;
     ce.n_valid = a->mean_count ? a->mean_count : counts;
     ce.loss_rows = a->loss_rows + lo; ce.z_loss_rows = a->z_loss_rows ? a->z_loss_rows + lo : nullptr;
+    ce.correct_rows = a->token_correct_rows ? a->token_correct_rows + lo : nullptr;
+    ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {
       ProfScope ps(1, st);

@@ -35,6 +35,7 @@ struct EpiArgs {
   int64_t n_parts;
   float* tgt_logit;       // [M] (legacy register epilogue only)
   int want_sum;           // EPI_LOGITS: also accumulate sum of logits (label smoothing)
+  int want_argmax;        // EPI_LOGITS: first column of the tile max -> partials[].w (int bits)
   int64_t M, N;           // valid output extent
 };
 

@@ -227,6 +227,8 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
   const float inv_cap = cap ? 1.f / e.softcap : 0.f;
   float m = -INFINITY, s = 0.f, sz = 0.f, tv = 0.f;
   bool have_t = false;
+  float best_v = -INFINITY;
+  int best_i = 0;
   T* orow = static_cast<T*>(e.out) + grow * e.ldo;
   const bool vec_ok = (e.ldo % 8) == 0;
 #pragma unroll 1
@@ -250,6 +252,14 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (j < nvalid) cm = fmaxf(cm, v[j]);
+    if (e.want_argmax && cm > best_v) {
+      int jj = 0;
+#pragma unroll
+      for (int j = 31; j >= 0; --j)
+        if (j < nvalid && v[j] == cm) jj = j;
+      best_v = cm;
+      best_i = (int)(col0 + jj);
+    }
     const float mn = fmaxf(m, cm);
     float acc = 0.f, zs = 0.f;
 #pragma unroll
@@ -271,7 +281,7 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
     }
   }
   if (row_ok) {
-    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
+    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, e.want_argmax ? __int_as_float(best_i) : 0.f);
     if (have_t) e.tgt_logit[grow] = tv;
   }
 }
@@ -493,7 +503,10 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
   constexpr float LOG2E = 1.4426950408889634f;
   const bool row_ok = grow < e.M;
   const bool want_sum = LOGITS && e.want_sum;
+  const bool want_arg = LOGITS && e.want_argmax;
   float m = -INFINITY, s = 0.f, sz = 0.f;
+  float best_v = -INFINITY;  // argmax (token accuracy / predicted tokens): first column of the max
+  int best_i = 0;
 #pragma unroll 1
   for (int g = 0; g < BN / 64; ++g) {
     uint32_t r0[32], r1[32];
@@ -507,6 +520,20 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
       const int nvalid = (int)(rem < 64 ? (rem > 0 ? rem : 0) : 64);
       float v[64];
       logits_values<T>(e, r0, r1, col0, nvalid, v);
+      if (want_arg && nvalid > 0) {  // warp-uniform option branch, off on the default path
+        float gm = -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (j < nvalid) gm = fmaxf(gm, v[j]);
+        if (gm > best_v) {  // strict: an earlier group keeps ties (first index wins)
+          int jj = 0;
+#pragma unroll
+          for (int j = 63; j >= 0; --j)  // static indices: v stays in registers
+            if (j < nvalid && v[j] == gm) jj = j;
+          best_v = gm;
+          best_i = (int)(col0 + jj);
+        }
+      }
       if (nvalid == 64) {
         const float mn = fmaxf(m, tree_max<64>(v));
         const float ml = mn * LOG2E;
@@ -550,7 +577,8 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
     // EPI_ACCUM into a 16-bit grad_w (weight-dtype accumulation): later chunks reduce-add
     sg.flush(omap, buf, (int)col0, row0, !LOGITS && e.kind == EPI_ACCUM && e.beta != 0, lane);
   }
-  if (LOGITS && row_ok) e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, 0.f);
+  if (LOGITS && row_ok)
+    e.partials[grow * e.n_parts + n_blk] = make_float4(m, s, sz, want_arg ? __int_as_float(best_i) : 0.f);
 }
 
 // fp32 output: plain store (F32 / first dW chunk) or reduce-add (later dW chunks).

@@ -82,8 +82,8 @@ def fused_linear_cross_entropy_forward(
     """
     if ce_weight is not None:
         raise errors.UnsupportedOption("ce_weight is not implemented in the B200 build")
-    if use_token_scaling or return_token_accuracy or return_predicted_tokens:
-        raise errors.UnsupportedOption("token scaling / accuracy / predicted tokens are not implemented")
+    if use_token_scaling:
+        raise errors.UnsupportedOption("use_token_scaling is not implemented in the B200 build")
     if not (0.0 <= label_smoothing <= 1.0):
         raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
     if reduction not in _capi.REDUCTIONS:
@@ -119,6 +119,8 @@ def fused_linear_cross_entropy_forward(
     z_rows = torch.empty(bt, dtype=torch.float32, device=dev) if return_z_loss else None
     z_sum = torch.empty((), dtype=torch.float32, device=dev) if return_z_loss else None
     stats = torch.empty(2, dtype=torch.int64, device=dev)
+    correct = torch.empty(bt, dtype=torch.float32, device=dev) if return_token_accuracy else None
+    pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None
     L = lib()
     dt = dtype_code(x)
     cr = int(chunk_rows or 0)
@@ -142,6 +144,7 @@ def fused_linear_cross_entropy_forward(
         grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=ptr(ws), workspace_bytes=ws.numel(),
         stream=stream_of(x), force_simt=int(bool(force_simt)),
         mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
+        token_correct_rows=ptr(correct), predicted_tokens=ptr(pred),
     )
     if mean_count is not None and (mean_count.dtype != torch.int64 or not mean_count.is_cuda):
         raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")
@@ -151,10 +154,14 @@ def fused_linear_cross_entropy_forward(
     if reduction == "none":
         loss = loss_rows
         z_loss = z_rows.to(x.dtype) if return_z_loss else None
+        acc = correct
     else:
         loss = loss_sum
         z_loss = z_sum.to(x.dtype) if return_z_loss else None
-    return loss, z_loss, None, None, grad_x, grad_w, grad_b
+        # mean over non-ignored tokens (LK/ops/fused_linear_cross_entropy.py:234-236)
+        denom = (mean_count[:1] if mean_count is not None else stats[:1]).clamp(min=1)
+        acc = correct.sum() / denom[0] if return_token_accuracy else None
+    return loss, z_loss, acc, pred, grad_x, grad_w, grad_b
 
 
 def fused_linear_cross_entropy_backward(grad_output, grad_input, grad_weight, grad_bias):

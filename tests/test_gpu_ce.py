@@ -189,3 +189,40 @@ def test_rowfuse_inplace_contract_port_vs_gpu(golden):
     rp.cross_entropy_(ref, golden["ce_rand_a_target"], mean=True)
     ok, err = rel_close(buf.cpu().numpy(), ref, 1e-4)
     assert ok, err
+
+
+@pytest.mark.parametrize("impl", ["ring", "block"])
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+@pytest.mark.parametrize("cap", [None, 20.0])
+def test_ce_token_accuracy_and_predicted_tokens(impl, reduction, cap, monkeypatch):
+    """Liger return_token_accuracy / return_predicted_tokens (LK/ops/cross_entropy.py:131-163, 294-299, 415-420)."""
+    monkeypatch.setenv("LK_CE_IMPL", impl)
+    rows, v = 300, 32000
+    g = torch.Generator(device="cuda").manual_seed(7)
+    z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    zz = z.float() if cap is None else (cap * torch.tanh(z.float() / cap))
+    t[::3] = zz[::3].argmax(1)  # a third of the rows predicted correctly
+    t[::7] = -100
+    x = z.clone().requires_grad_(True)
+    out = lk.LigerCrossEntropyLoss(reduction=reduction, softcap=cap, return_token_accuracy=True,
+                                   return_predicted_tokens=True)(x, t)
+    want_pred = zz.argmax(1)
+    want_pred[t == -100] = -1
+    pred = out.predicted_tokens
+    ign = t == -100
+    if cap is None:
+        assert torch.equal(pred, want_pred)
+    else:  # bf16 tanh.approx vs torch tanh: a near-tie may resolve to a neighbour within one ulp
+        assert (pred == want_pred).float().mean().item() > 0.99
+        assert torch.all(pred[ign] == -1)
+    correct = ((pred == t) & ~ign).float()
+    if reduction == "none":
+        assert torch.equal(out.token_accuracy, correct)
+    else:
+        assert abs(out.token_accuracy.item() - correct.sum().item() / (~ign).sum().item()) < 1e-6
+    out.loss.sum().backward()  # gradients are unaffected by the options
+    ref = lk.LigerCrossEntropyLoss(reduction=reduction, softcap=cap)
+    x2 = z.clone().requires_grad_(True)
+    ref(x2, t).sum().backward()
+    assert torch.equal(x.grad, x2.grad)

@@ -270,3 +270,39 @@ def test_cfg4_gemma2_head_softcap_smoothing():
     assert abs(loss.item() - rloss.item()) <= 2e-2 * abs(rloss.item())
     assert close(gx, rgx, 2e-2), rel_err(gx, rgx)
     assert close(gw, rgw, 2e-2), rel_err(gw, rgw)
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("kw", [dict(), dict(softcap=30.0, label_smoothing=0.1)])
+def test_flce_token_accuracy_and_predicted_tokens(simt, kw):
+    """Liger return_token_accuracy / return_predicted_tokens on the FLCE head (argmax of the rounded,
+    softcapped logits; the tcgen05 path tracks it in the logits epilogue, no extra pass)."""
+    xb, wb, tb, x, w, t = bf16_problem(700, 256, 5000, seed=21)
+    if simt:
+        xb, wb = xb.float(), wb.float()
+    logits = xb.float() @ wb.float().T
+    if "softcap" in kw:
+        logits = kw["softcap"] * torch.tanh(logits / kw["softcap"])
+    logits = logits.to(xb.dtype).float()
+    tb = tb.clone()
+    tb[::4] = logits[::4].argmax(1)
+    tb[::9] = -100
+    loss, _, acc, pred, gx, gw, _ = flce_fwd(xb, wb, tb, compute_grad_input=True, compute_grad_weight=True,
+                                              return_token_accuracy=True, return_predicted_tokens=True,
+                                              force_simt=simt, chunk_rows=256, **kw)
+    ign = tb == -100
+    want = logits.argmax(1)
+    want[ign] = -1
+    assert torch.all(pred[ign] == -1)
+    agree = (pred == want).float().mean().item()
+    assert agree > 0.99, agree
+    mism = (pred != want) & ~ign
+    if mism.any():  # GEMM summation order: a disagreement is a near-tie of the rounded logits
+        r = mism.nonzero().flatten()
+        gap = (logits[r, want[r]] - logits[r, pred[r]]).abs()
+        assert torch.all(gap <= 2 ** -7 * logits[r, want[r]].abs() + 1e-6)
+    correct = ((pred == tb) & ~ign).float()
+    assert abs(acc.item() - correct.sum().item() / (~ign).sum().item()) < 1e-6
+    loss2, _, _, _, gx2, gw2, _ = flce_fwd(xb, wb, tb, compute_grad_input=True, compute_grad_weight=True,
+                                           force_simt=simt, chunk_rows=256, **kw)
+    assert loss.item() == loss2.item() and torch.equal(gx, gx2) and torch.equal(gw, gw2)
