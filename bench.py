@@ -40,6 +40,10 @@ BT, H, V = 8192, 4096, 128256
 IGNORE_FRAC = 0.1
 METRIC = "FLCE fwd+bwd tokens/s & peak mem @Llama-3-8B head; % tensor/HBM roofline"
 WORKLOAD = "cfg2: Llama-3-8B lm_head FLCE fwd+bwd, BT=8192 tokens, H=4096, V=128256, bf16, 10% ignore_index"
+# --config cfg4 (BASELINE.json configs[3]; not the headline line): Gemma-2-9B head
+CFG4 = dict(hidden=3584, vocab=256000, softcap=30.0, label_smoothing=0.1,
+            workload="cfg4: Gemma-2-9B lm_head FLCE fwd+bwd, BT=8192 tokens, H=3584, V=256000, softcap 30, "
+                     "label_smoothing 0.1, bf16, 10% ignore_index")
 
 
 def env_rank():
@@ -198,6 +202,8 @@ def run_ours(args):
     torch.cuda.set_device(dev)
     L = _capi.load()
     bt, h, v = args.bt, args.hidden, args.vocab
+    opts = dict(softcap=args.softcap, label_smoothing=args.label_smoothing)
+    workload = CFG4["workload"] if args.config == "cfg4" else WORKLOAD
 
     # token mode: every rank its own BT tokens (weak scaling); vocab mode: one global problem,
     # W rows sharded over ranks (strong scaling of the GEMM work)
@@ -213,10 +219,10 @@ def run_ours(args):
 
     def step():
         if vocab_mode:
-            return vocab_parallel_flce(x, w, t, shard, chunk_rows=chunk)
+            return vocab_parallel_flce(x, w, t, shard, chunk_rows=chunk, **opts)
         if world > 1:
-            return token_sharded_flce(x, w, t, chunk_rows=chunk)
-        return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True,
+            return token_sharded_flce(x, w, t, chunk_rows=chunk, **opts)
+        return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True, **opts,
                                                   compute_grad_weight=True)
 
     def barrier():
@@ -275,16 +281,16 @@ def run_ours(args):
     xh = x.cpu().pin_memory()
     th = t.cpu().pin_memory()
     wp = torch.nn.Parameter(w.clone())
-    loss_fn = lk.LigerFusedLinearCrossEntropyLoss(chunk_rows=chunk)
+    loss_fn = lk.LigerFusedLinearCrossEntropyLoss(chunk_rows=chunk, **opts)
 
     def e2e_step():
         xd = xh.to(dev, non_blocking=True).requires_grad_(True)
         td = th.to(dev, non_blocking=True)
         if vocab_mode:
-            loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk)
+            loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, **opts)
             val = loss.item()
         elif world > 1:
-            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk)
+            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk, **opts)
             val = loss.item()
         else:
             loss = loss_fn(wp, xd, td)
@@ -337,7 +343,8 @@ def run_ours(args):
             "scaling": "strong" if vocab_mode else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform X, W, 10% ignore_index targets)",
             "config": {
-                "workload": WORKLOAD, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
+                "workload": workload, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
+                "softcap": args.softcap, "label_smoothing": args.label_smoothing,
                 "num_chunks": -(-bt // chunk), "global_tokens": tokens_per_step,
                 "parallelism": (f"vocab-parallel vp{world}" if vocab_mode else
                                 (f"token-sharded dp{world}" if world > 1 else "single GPU")),
@@ -382,12 +389,19 @@ def main():
     ap.add_argument("--hidden", type=int, default=H)
     ap.add_argument("--vocab", type=int, default=V)
     ap.add_argument("--chunk-rows", type=int, default=0)
+    ap.add_argument("--config", choices=["cfg2", "cfg4"], default="cfg2",
+                    help="cfg2 = Llama-3-8B head (headline); cfg4 = Gemma-2-9B head with softcap 30 + smoothing 0.1")
+    ap.add_argument("--softcap", type=float, default=None)
+    ap.add_argument("--label-smoothing", type=float, default=0.0)
     ap.add_argument("--mode", choices=["token", "vocab"], default="token",
                     help="multi-GPU shard mode: token-sharded (default, weak scaling) or vocab-parallel (strong)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.config == "cfg4":
+        args.hidden, args.vocab = CFG4["hidden"], CFG4["vocab"]
+        args.softcap, args.label_smoothing = CFG4["softcap"], CFG4["label_smoothing"]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

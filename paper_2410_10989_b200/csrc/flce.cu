@@ -357,7 +357,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
       if (tc) {
         tc::TmaOperand A{xc, H, r, H, 0}, B{a->weight, H, V, H, 0};
         tc::Problem P{};
-        P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
+        P.M = r; P.N = V; P.K = H; P.epi = le;
+        P.n_fast = getenv("LK_LOGITS_NFAST") ? 1 : 0;  // experiment hook: tile raster order
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
       } else {
         Operand A{xc, H, 1}, B{a->weight, H, 1};

@@ -2,12 +2,14 @@
 //
 // Forward (rowfuse/ops.py:248-275; Liger LK/ops/layer_norm.py:169-227):
 //   mu = mean(x), r = 1/sqrt(mean((x - mu)^2) + eps), y = (x - mu) * r * w + b,
-//   per-row mean and r cached in fp32.  One CTA per row, the row in registers, two
-//   reductions (centred variance, as the reference computes it), packed fp32x2 math.
+//   per-row mean and r cached in fp32.  One CTA per row, the row in registers, sums shifted
+//   by the row's first element so one CTA reduction (a single barrier) gives the centred
+//   variance without the E[x^2] - mean^2 cancellation; packed fp32x2 math.
 // Backward (rowfuse/ops.py:278-311; LK/ops/layer_norm.py:230-304):
 //   xt = (x - mu) r, gy = dy w, dx = r (gy - (xt . gy / n) xt - sum(gy) / n),
 //   dw = sum_rows dy xt, db = sum_rows dy.  Persistent CTAs over contiguous row ranges,
-//   next row prefetched into registers, both row reductions in one CTA barrier, dw/db
+//   rows prefetched `slots` ahead into a shared-memory ring by 1D bulk copies (issued by
+//   thread 0 after the row barrier), both row reductions in one CTA barrier, dw/db
 //   partials in registers -> one partial row each per CTA -> fixed-order column sums
 //   (rowfuse's _tree_sum role, ops.py:138-152): bitwise deterministic for a given grid.
 #include "norm_cta.cuh"
@@ -37,7 +39,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_cta(const T* __restrict__ x
                                                          int rows, int cols, float eps) {
   using P = ring::Pairs<T>;
   constexpr int NP = P::NP, NV = 16 / sizeof(T);
-  __shared__ float sh[64];
+  __shared__ float sh[128];
   const int nvec = cols / NV, row = blockIdx.x, tid = threadIdx.x, nt = blockDim.x;
   const T* xr = x + (int64_t)row * cols;
   float2 f[VPT][NP];
@@ -46,26 +48,29 @@ __global__ void __launch_bounds__(256) layernorm_fwd_cta(const T* __restrict__ x
     const int v = tid + k * nt;
     P::unpack(v < nvec ? ldg_stream(xr + v * NV) : make_uint4(0, 0, 0, 0), f[k]);
   }
-  float2 s = make_float2(0.f, 0.f);
-#pragma unroll
-  for (int k = 0; k < VPT; ++k)
-#pragma unroll
-    for (int e = 0; e < NP; ++e) s = __fadd2_rn(s, f[k][e]);
-  const float mu = cta_sum(s.x + s.y, sh, 0) / (float)cols;
-  const float2 nmu = make_float2(-mu, -mu);
-  float2 q = make_float2(0.f, 0.f);
+  // shifted sums around K = x[row, 0] (one broadcast L1 load): var = (S2 - S1^2 / n) / n with
+  // S1 = sum(x - K), S2 = sum((x - K)^2) -- one CTA reduction of two values, and no
+  // E[x^2] - mean^2 cancellation because K sits inside the row's distribution
+  const float K = to_f<T>(xr[0]);
+  const float2 nk = make_float2(-K, -K);
+  float2 s1 = make_float2(0.f, 0.f), s2 = make_float2(0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
-    const bool in = tid + k * nt < nvec;
+    if (tid + k * nt >= nvec) continue;
 #pragma unroll
     for (int e = 0; e < NP; ++e) {
-      f[k][e] = in ? __fadd2_rn(f[k][e], nmu) : make_float2(0.f, 0.f);  // centred; padding stays 0
-      q = __ffma2_rn(f[k][e], f[k][e], q);
+      const float2 d = __fadd2_rn(f[k][e], nk);
+      s1 = __fadd2_rn(s1, d);
+      s2 = __ffma2_rn(d, d, s2);
     }
   }
-  const float r = rsqrtf(cta_sum(q.x + q.y, sh, 1) / (float)cols + eps);
+  const float2 tot = cta_sum2(s1.x + s1.y, s2.x + s2.y, reinterpret_cast<float*>(sh), 0);
+  const float dm = tot.x / (float)cols;
+  const float mu = K + dm;
+  const float m2 = fmaxf(tot.y - tot.x * dm, 0.f);
+  const float r = rsqrtf(m2 / (float)cols + eps);
   if (tid == 0) { mean[row] = mu; rstd[row] = r; }
-  const float2 r2 = make_float2(r, r);
+  const float2 nmu = make_float2(-mu, -mu), r2 = make_float2(r, r);
   T* yr = y + (int64_t)row * cols;
 #pragma unroll
   for (int k = 0; k < VPT; ++k) {
@@ -76,7 +81,7 @@ __global__ void __launch_bounds__(256) layernorm_fwd_cta(const T* __restrict__ x
       if (b) P::unpack(__ldg(reinterpret_cast<const uint4*>(b) + v), bv);
 #pragma unroll
       for (int e = 0; e < NP; ++e) {
-        const float2 t = __fmul2_rn(__fmul2_rn(f[k][e], r2), wv[e]);
+        const float2 t = __fmul2_rn(__fmul2_rn(__fadd2_rn(f[k][e], nmu), r2), wv[e]);
         f[k][e] = b ? __fadd2_rn(t, bv[e]) : t;
       }
       ring::stg128(yr + v * NV, P::pack(f[k]));
@@ -89,11 +94,14 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
                                                          const T* __restrict__ w, const float* __restrict__ mean,
                                                          const float* __restrict__ rstd, T* dx,
                                                          float* __restrict__ dw_part, float* __restrict__ db_part,
-                                                         int rows, int cols) {
+                                                         int rows, int cols, int slots) {
   using P = ring::Pairs<T>;
   constexpr int NP = P::NP, NV = 16 / sizeof(T);
   __shared__ float sh[128];
+  __shared__ uint64_t full[8];
+  extern __shared__ __align__(128) uint8_t ring_sm[];
   const int nvec = cols / NV, tid = threadIdx.x, nt = blockDim.x;
+  const uint32_t rb = (uint32_t)cols * sizeof(T);
   const int per = (rows + gridDim.x - 1) / gridDim.x;
   const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
   float2 aw[VPT][NP], ab[VPT][NP], wv[VPT][NP];
@@ -107,33 +115,38 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
       if (v >= nvec) wv[k][e] = make_float2(0.f, 0.f);
     }
   }
-  uint4 gn[VPT], xn[VPT];
-  auto load = [&](int row) {
-#pragma unroll
-    for (int k = 0; k < VPT; ++k) {
-      const int v = tid + k * nt;
-      const bool ok = row < r1 && v < nvec;
-      const int64_t off = (int64_t)row * cols + v * NV;
-      gn[k] = ok ? ldg_stream(dy + off) : make_uint4(0, 0, 0, 0);
-      xn[k] = ok ? ldg_stream(x + off) : make_uint4(0, 0, 0, 0);
-    }
+  auto issue = [&](int row, int slot) {  // thread 0 only: dy row and x row into one ring slot
+    uint8_t* st = ring_sm + (size_t)slot * 2 * rb;
+    ring::expect_tx(&full[slot], 2 * rb);
+    ring::bulk_g2s(st, dy + (int64_t)row * cols, rb, &full[slot]);
+    ring::bulk_g2s(st + rb, x + (int64_t)row * cols, rb, &full[slot]);
   };
-  load(r0);
+  if (tid == 0) {
+    for (int q = 0; q < slots; ++q) ring::mbar_init(&full[q], 1);
+    ring::fence_init();
+    for (int q = 0; q < slots && r0 + q < r1; ++q) issue(r0 + q, q);
+  }
+  __syncthreads();
+  const uint32_t base = ring::s_u32(ring_sm);
+  ring::Cursor cur(slots);
   int par = 0;
-  for (int row = r0; row < r1; ++row, par ^= 1) {
+  for (int row = r0; row < r1; ++row, par ^= 1, cur.next()) {
     const float mu = mean[row], r = rstd[row];
     const float2 nmu = make_float2(-mu, -mu), r2 = make_float2(r, r);
+    const uint32_t st = base + (uint32_t)cur.s * 2u * rb;
+    ring::wait(&full[cur.s], cur.phase);
     float2 xt[VPT][NP], gy[VPT][NP];
     float2 pj = make_float2(0.f, 0.f), sf = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < VPT; ++k) {
+      const int v = tid + k * nt;
+      const bool in = v < nvec;
       float2 g[NP], xv[NP];
-      P::unpack(gn[k], g);
-      P::unpack(xn[k], xv);
+      P::unpack(in ? ring::lds128(st + (uint32_t)v * 16u) : make_uint4(0, 0, 0, 0), g);
+      P::unpack(in ? ring::lds128(st + rb + (uint32_t)v * 16u) : make_uint4(0, 0, 0, 0), xv);
 #pragma unroll
       for (int e = 0; e < NP; ++e) {
-        xt[k][e] = __fmul2_rn(__fadd2_rn(xv[e], nmu), r2);
-        if (tid + k * nt >= nvec) xt[k][e] = make_float2(0.f, 0.f);
+        xt[k][e] = in ? __fmul2_rn(__fadd2_rn(xv[e], nmu), r2) : make_float2(0.f, 0.f);
         gy[k][e] = __fmul2_rn(g[e], wv[k][e]);
         pj = __ffma2_rn(xt[k][e], gy[k][e], pj);
         sf = __fadd2_rn(sf, gy[k][e]);
@@ -141,8 +154,9 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
         ab[k][e] = __fadd2_rn(ab[k][e], g[e]);
       }
     }
-    load(row + 1);  // next row in flight during the reduction and the write
     const float2 t = cta_sum2(pj.x + pj.y, sf.x + sf.y, sh, par);
+    // every thread is past its reads of this slot (cta_sum2's barrier): refill it
+    if (tid == 0 && row + slots < r1) issue(row + slots, cur.s);
     const float proj = t.x / (float)cols, shift = t.y / (float)cols;
     const float2 np2 = make_float2(-proj, -proj), ns2 = make_float2(-shift, -shift);
 #pragma unroll
@@ -255,12 +269,17 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
     LK_DISPATCH_FLOAT(dtype, T, {
       LK_LN_VPT(vpt, VPT, {
         auto kern = ln::layernorm_bwd_cta<T, VPT>;
+        const int64_t rbytes = cols * (int64_t)sizeof(T);
+        const int slots = (int)std::max<int64_t>(2, std::min<int64_t>(3, (96 * 1024) / (2 * rbytes)));
+        const int smem = (int)(slots * 2 * rbytes);
+        LK_REQUIRE(smem <= 200 * 1024, LK_UNSUPPORTED, "row too wide for the LayerNorm backward ring");
+        LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), smem));
         int per_sm = 0;
-        LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
+        LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         grid = std::max<int64_t>(1, std::min<int64_t>({rows, gmax, (int64_t)std::max(1, per_sm) * sm_count()}));
-        kern<<<(unsigned)grid, threads, 0, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
-                                                 static_cast<const T*>(weight), mean, rstd, static_cast<T*>(dx), pw,
-                                                 db ? pb : nullptr, (int)rows, (int)cols);
+        kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
+                                                    static_cast<const T*>(weight), mean, rstd, static_cast<T*>(dx), pw,
+                                                    db ? pb : nullptr, (int)rows, (int)cols, slots);
       });
     });
     int rc = check_launch("layernorm_bwd_cta");
