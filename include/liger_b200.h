@@ -180,6 +180,13 @@ typedef struct {
    * NULL = not computed (the epilogue then skips the argmax search). */
   float* token_correct_rows;  /* [BT] fp32 or NULL */
   int64_t* predicted_tokens;  /* [BT] or NULL      */
+  /* Token-sharded overlap: when > 1 (tcgen05 path, at most 16), the last
+   * chunk's grad_w GEMM runs as this many launches over contiguous vocab-row slices and
+   * grad_w_slice_events[s] (cudaEvent_t, created by the caller) is recorded on `stream` as
+   * soon as rows [s*V/S, (s+1)*V/S) (rounded to 256) of grad_w are final, so the caller can
+   * all-reduce slice s while later slices are still being computed. */
+  int grad_w_slices;
+  void* const* grad_w_slice_events;
 } lk_flce_args;
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };

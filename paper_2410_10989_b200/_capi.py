@@ -65,6 +65,8 @@ class FlceArgs(C.Structure):
         ("grad_w_accum", c_int),
         ("token_correct_rows", c_void),
         ("predicted_tokens", c_void),
+        ("grad_w_slices", c_int),
+        ("grad_w_slice_events", c_void),
     ]
 
 

@@ -255,7 +255,7 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   size_t off = 0;
   auto take = [&](size_t bytes) { off = align_up(off, 1024); size_t o = off; off += bytes; return o; };
   L.off_counts = take(2 * sizeof(int64_t));
-  L.off_sched = take((size_t)(2 * L.nchunks + 2) * sizeof(int));
+  L.off_sched = take((size_t)(2 * L.nchunks + 2 + 16) * sizeof(int));  // + per-slice counters
   L.off_z = take((size_t)L.C * L.ldz * elt_size(dtype));
   L.off_parts = take(tc ? (size_t)L.C * L.nparts * sizeof(float4) : 0);
   L.off_tgt = take(tc ? (size_t)L.C * sizeof(float) : 0);
@@ -330,7 +330,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   if (rc) return rc;
   if (a->target_stats)
     LK_CUDA(cudaMemcpyAsync(a->target_stats, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-  if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2) * sizeof(int), st));
+  if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
   if (BT == 0) {
     if (a->loss_sum) LK_CUDA(cudaMemsetAsync(a->loss_sum, 0, sizeof(float), st));
     if (a->z_loss_sum) LK_CUDA(cudaMemsetAsync(a->z_loss_sum, 0, sizeof(float), st));
@@ -428,7 +428,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
         ++np;
       }
-      if (a->grad_w) {
+      const int slices = (last && a->grad_w && a->grad_w_slice_events) ? std::min(a->grad_w_slices, 16) : 1;
+      if (a->grad_w && slices <= 1) {
         As[np] = {zbuf, V, r, L.ldz, 1};
         Bs[np] = {xc, H, r, H, 1};
         Ps[np] = tc::Problem{};
@@ -436,6 +437,24 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         ++np;
       }
       if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, dt, sched + 2 * ci + 1, st);
+      // token-sharded overlap: the last chunk's dW in vocab-row slices, one event per slice
+      const int64_t step = (V + slices - 1) / slices;
+      const int64_t sl_rows = (step + 255) / 256 * 256;
+      for (int sl = 0; !rc && slices > 1 && sl < slices; ++sl) {
+        const int64_t v0 = sl * sl_rows, v1 = std::min<int64_t>(V, v0 + sl_rows);
+        if (v0 < v1) {
+          EpiArgs ws = we;
+          ws.out = static_cast<char*>(a->grad_w) + v0 * H * es;
+          if (ws.acc) ws.acc = ws.acc + v0 * H;
+          ws.M = v1 - v0;
+          tc::TmaOperand As1{static_cast<const char*>(zbuf) + v0 * es, v1 - v0, r, L.ldz, 1};
+          tc::TmaOperand Bs1{xc, H, r, H, 1};
+          tc::Problem P1{};
+          P1.M = v1 - v0; P1.N = H; P1.K = r; P1.n_fast = 1; P1.epi = ws;
+          rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, dt, sched + 2 * L.nchunks + 2 + sl, st);
+        }
+        if (!rc) LK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->grad_w_slice_events[sl]), st));
+      }
     } else {
       if (a->grad_x) {
         Operand A{zbuf, L.ldz, 1}, B{a->weight, 1, H};

@@ -53,6 +53,27 @@ def _local_flce_cuda(x, w, t, mean_count, **kw):
     return loss, gx, gw
 
 
+def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw):
+    """Local FLCE whose last-chunk grad_w GEMM is split into `dw_slices` vocab-row slices;
+    slice s is all-reduced on a side stream as soon as its event fires, so all but the last
+    slice's all-reduce hide under the remaining dW GEMM launches."""
+    events = [torch.cuda.Event() for _ in range(dw_slices)]
+    loss, gx, gw = local_fn(x, w, t, counts, grad_w_slice_events=events, **kw)
+    v = gw.shape[0]
+    step = -(-v // dw_slices)
+    rows = -(-step // 256) * 256  # same slice bounds as the library (flce.cu)
+    comm = torch.cuda.Stream(device=gw.device)
+    for s, ev in enumerate(events):
+        lo, hi = s * rows, min(v, (s + 1) * rows)
+        comm.wait_event(ev)
+        if lo < hi:
+            with torch.cuda.stream(comm):
+                dist.all_reduce(gw[lo:hi], op=dist.ReduceOp.SUM, group=group)
+    torch.cuda.current_stream(gw.device).wait_stream(comm)
+    gw.record_stream(comm)
+    return loss, gx, gw
+
+
 def token_sharded_flce(
     x_local: torch.Tensor,
     weight: torch.Tensor,
@@ -63,20 +84,30 @@ def token_sharded_flce(
     count_fn: Optional[Callable] = None,
     local_fn: Optional[Callable] = None,
     reduce_grad_weight: bool = True,
+    dw_slices: int = 4,
     **kw,
 ):
-    """Returns (global loss, local grad_x, all-reduced grad_w)."""
+    """Returns (global loss, local grad_x, all-reduced grad_w).
+
+    With the CUDA kernels (default `local_fn`) and `dw_slices` > 1, the grad_w all-reduce
+    overlaps the last chunk's grad_w GEMM (`_allreduce_grad_w_overlapped`).
+    """
     t = as_targets(target_local) if target_local.is_cuda else target_local.reshape(-1).to(torch.int64)
     count_fn = count_fn or (lambda tt: _count_cuda(tt, weight.shape[0], ignore_index))
+    overlap = local_fn is None and reduce_grad_weight and dw_slices > 1 and x_local.is_cuda
     local_fn = local_fn or _local_flce_cuda
     counts = count_fn(t)
     if reduction == "mean":
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
-    loss, gx, gw = local_fn(x_local, weight, t, counts, ignore_index=ignore_index, reduction=reduction, **kw)
+    kw = dict(kw, ignore_index=ignore_index, reduction=reduction)
+    if overlap:
+        loss, gx, gw = _allreduce_grad_w_overlapped(x_local, weight, t, counts, group, dw_slices, local_fn, kw)
+    else:
+        loss, gx, gw = local_fn(x_local, weight, t, counts, **kw)
+        if reduce_grad_weight and gw is not None:
+            dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=group)
     loss = loss.clone()
     dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
-    if reduce_grad_weight and gw is not None:
-        dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=group)
     return loss, gx, gw
 
 

@@ -68,6 +68,7 @@ def fused_linear_cross_entropy_forward(
     compute_grad_input: Optional[bool] = None,
     compute_grad_weight: Optional[bool] = None,
     mean_count: Optional[torch.Tensor] = None,
+    grad_w_slice_events=None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -78,7 +79,9 @@ def fused_linear_cross_entropy_forward(
     weight dtype when the plan has <= 8 chunks (no fp32 workspace: peak memory ~ one
     logits chunk), fp32 beyond that.  Returned in weight.dtype, as Liger does.
     `mean_count` (CUDA int64 scalar) overrides the MEAN denominator with a global
-    non-ignored count (token-sharded mode).
+    non-ignored count (token-sharded mode).  `grad_w_slice_events` (list of torch.cuda.Event)
+    splits the last chunk's grad_w GEMM into that many vocab-row slices and records event s
+    when slice s of grad_w is final (overlap of the token-sharded dW all-reduce).
     """
     if ce_weight is not None:
         raise errors.UnsupportedOption("ce_weight is not implemented in the B200 build")
@@ -146,6 +149,14 @@ def fused_linear_cross_entropy_forward(
         mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
         token_correct_rows=ptr(correct), predicted_tokens=ptr(pred),
     )
+    ev_arr = None
+    if grad_w_slice_events:
+        for ev in grad_w_slice_events:  # torch creates the CUDA event lazily on first record
+            if not ev.cuda_event:
+                ev.record(torch.cuda.current_stream(dev))
+        ev_arr = (_capi.C.c_void_p * len(grad_w_slice_events))(*[ev.cuda_event for ev in grad_w_slice_events])
+        args.grad_w_slices = len(grad_w_slice_events)
+        args.grad_w_slice_events = _capi.C.cast(ev_arr, _capi.C.c_void_p)
     if mean_count is not None and (mean_count.dtype != torch.int64 or not mean_count.is_cuda):
         raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")
     check(L.lk_flce_forward_backward(_capi.C.byref(args)))

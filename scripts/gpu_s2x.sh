@@ -1,0 +1,10 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+T=s2x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/${T}_build.log 2>&1
+timeout -s KILL 900 python -m pytest tests -m gpu -q -rf --timeout 300 --timeout-method=thread -p no:cacheprovider > gpurun_out/${T}_tests.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${T}_tests.log
+timeout -s KILL 600 python bench.py > gpurun_out/${T}_bench.log 2>&1
+timeout -s KILL 300 python bench.py --mode vocab --steps 20 --no-cpu-baseline > gpurun_out/${T}_bench_vocab.log 2>&1
+tail -n 4 gpurun_out/${T}_tests.log; for f in bench bench_vocab; do python -c "
+import json; d=json.loads(open('gpurun_out/${T}_'+'$f'+'.log').read().strip().splitlines()[-1]); print('$f', round(d['value']), d['ms_per_step'], d['e2e']['value'], d['clocks']['sm_mhz'])"; done

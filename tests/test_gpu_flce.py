@@ -306,3 +306,20 @@ def test_flce_token_accuracy_and_predicted_tokens(simt, kw):
     loss2, _, _, _, gx2, gw2, _ = flce_fwd(xb, wb, tb, compute_grad_input=True, compute_grad_weight=True,
                                            force_simt=simt, chunk_rows=256, **kw)
     assert loss.item() == loss2.item() and torch.equal(gx, gx2) and torch.equal(gw, gw2)
+
+
+@pytest.mark.parametrize("accum_dtype", [None, torch.float32])
+@pytest.mark.parametrize("slices", [2, 4, 5])
+def test_grad_w_slices_with_events_bitwise(slices, accum_dtype):
+    """Token-sharded overlap hook: the last chunk's grad_w GEMM in vocab-row slices with one
+    event per slice gives bitwise the same gradients (same tiles, same K order)."""
+    xb, wb, tb, *_ = bf16_problem(1000, 256, 5000, seed=31)
+    a = flce(xb, wb, tb, chunk_rows=256, accum_dtype=accum_dtype)
+    events = [torch.cuda.Event() for _ in range(slices)]
+    b_loss, _, _, _, b_gx, b_gw, _ = flce_fwd(xb, wb, tb, compute_grad_input=True, compute_grad_weight=True,
+                                              chunk_rows=256, accum_dtype=accum_dtype, grad_w_slice_events=events)
+    for ev in events:
+        ev.synchronize()
+    torch.cuda.synchronize()
+    assert a[0].item() == b_loss.item()
+    assert torch.equal(a[2], b_gx) and torch.equal(a[3], b_gw)
