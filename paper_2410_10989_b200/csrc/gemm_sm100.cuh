@@ -44,6 +44,7 @@ struct Problem {
   int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
   int tma_out;          // 1: epilogue writes through smem staging + TMA store (map mc<p>)
+  int pf_dist;          // > 0: L2-prefetch the B box this many k-blocks ahead (HBM-streamed operand)
   EpiArgs epi;
 };
 
@@ -142,6 +143,15 @@ __device__ __forceinline__ uint32_t elect_one() {
 }
 __device__ __forceinline__ void umma_commit_addr(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_2d(uint64_t map, int x, int y) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2_3d(uint64_t map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map), "r"(x), "r"(y),
+               "r"(z)
+               : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -474,14 +484,45 @@ __device__ __forceinline__ float tree_max(const float* v) {
   return t[0];
 }
 
-// Logit transform of one 64-column group: (+bias) -> (softcap) -> round to the logits
-// dtype.  The branches are warp-uniform and sit outside the unrolled element loop.
+// Packed 16-bit pairs for the logits epilogue: one F2FP rounds two logits, the max runs on
+// the packed values (HMNMX2 is exact), and the statistics unpack exactly with integer ops --
+// no per-element F2F round trip (which sits on the 16/clk conversion pipe).
+template <typename T> struct P16;
+template <> struct P16<__nv_bfloat16> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t u) {
+    return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+  }
+  static __device__ __forceinline__ uint32_t hmax(uint32_t a, uint32_t b) {
+    __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+};
+template <> struct P16<__half> {
+  static __device__ __forceinline__ uint32_t pack(float a, float b) {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
+  static __device__ __forceinline__ float2 unpack(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
+  static __device__ __forceinline__ uint32_t hmax(uint32_t a, uint32_t b) {
+    __half2 r = __hmax2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+};
+
+// Logit transform of one 64-column group: (+bias) -> (softcap); the caller rounds to the
+// logits dtype when it packs.  The branches are warp-uniform and sit outside the unrolled
+// element loop.
 template <typename T>
 __device__ __forceinline__ void logits_values(const EpiArgs& e, const uint32_t (&r0)[32], const uint32_t (&r1)[32],
                                               int64_t col0, int nvalid, float (&v)[64]) {
 #pragma unroll
   for (int j = 0; j < 64; ++j) v[j] = __uint_as_float(j < 32 ? r0[j] : r1[j - 32]);
   if (e.bias) {
+#pragma unroll
     for (int j = 0; j < 64; ++j)
       if (j < nvalid) v[j] += load_any(e.bias, col0 + j, e.out_dtype);
   }
@@ -490,8 +531,6 @@ __device__ __forceinline__ void logits_values(const EpiArgs& e, const uint32_t (
 #pragma unroll
     for (int j = 0; j < 64; ++j) v[j] = c * tanh_fast(v[j] * ic);
   }
-#pragma unroll
-  for (int j = 0; j < 64; ++j) v[j] = round_to<T>(v[j]);
 }
 
 // 16-bit output (logits with online-softmax partials, or alpha * acc), 64-column groups.
@@ -516,55 +555,88 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
     const int64_t col0 = n0 + g * 64;
     uint32_t w[32];
     if (LOGITS) {
+      using H = P16<T>;
       const int64_t rem = e.N - col0;
       const int nvalid = (int)(rem < 64 ? (rem > 0 ? rem : 0) : 64);
-      float v[64];
-      logits_values<T>(e, r0, r1, col0, nvalid, v);
+      // 1. (+bias) (softcap) and round to the logits dtype: one F2FP per pair of columns
+      if (!e.bias && !(e.softcap > 0.f)) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          w[j] = H::pack(__uint_as_float(r0[2 * j]), __uint_as_float(r0[2 * j + 1]));
+          w[16 + j] = H::pack(__uint_as_float(r1[2 * j]), __uint_as_float(r1[2 * j + 1]));
+        }
+      } else {
+        float v[64];
+        logits_values<T>(e, r0, r1, col0, nvalid, v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) w[j] = H::pack(v[2 * j], v[2 * j + 1]);
+      }
+      // 2. online-softmax statistics of the ROUNDED values (self-consistent with the finalize)
       if (want_arg && nvalid > 0) {  // warp-uniform option branch, off on the default path
         float gm = -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 64; ++j)
-          if (j < nvalid) gm = fmaxf(gm, v[j]);
+        for (int j = 0; j < 32; ++j) {
+          const float2 z = H::unpack(w[j]);
+          if (2 * j < nvalid) gm = fmaxf(gm, z.x);
+          if (2 * j + 1 < nvalid) gm = fmaxf(gm, z.y);
+        }
         if (gm > best_v) {  // strict: an earlier group keeps ties (first index wins)
           int jj = 0;
 #pragma unroll
-          for (int j = 63; j >= 0; --j)  // static indices: v stays in registers
-            if (j < nvalid && v[j] == gm) jj = j;
+          for (int j = 31; j >= 0; --j) {  // static indices: w stays in registers
+            const float2 z = H::unpack(w[j]);
+            if (2 * j + 1 < nvalid && z.y == gm) jj = 2 * j + 1;
+            if (2 * j < nvalid && z.x == gm) jj = 2 * j;
+          }
           best_v = gm;
           best_i = (int)(col0 + jj);
         }
       }
-      if (nvalid == 64) {
-        const float mn = fmaxf(m, tree_max<64>(v));
-        const float ml = mn * LOG2E;
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      if (e.exp_flags == 1) {
+        // timing experiment: no statistics
+      } else if (nvalid == 64) {
+        uint32_t mx[16];
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
-          a0 += ex2f(fmaf(v[j], LOG2E, -ml));
-          a1 += ex2f(fmaf(v[j + 1], LOG2E, -ml));
-          a2 += ex2f(fmaf(v[j + 2], LOG2E, -ml));
-          a3 += ex2f(fmaf(v[j + 3], LOG2E, -ml));
-        }
-        if (want_sum) {
-          float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+        for (int j = 0; j < 16; ++j) mx[j] = H::hmax(w[2 * j], w[2 * j + 1]);
 #pragma unroll
-          for (int j = 0; j < 64; j += 4) { z0 += v[j]; z1 += v[j + 1]; z2 += v[j + 2]; z3 += v[j + 3]; }
-          sz += (z0 + z1) + (z2 + z3);
+        for (int wd = 8; wd >= 1; wd >>= 1)
+#pragma unroll
+          for (int j = 0; j < wd; ++j) mx[j] = H::hmax(mx[j], mx[j + wd]);
+        const float2 gm2 = H::unpack(mx[0]);
+        const float mn = fmaxf(m, fmaxf(gm2.x, gm2.y));
+        const float2 l2e2 = make_float2(LOG2E, LOG2E), nml2 = make_float2(-mn * LOG2E, -mn * LOG2E);
+        float2 a0 = make_float2(0.f, 0.f), a1 = a0, z0 = a0, z1 = a0;
+#pragma unroll
+        for (int j = 0; j < 32; j += 2) {
+          const float2 za = H::unpack(w[j]), zb = H::unpack(w[j + 1]);
+          const float2 ta = __ffma2_rn(za, l2e2, nml2), tb = __ffma2_rn(zb, l2e2, nml2);
+          a0 = __fadd2_rn(a0, make_float2(ex2f(ta.x), ex2f(ta.y)));
+          a1 = __fadd2_rn(a1, make_float2(ex2f(tb.x), ex2f(tb.y)));
+          if (want_sum) { z0 = __fadd2_rn(z0, za); z1 = __fadd2_rn(z1, zb); }
         }
-        s = s * ex2f((m - mn) * LOG2E) + ((a0 + a1) + (a2 + a3));  // m = -inf first: ex2(-inf) = 0
+        if (want_sum) sz += (z0.x + z0.y) + (z1.x + z1.y);
+        s = s * ex2f((m - mn) * LOG2E) + ((a0.x + a0.y) + (a1.x + a1.y));  // m = -inf first: ex2(-inf) = 0
         m = mn;
       } else if (nvalid > 0) {
         float cm = -INFINITY;
-        for (int j = 0; j < nvalid; ++j) cm = fmaxf(cm, v[j]);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 z = H::unpack(w[j]);
+          if (2 * j < nvalid) cm = fmaxf(cm, z.x);
+          if (2 * j + 1 < nvalid) cm = fmaxf(cm, z.y);
+        }
         const float mn = fmaxf(m, cm);
-        float a = 0.f, z = 0.f;
-        for (int j = 0; j < nvalid; ++j) { a += ex2f((v[j] - mn) * LOG2E); z += v[j]; }
+        float a = 0.f, zs = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float2 z = H::unpack(w[j]);
+          if (2 * j < nvalid) { a += ex2f((z.x - mn) * LOG2E); zs += z.x; }
+          if (2 * j + 1 < nvalid) { a += ex2f((z.y - mn) * LOG2E); zs += z.y; }
+        }
         s = s * ex2f((m - mn) * LOG2E) + a;
         m = mn;
-        if (want_sum) sz += z;
+        if (want_sum) sz += zs;
       }
-#pragma unroll
-      for (int j = 0; j < 32; ++j) w[j] = pack2<T>(v[2 * j], v[2 * j + 1]);
     } else {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
@@ -602,7 +674,10 @@ __device__ __forceinline__ void run_epilogue(const Problem& P, uint64_t omap, St
   const EpiArgs& e = P.epi;
   if (P.tma_out) {
     switch (e.kind) {
-      case EPI_LOGITS: epi_tma16<T, true>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
+      case EPI_LOGITS:
+        if (e.exp_flags == 2) epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr);
+        else epi_tma16<T, true>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr);
+        break;
       case EPI_STORE: epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
       case EPI_ACCUM:
         if (e.acc) epi_tma32(omap, sg, lane, row0, n0, e.beta != 0, taddr);
