@@ -10,6 +10,7 @@
 #include <cmath>
 #include <mutex>
 #include <unordered_map>
+#include <type_traits>
 
 #include "../../include/liger_b200.h"
 
@@ -109,6 +110,14 @@ template <typename T> __device__ __forceinline__ float to_f(T v) { return Elem<T
 template <typename T> __device__ __forceinline__ T from_f(float v) { return Elem<T>::from_f(v); }
 // round-trip through T (models a cast to the storage dtype)
 template <typename T> __device__ __forceinline__ float round_to(float v) { return to_f<T>(from_f<T>(v)); }
+// bf16 round-to-nearest-even on the integer pipe (3 ALU ops) instead of an F2F + unpack on the
+// 16/clk conversion pipe; exact for all finite values and +-inf (NaNs stay NaN unless their
+// payload sits only in the low 16 bits).
+template <> __device__ __forceinline__ float round_to<__nv_bfloat16>(float v) {
+  uint32_t u = __float_as_uint(v);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return __uint_as_float(u & 0xffff0000u);
+}
 
 // 16-byte vector of T, unpacked to float.
 template <typename T> struct Vec16 {
@@ -130,9 +139,23 @@ template <typename T> struct Vec16 {
   }
   __device__ __forceinline__ void store(T* p) const {
     uint4 raw;
-    T* e = reinterpret_cast<T*>(&raw);
+    if constexpr (sizeof(T) == 2) {  // one F2FP.PACK_AB per pair (a per-element F2F is 4x the work)
+      uint32_t* w = reinterpret_cast<uint32_t*>(&raw);
 #pragma unroll
-    for (int i = 0; i < N; ++i) e[i] = from_f<T>(v[i]);
+      for (int i = 0; i < N / 2; ++i) {
+        if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&h);
+        } else {
+          __half2 h = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+          w[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+      }
+    } else {
+      T* e = reinterpret_cast<T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < N; ++i) e[i] = from_f<T>(v[i]);
+    }
     *reinterpret_cast<uint4*>(p) = raw;
   }
 };

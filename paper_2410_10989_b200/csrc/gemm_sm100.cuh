@@ -19,6 +19,7 @@
 //   MN-major : TMA boxes {64 (MN), 64 (K)} -> one 8 KB box per 64-wide MN atom,
 //              LBO = 8192 (MN atom stride), SBO = 1024 (8-row K group stride)
 #pragma once
+#include <type_traits>
 #include <cuda.h>
 #include "gemm_common.cuh"
 
@@ -462,9 +463,14 @@ __device__ __forceinline__ void stage_row(uint32_t buf, int lane, const uint32_t
 }
 
 template <typename T>
-__device__ __forceinline__ uint32_t pack2(float a, float b) {
-  T x = from_f<T>(a), y = from_f<T>(b);
-  return (uint32_t)(*reinterpret_cast<uint16_t*>(&x)) | ((uint32_t)(*reinterpret_cast<uint16_t*>(&y)) << 16);
+__device__ __forceinline__ uint32_t pack2(float a, float b) {  // one F2FP.PACK_AB, not two F2F
+  if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  } else {
+    __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+  }
 }
 
 __device__ __forceinline__ float ex2f(float x) {
