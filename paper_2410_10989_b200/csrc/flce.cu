@@ -352,15 +352,14 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     le.ignore_index = a->ignore_index; le.partials = parts; le.n_parts = L.nparts; le.tgt_logit = tgt;
     le.M = r; le.N = V; le.want_sum = a->label_smoothing > 0.f ? 1 : 0;
     le.want_argmax = (a->token_correct_rows || a->predicted_tokens) ? 1 : 0;
-    le.exp_flags = getenv("LK_EXP_EPI") ? atoi(getenv("LK_EXP_EPI")) : 0;  // timing experiments only
     {
       ProfScope ps(0, st);
       if (tc) {
         tc::TmaOperand A{xc, H, r, H, 0}, B{a->weight, H, V, H, 0};
         tc::Problem P{};
-        P.M = r; P.N = V; P.K = H; P.epi = le;
-        P.n_fast = getenv("LK_LOGITS_NFAST") ? 1 : 0;  // experiment hook: tile raster order
-        P.pf_dist = getenv("LK_LOGITS_PF") ? atoi(getenv("LK_LOGITS_PF")) : 0;
+        // m-fastest raster: the 8 pairs working on one W tile run together (W read once from HBM;
+        // n-fastest measured 15% slower, profiles/README.md)
+        P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
       } else {
         Operand A{xc, H, 1}, B{a->weight, H, 1};
@@ -428,7 +427,6 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Bs[np] = {a->weight, H, V, H, 1};
         Ps[np] = tc::Problem{};
         Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
-        Ps[np].pf_dist = getenv("LK_DX_PF") ? atoi(getenv("LK_DX_PF")) : 0;
         ++np;
       }
       const int slices = (last && a->grad_w && a->grad_w_slice_events) ? std::min(a->grad_w_slices, 16) : 1;

@@ -36,7 +36,6 @@ struct EpiArgs {
   float* tgt_logit;       // [M] (legacy register epilogue only)
   int want_sum;           // EPI_LOGITS: also accumulate sum of logits (label smoothing)
   int want_argmax;        // EPI_LOGITS: first column of the tile max -> partials[].w (int bits)
-  int exp_flags;          // timing experiments only (LK_EXP_EPI): 1 = skip softmax stats, 2 = plain store
   int64_t M, N;           // valid output extent
 };
 

@@ -45,7 +45,6 @@ struct Problem {
   int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
   int tma_out;          // 1: epilogue writes through smem staging + TMA store (map mc<p>)
-  int pf_dist;          // > 0: L2-prefetch the B box this many k-blocks ahead (HBM-streamed operand)
   EpiArgs epi;
 };
 
@@ -598,9 +597,7 @@ __device__ __forceinline__ void epi_tma16(const EpiArgs& e, uint64_t omap, Stage
           best_i = (int)(col0 + jj);
         }
       }
-      if (e.exp_flags == 1) {
-        // timing experiment: no statistics
-      } else if (nvalid == 64) {
+      if (nvalid == 64) {
         uint32_t mx[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) mx[j] = H::hmax(w[2 * j], w[2 * j + 1]);
@@ -680,10 +677,7 @@ __device__ __forceinline__ void run_epilogue(const Problem& P, uint64_t omap, St
   const EpiArgs& e = P.epi;
   if (P.tma_out) {
     switch (e.kind) {
-      case EPI_LOGITS:
-        if (e.exp_flags == 2) epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr);
-        else epi_tma16<T, true>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr);
-        break;
+      case EPI_LOGITS: epi_tma16<T, true>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
       case EPI_STORE: epi_tma16<T, false>(e, omap, sg, lane, grow, row0, n0, n_blk, taddr); break;
       case EPI_ACCUM:
         if (e.acc) epi_tma32(omap, sg, lane, row0, n0, e.beta != 0, taddr);

@@ -204,7 +204,6 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = pt.m_blk * PBM + (int)rank * HALF;
       const int n0 = pt.n_blk * PBN + (int)rank * HALF;
-      const int pf = p ? args.prob[1].pf_dist : args.prob[0].pf_dist;
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
         if (elect_one()) {
@@ -228,11 +227,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
             tma_2d_cg2(mb, fb, b_dst, n0, k0);
             tma_2d_cg2(mb, fb, b_dst + 8192, n0 + 64, k0);
           }
-          if (pf > 0 && kb + pf < kblocks) {  // the HBM-streamed B operand, pf k-blocks ahead
-            const int kp = (kb + pf) * BK;
-            if (b_mode == 0) tc::tma_prefetch_l2_2d(mb, kp, n0);
-            else if (b_mode == 1) tc::tma_prefetch_l2_3d(mb, 0, kp, n0 >> 6);
-          }
+          // (L2 prefetch of the B operand 8/16/32 k-blocks ahead measured 5-7% slower on the
+          // logits GEMM: the stall was the epilogue, not operand latency; profiles/README.md)
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
