@@ -191,12 +191,20 @@ def run_ours(args):
 
     rank, world, local = env_rank()
     vocab_mode = args.mode == "vocab"
+    # Test hook for the multi-rank code path on a 1-GPU box: LK_BENCH_SHARE_GPU=1 puts every
+    # rank on cuda:0 over gloo (NCCL refuses two ranks per device).  Numbers from it are not
+    # bench values.
+    share = os.environ.get("LK_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1 or vocab_mode:
         torch.cuda.set_device(local)
         if world == 1:  # vocab-parallel at N=1: a one-rank group so the same code path runs
             os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
             os.environ.setdefault("MASTER_PORT", str(29500 + os.getpid() % 1000))
             dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", local))
+        elif share:
+            dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
@@ -393,7 +401,10 @@ def run_ours(args):
                          "full_logits_bytes_avoided": bt * v * 2},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": bt * h * 2 + bt * 8,
-                    "d2h_bytes_per_step": 4, "api": "LigerFusedLinearCrossEntropyLoss + backward()",
+                    "d2h_bytes_per_step": 4,
+                    "api": ("distributed.vocab_parallel_flce" if vocab_mode else
+                            "distributed.token_sharded_flce" if world > 1 else
+                            "LigerFusedLinearCrossEntropyLoss + backward()"),
                     "h2d_pipeline": "each step's X/targets copied from pinned host memory on a side stream, "
                                     "double-buffered one step ahead; loss read back with .item() every step"},
             "gpu_launches": launches * args.steps,
