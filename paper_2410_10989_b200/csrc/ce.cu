@@ -170,7 +170,7 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
   LK_REQUIRE(rows >= 0 && vocab >= 1, LK_SIZE_MISMATCH, "rows must be >= 0 and vocab >= 1");
   LK_REQUIRE(ld >= vocab, LK_NON_CONTIGUOUS, "row stride smaller than vocab");
   LK_REQUIRE(rows == 0 || (logits && targets), LK_INVALID_ARGUMENT, "null logits/targets");
-  LK_REQUIRE(loss_rows != nullptr, LK_INVALID_ARGUMENT, "loss_rows is null");
+  LK_REQUIRE(rows == 0 || loss_rows != nullptr, LK_INVALID_ARGUMENT, "loss_rows is null");
   LK_REQUIRE(reduction >= 0 && reduction <= 2, LK_INVALID_ARGUMENT, "bad reduction");
   LK_REQUIRE(label_smoothing >= 0.f && label_smoothing <= 1.f, LK_INVALID_ARGUMENT,
              "label_smoothing must be in [0, 1]");

@@ -300,7 +300,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   LK_REQUIRE(a->reduction >= 0 && a->reduction <= 2, LK_INVALID_ARGUMENT, "bad reduction");
   LK_REQUIRE(a->label_smoothing >= 0.f && a->label_smoothing <= 1.f, LK_INVALID_ARGUMENT,
              "label_smoothing must be in [0, 1]");
-  LK_REQUIRE(a->loss_rows != nullptr, LK_INVALID_ARGUMENT, "loss_rows is null");
+  LK_REQUIRE(a->bt == 0 || a->loss_rows != nullptr, LK_INVALID_ARGUMENT, "loss_rows is null");
   LK_REQUIRE(BT == 0 || (a->x && a->weight && a->target), LK_INVALID_ARGUMENT, "null input");
   cudaStream_t st = as_stream(a->stream);
   const bool tc = use_tc_path(dt, H, a->x, a->weight, a->force_simt);

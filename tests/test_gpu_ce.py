@@ -226,3 +226,26 @@ def test_ce_token_accuracy_and_predicted_tokens(impl, reduction, cap, monkeypatc
     x2 = z.clone().requires_grad_(True)
     ref(x2, t).sum().backward()
     assert torch.equal(x.grad, x2.grad)
+
+
+def test_ce_int64_offsets_beyond_2_31_elements():
+    """Logits with > 2^31 elements (8448 x 256000 bf16 = 4.3 GB, cfg4's vocabulary): rows past
+    element 2^31 are addressed with 64-bit offsets; they match the oracle."""
+    rows, v = 8448, 256000
+    assert rows * v > 2**31
+    g = torch.Generator(device="cuda").manual_seed(9)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    t[-3] = -100
+    x = torch.empty(rows, v, dtype=torch.bfloat16, device="cuda")
+    x.normal_(generator=g)
+    sel = torch.tensor([0, rows // 2, rows - 4, rows - 3, rows - 2, rows - 1], device="cuda")
+    ref_in = x[sel].double().cpu().numpy()
+    x.requires_grad_(True)
+    loss = lk.LigerCrossEntropyLoss(reduction="none")(x, t)
+    loss.sum().backward()
+    _, rrows, _, rgrad = liger_ref.ce(ref_in, t[sel].cpu().numpy(), reduction="none")
+    ok, err = rel_close(loss.detach()[sel].float().cpu().numpy(), rrows, 2e-2)
+    assert ok, err
+    ok, err = rel_close(x.grad[sel].float().cpu().numpy(), rgrad, 2e-2)
+    assert ok, err
+    assert torch.all(x.grad[rows - 3] == 0) and loss[rows - 3].item() == 0.0

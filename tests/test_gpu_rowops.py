@@ -284,3 +284,40 @@ def test_benchrecord_gpu_rows(tmp_path):
     back = br.read_records(p)
     assert [r.op for r in back] == list(br.OPS)
     assert all(r.variant == "fused" and r.median_s > 0 and r.q20_s <= r.q80_s for r in back)
+
+
+def test_empty_inputs_all_ops():
+    """Zero rows / tokens through every op (SURVEY §8(c) edge cases): no launch errors, empty
+    outputs, zero parameter gradients."""
+    dev = "cuda"
+    bf = torch.bfloat16
+    # RMSNorm / LayerNorm
+    x = torch.empty(0, 64, dtype=bf, device=dev, requires_grad=True)
+    w = torch.ones(64, dtype=bf, device=dev, requires_grad=True)
+    b = torch.zeros(64, dtype=bf, device=dev, requires_grad=True)
+    y = lk.liger_rms_norm(x, w, 1e-6, 0.0, "llama", False)
+    y.backward(torch.empty_like(y))
+    assert y.shape == (0, 64) and torch.all(w.grad == 0)
+    w.grad = None
+    y = lk.liger_layer_norm(x, w, b, 1e-6)
+    y.backward(torch.empty_like(y))
+    assert y.shape == (0, 64) and torch.all(w.grad == 0) and torch.all(b.grad == 0)
+    # SwiGLU
+    a = torch.empty(0, 128, dtype=bf, device=dev, requires_grad=True)
+    c = lk.LigerSiLUMulFunction.apply(a, a.detach().clone().requires_grad_(True))
+    assert c.shape == (0, 128)
+    # RoPE with zero tokens
+    q = torch.empty(1, 2, 0, 8, dtype=bf, device=dev)
+    cos = torch.empty(1, 0, 8, dtype=bf, device=dev)
+    qo, ko = lk.liger_rotary_pos_emb(q, q.clone(), cos, cos)
+    assert qo.shape == (1, 2, 0, 8)
+    # CE / FLCE with zero tokens
+    z = torch.empty(0, 100, dtype=bf, device=dev, requires_grad=True)
+    t = torch.empty(0, dtype=torch.long, device=dev)
+    loss = lk.LigerCrossEntropyLoss(reduction="sum")(z, t)
+    assert loss.item() == 0.0
+    xw = torch.empty(0, 64, dtype=bf, device=dev, requires_grad=True)
+    W = torch.randn(100, 64, dtype=bf, device=dev, requires_grad=True)
+    loss = lk.LigerFusedLinearCrossEntropyLoss(reduction="sum")(W, xw, t)
+    loss.backward()
+    assert loss.item() == 0.0 and torch.all(W.grad == 0)
