@@ -103,12 +103,14 @@ int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* targets, int64
                          void* workspace, size_t workspace_bytes, void* stream);
 /* Same, plus Liger's return_token_accuracy / return_predicted_tokens outputs: per row
  * 1.0 if argmax == target else 0.0 (correct_rows) and the argmax (pred_rows); ignored rows
- * -> 0.0 / -1; either may be NULL (LK/ops/cross_entropy.py:131-163, 294-299). */
+ * -> 0.0 / -1; either may be NULL (LK/ops/cross_entropy.py:131-163, 294-299).  class_weight
+ * ([vocab] fp32 or NULL) is Liger's `weight` (LK/ops/cross_entropy.py:122-124, 220-239,
+ * 278-288); with label_smoothing > 0 it returns LK_UNSUPPORTED. */
 int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* targets, int64_t rows, int64_t vocab,
                             int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
                             float softcap, int reduction, int compute_grad, float* loss_rows, float* loss_sum,
                             float* z_loss_rows, float* z_loss_sum, float* correct_rows, int64_t* pred_rows,
-                            void* workspace, size_t workspace_bytes, void* stream);
+                            const float* class_weight, void* workspace, size_t workspace_bytes, void* stream);
 
 /* Count of targets != ignore_index and the out-of-range flag, on device.
  * out[0] = n_non_ignore (as int64), out[1] = number of out-of-range targets. */
@@ -187,6 +189,11 @@ typedef struct {
    * all-reduce slice s while later slices are still being computed. */
   int grad_w_slices;
   void* const* grad_w_slice_events;
+  /* Liger use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139, 187-206): each
+   * row's loss, z-loss and gradient scaled by its detached target probability. */
+  int use_token_scaling;
+  /* Liger ce_weight: [vocab] fp32 class weights or NULL (no label smoothing with weights). */
+  const float* ce_weight;
 } lk_flce_args;
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };

@@ -21,8 +21,13 @@ import numpy as np
 
 
 def ce(logits, target, ignore_index=-100, label_smoothing=0.0, lse_square_scale=0.0, softcap=None,
-       reduction="mean"):
-    """Returns (loss, loss_rows, z_loss, grad) in float64. loss is a scalar unless reduction='none'."""
+       reduction="mean", token_scaling=False, weight=None):
+    """Returns (loss, loss_rows, z_loss, grad) in float64. loss is a scalar unless reduction='none'.
+
+    token_scaling: Liger FLCE use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139,
+    187-206): each row's loss, z-loss and gradient times its detached target probability.
+    weight: class weights without label smoothing (LK/ops/cross_entropy.py:122-124, 220-239,
+    278-288): loss_i = w[y_i](lse - z_y), MEAN over sum_valid w[y_i]; z-loss still over the count."""
     z = np.asarray(logits, dtype=np.float64)
     y = np.asarray(target, dtype=np.int64)
     rows, vocab = z.shape
@@ -46,6 +51,28 @@ def ce(logits, target, ignore_index=-100, label_smoothing=0.0, lse_square_scale=
         loss = loss * (1.0 - label_smoothing) + (label_smoothing * lse - eps * zc.sum(axis=1))
     zl = lse_square_scale * lse * lse
     scale = 1.0 / max(n, 1) if reduction == "mean" else 1.0
+    ts = np.exp(zy - lse) if token_scaling else np.ones(rows)  # per row, detached
+    if weight is not None:
+        assert label_smoothing == 0.0
+        wv = np.asarray(weight, dtype=np.float64)
+        wy = np.where(valid, wv[ysafe], 0.0)
+        swn = wy.sum() if reduction == "mean" else 1.0
+        s1 = ts / (swn if swn != 0 else 1.0)
+        s2 = ts * scale
+        loss = wy * (lse - zy) * s1 + zl * s2
+        zl = zl * s2
+        loss = np.where(valid, loss, 0.0)
+        zl = np.where(valid, zl, 0.0)
+        p = e / s
+        g = p * (wy * s1 + 2.0 * lse_square_scale * lse * s2)[:, None]
+        g[np.arange(rows), ysafe] -= np.where(valid, wy * s1, 0.0)
+        if t is not None:
+            g *= 1.0 - t * t
+        g[~valid] = 0.0
+        if reduction == "none":
+            return loss, loss, zl, g
+        return float(loss.sum()), loss, float(zl.sum()), g
+    scale = scale * ts
     loss = (loss + zl) * scale
     zl = zl * scale
     loss = np.where(valid, loss, 0.0)
@@ -53,7 +80,7 @@ def ce(logits, target, ignore_index=-100, label_smoothing=0.0, lse_square_scale=
     p = e / s
     g = p * (1.0 + 2.0 * lse_square_scale * lse[:, None]) - eps
     g[np.arange(rows), ysafe] -= np.where(valid, 1.0 - label_smoothing, 0.0)
-    g *= scale
+    g *= scale[:, None] if np.ndim(scale) else scale
     if t is not None:
         g *= 1.0 - t * t
     g[~valid] = 0.0

@@ -67,6 +67,8 @@ class FlceArgs(C.Structure):
         ("predicted_tokens", c_void),
         ("grad_w_slices", c_int),
         ("grad_w_slice_events", c_void),
+        ("use_token_scaling", c_int),
+        ("ce_weight", c_void),
     ]
 
 
@@ -80,8 +82,8 @@ SIGNATURES: dict[str, tuple] = {
     "lk_launch_count": (c_i64, []),
     "lk_cross_entropy_workspace_bytes": (c_size, [c_i64]),
     "lk_cross_entropy_fwd_ex": (c_int, [c_void, c_i64, c_void, c_i64, c_i64, c_int, c_i64, c_float, c_float, c_float,
-                                        c_int, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_size,
-                                        c_void]),
+                                        c_int, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_void,
+                                        c_size, c_void]),
     "lk_flce_workspace_bytes_ex": (c_size, [c_i64, c_i64, c_i64, c_int, c_i64, c_int, c_int]),
     "lk_cross_entropy_fwd": (
         c_int,

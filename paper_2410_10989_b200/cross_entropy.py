@@ -62,8 +62,6 @@ def cross_entropy_forward(
 ):
     """Loss (+ optional z-loss) with d(loss)/d(input) left in `_input` (mirrors LK/ops/cross_entropy.py:302-407)."""
     _validate(label_smoothing, reduction, softcap)
-    if weight is not None:
-        raise errors.UnsupportedOption("class weights (ce_weight) are not implemented in the B200 build")
     require_cuda(_input, target)
     if _input.dim() != 2:
         raise errors.ShapeMismatch(f"input must be (BT, V), got {tuple(_input.shape)}")
@@ -79,6 +77,13 @@ def cross_entropy_forward(
     loss_sum = torch.empty((), dtype=torch.float32, device=dev)
     z_rows = torch.empty(bt, dtype=torch.float32, device=dev) if return_z_loss else None
     z_sum = torch.empty((), dtype=torch.float32, device=dev) if return_z_loss else None
+    cw = None
+    if weight is not None:  # Liger class weights (LK/ops/cross_entropy.py:369-378)
+        if weight.shape != (v,) or not torch.is_floating_point(weight):
+            raise errors.ShapeMismatch(f"weight must be a floating tensor of size V={v}, got {tuple(weight.shape)}")
+        if label_smoothing > 0:
+            raise errors.UnsupportedOption("class weights with label_smoothing are not implemented in the B200 build")
+        cw = weight.detach().to(device=dev, dtype=torch.float32).contiguous()
     correct = torch.empty(bt, dtype=torch.float32, device=dev) if return_token_accuracy else None
     pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None
     L = lib()
@@ -88,7 +93,7 @@ def cross_entropy_forward(
             _input.data_ptr(), _input.stride(0) if bt > 0 else v, ptr(t), bt, v, dtype_code(_input),
             int(ignore_index), float(label_smoothing), float(lse_square_scale),
             float(softcap) if softcap is not None else 0.0, _capi.REDUCTIONS[reduction], int(bool(grad)),
-            loss_rows.data_ptr(), loss_sum.data_ptr(), ptr(z_rows), ptr(z_sum), ptr(correct), ptr(pred),
+            loss_rows.data_ptr(), loss_sum.data_ptr(), ptr(z_rows), ptr(z_sum), ptr(correct), ptr(pred), ptr(cw),
             ws.data_ptr(), ws.numel(), stream_of(_input),
         )
     )

@@ -19,6 +19,31 @@ __global__ void reduce_sum_kernel(const float* __restrict__ v, int64_t n, float*
   if (threadIdx.x == 0) *out = (float)sh[0];
 }
 
+// sum_{i valid} w[y_i] in a fixed order (one CTA, double accumulation): the MEAN denominator with
+// class weights (LK/ops/cross_entropy.py:369-375, sum_non_ignore_weight).
+__global__ void weight_sum_kernel(const int64_t* __restrict__ t, int64_t rows, int64_t ignore_index,
+                                  const float* __restrict__ w, float* out) {
+  __shared__ double sh[1024];
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
+    const int64_t y = t[i];
+    if (y != ignore_index) acc += (double)w[y];
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int k = blockDim.x / 2; k > 0; k >>= 1) {
+    if ((int)threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = (float)sh[0];
+}
+
+int launch_weight_sum(const int64_t* t, int64_t rows, int64_t ignore_index, const float* w, float* out,
+                      cudaStream_t st) {
+  weight_sum_kernel<<<1, 1024, 0, st>>>(t, rows, ignore_index, w, out);
+  return check_launch("weight_sum_kernel");
+}
+
 __global__ void count_targets_kernel(const int64_t* __restrict__ t, int64_t rows, int64_t vocab,
                                      int64_t ignore_index, unsigned long long* out) {
   unsigned long long valid = 0, bad = 0;
@@ -158,15 +183,16 @@ extern "C" int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* tar
                                     void* workspace, size_t workspace_bytes, void* stream) {
   return lk_cross_entropy_fwd_ex(logits, ld, targets, rows, vocab, dtype, ignore_index, label_smoothing,
                                  lse_square_scale, softcap, reduction, compute_grad, loss_rows, loss_sum,
-                                 z_loss_rows, z_loss_sum, nullptr, nullptr, workspace, workspace_bytes, stream);
+                                 z_loss_rows, z_loss_sum, nullptr, nullptr, nullptr, workspace, workspace_bytes,
+                                 stream);
 }
 
 extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* targets, int64_t rows,
                                        int64_t vocab, int dtype, int64_t ignore_index, float label_smoothing,
                                        float lse_square_scale, float softcap, int reduction, int compute_grad,
                                        float* loss_rows, float* loss_sum, float* z_loss_rows, float* z_loss_sum,
-                                       float* correct_rows, int64_t* pred_rows, void* workspace,
-                                       size_t workspace_bytes, void* stream) {
+                                       float* correct_rows, int64_t* pred_rows, const float* class_weight,
+                                       void* workspace, size_t workspace_bytes, void* stream) {
   LK_REQUIRE(rows >= 0 && vocab >= 1, LK_SIZE_MISMATCH, "rows must be >= 0 and vocab >= 1");
   LK_REQUIRE(ld >= vocab, LK_NON_CONTIGUOUS, "row stride smaller than vocab");
   LK_REQUIRE(rows == 0 || (logits && targets), LK_INVALID_ARGUMENT, "null logits/targets");
@@ -176,10 +202,17 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
              "label_smoothing must be in [0, 1]");
   LK_REQUIRE(workspace && workspace_bytes >= lk_cross_entropy_workspace_bytes(rows),
              LK_INVALID_ARGUMENT, "workspace too small");
+  LK_REQUIRE(!class_weight || label_smoothing == 0.f, LK_UNSUPPORTED,
+             "class weights with label smoothing are not implemented in the B200 build");
   cudaStream_t st = as_stream(stream);
   int64_t* counts = static_cast<int64_t*>(workspace);
+  float* wsum = reinterpret_cast<float*>(static_cast<char*>(workspace) + 32);
   int rc = launch_count_targets(targets, rows, vocab, ignore_index, counts, st);
   if (rc) return rc;
+  if (class_weight) {
+    rc = launch_weight_sum(targets, rows, ignore_index, class_weight, wsum, st);
+    if (rc) return rc;
+  }
   CeRowArgs a{};
   a.x = logits; a.ld = ld; a.target = targets; a.rows = rows; a.n_cols = vocab;
   a.vocab_total = vocab; a.col_offset = 0; a.ignore_index = ignore_index;
@@ -187,6 +220,7 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
   a.input_capped = 0; a.reduction = reduction; a.compute_grad = compute_grad; a.n_valid = counts;
   a.loss_rows = loss_rows; a.z_loss_rows = z_loss_rows;
   a.correct_rows = correct_rows; a.pred_rows = pred_rows;
+  a.class_weight = class_weight; a.sum_valid_weight = class_weight ? wsum : nullptr;
   // LK_CE_IMPL = ring (default) | cluster | block (one CTA per row, ce_rows_kernel)
   const char* impl_env = getenv("LK_CE_IMPL");  // read per call so tests can switch paths
   const char impl = impl_env ? impl_env[0] : 'r';

@@ -45,7 +45,58 @@ struct CeRowArgs {
   // partials, the argmax comes from partials[].w (int bits) written by the logits epilogue.
   float* correct_rows;     // [rows] 1.0 if argmax == target else 0.0, or null
   int64_t* pred_rows;      // [rows] argmax (global column), -1 for ignored rows, or null
+  // Liger FLCE use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139, 187-206):
+  // loss, z-loss and gradient of a row scaled by its detached target probability
+  // p_t = softmax(z)[t], rounded to the logits dtype as torch.softmax on the logits returns it.
+  int token_scaling;
+  // Liger class weights (ce_weight; LK/ops/cross_entropy.py:122-124, 220-239, 278-288), without
+  // label smoothing: loss_i = w[y_i] (lse - z_y) / sum_valid(w[y]) (MEAN), gradient likewise.
+  const float* class_weight;      // [vocab_total] fp32 or null
+  const float* sum_valid_weight;  // device scalar sum_{valid i} w[y_i] (MEAN with class_weight)
 };
+
+// Per-row loss and gradient coefficients: grad = p * pc + ceps - [col == y] * chit (then the
+// softcap chain rule), p = softmax(z)[col].  Reduction, token scaling and class weights fold in
+// here so the streaming passes stay option-free.
+struct RowCoef {
+  float loss, zl, pc, ceps, chit;
+};
+template <typename T>
+__device__ __forceinline__ RowCoef ce_row_coefs(const CeRowArgs& a, float lse, float zy, float sz, int64_t y) {
+  const float lsm = a.label_smoothing, eps = lsm / (float)a.vocab_total, lss = a.lse_square_scale;
+  const bool mean = a.reduction == LK_REDUCTION_MEAN;
+  float inv_n = 1.f;
+  if (mean) {
+    const int64_t nv = *a.n_valid;
+    inv_n = 1.f / (float)(nv > 0 ? nv : 1);
+  }
+  const float ts = a.token_scaling ? round_to<T>(__expf(zy - lse)) : 1.f;
+  RowCoef c;
+  if (a.class_weight) {
+    const float wy = a.class_weight[y];
+    float s1 = ts;
+    if (mean) {
+      const float swn = *a.sum_valid_weight;
+      s1 = ts / (swn != 0.f ? swn : 1.f);
+    }
+    const float s2 = inv_n * ts;
+    c.zl = lss * lse * lse * s2;
+    c.loss = wy * (lse - zy) * s1 + c.zl;
+    c.pc = wy * s1 + 2.f * lss * lse * s2;
+    c.ceps = 0.f;
+    c.chit = wy * s1;
+  } else {
+    const float rs = inv_n * ts;
+    float loss = lse - zy;
+    if (lsm > 0.f) loss = loss * (1.f - lsm) + (-eps * sz + lsm * lse);
+    c.zl = lss * lse * lse * rs;
+    c.loss = loss * rs + c.zl;
+    c.pc = rs * (1.f + 2.f * lss * lse);
+    c.ceps = -eps * rs;
+    c.chit = (1.f - lsm) * rs;
+  }
+  return c;
+}
 
 // (value, index) argmax merge: larger value wins, ties keep the smaller index.
 __device__ __forceinline__ void am_merge(float& v, int& i, float v2, int i2) {
@@ -179,34 +230,20 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
   }
 
   const float lse = m + logf(s);
-  const float V = (float)a.vocab_total;
-  const float lsm = a.label_smoothing;
-  const float eps = lsm / V;
-  float scale = 1.f;
-  if (a.reduction == LK_REDUCTION_MEAN) {
-    int64_t nv = *a.n_valid;
-    scale = 1.f / (float)(nv > 0 ? nv : 1);
-  }
+  const RowCoef rc = ce_row_coefs<T>(a, lse, zy, sz, y);
   if (tid == 0) {
     if (want_arg) {  // global column; the finalize of a vocab shard is not supported (row_stats path)
       const int64_t am = a.row_stats ? -1 : (int64_t)bcast_arg + a.col_offset;
       if (a.pred_rows) a.pred_rows[row] = am;
       if (a.correct_rows) a.correct_rows[row] = am == y ? 1.f : 0.f;
     }
-    // LK/ops/cross_entropy.py:259-289
-    float loss = lse - zy;
-    if (lsm > 0.f) loss = loss * (1.f - lsm) + (-eps * sz + lsm * lse);
-    float zl = a.lse_square_scale * lse * lse;
-    loss = (loss + zl) * scale;
-    if (a.loss_rows) a.loss_rows[row] = loss;
-    if (a.z_loss_rows) a.z_loss_rows[row] = zl * scale;
+    if (a.loss_rows) a.loss_rows[row] = rc.loss;  // LK/ops/cross_entropy.py:259-289
+    if (a.z_loss_rows) a.z_loss_rows[row] = rc.zl;
   }
   if (!a.compute_grad) return;
 
   // pass 2: d(loss)/d(z) (LK/ops/cross_entropy.py:181-246)
-  const float inv_s = 1.f / s;
-  const float zfac = 1.f + 2.f * a.lse_square_scale * lse;
-  const float hit = 1.f - lsm;
+  const float pc = rc.pc / s;
   auto grad = [&](float z, int64_t col) -> float {
     float t = 0.f;
     if (has_cap) {
@@ -217,9 +254,8 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
         z = cap * t;
       }
     }
-    float g = __expf(z - m) * inv_s * zfac - eps;
-    if (col == yl) g -= hit;
-    g *= scale;
+    float g = __expf(z - m) * pc + rc.ceps;
+    if (col == yl) g -= rc.chit;
     if (has_cap) g *= (1.f - t * t);
     return g;
   };
@@ -252,6 +288,9 @@ int launch_ce_cluster(const CeRowArgs& a, int dtype, cudaStream_t st);
 int launch_count_targets(const int64_t* t, int64_t rows, int64_t vocab, int64_t ignore_index,
                          int64_t* out, cudaStream_t st);
 int launch_reduce_sum(const float* v, int64_t n, float* out, cudaStream_t st);
+// sum over non-ignored rows of class_weight[target] (MEAN denominator with class weights)
+int launch_weight_sum(const int64_t* t, int64_t rows, int64_t ignore_index, const float* w, float* out,
+                      cudaStream_t st);
 // Vocab-parallel stage 1: per-row local (max, sumexp, sum_logits, target_logit).
 int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols, int dtype,
                         const int64_t* target, int64_t col_offset, int64_t ignore_index,

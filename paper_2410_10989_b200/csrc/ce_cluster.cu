@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(BLOCK) ce_cluster_kernel(CeRowArgs a, int64_t 
 
 // Returns LK_UNSUPPORTED when the shape cannot take the cluster path (caller falls back).
 int launch_ce_cluster(const CeRowArgs& a, int dtype, cudaStream_t st) {
-  if (a.rows <= 0 || a.partials || a.row_stats || a.correct_rows || a.pred_rows) return LK_UNSUPPORTED;
+  if (a.rows <= 0 || a.partials || a.row_stats || a.correct_rows || a.pred_rows || a.class_weight ||
+      a.token_scaling)
+    return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   const int64_t nv = 16 / esz;
   if (a.n_cols % nv || a.ld % nv || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;

@@ -107,14 +107,6 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   }
 
   const float cap = a.softcap, inv_cap = CAP ? 1.f / a.softcap : 0.f;
-  const float lsm = LS ? a.label_smoothing : 0.f;
-  const float eps = lsm / (float)a.vocab_total;
-  const float hit = 1.f - lsm;
-  float scale = 1.f;
-  if (a.reduction == LK_REDUCTION_MEAN) {
-    const int64_t nv = *a.n_valid;
-    scale = 1.f / (float)(nv > 0 ? nv : 1);
-  }
   const int tid = threadIdx.x;
   const float2 l2e2 = make_float2(L2E, L2E);
   const bool want_arg = a.correct_rows || a.pred_rows;
@@ -272,21 +264,19 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     }
     par ^= 1;
     const float lse = m + logf(se);
+    // reduction (MEAN), token scaling and class weights folded into per-row coefficients
+    const RowCoef rcf = ce_row_coefs<T>(a, lse, zy, sz, y);
     if (tid == 0) {  // LK/ops/cross_entropy.py:259-289
-      float loss = lse - zy;
-      if (LS) loss = loss * (1.f - lsm) + (-eps * sz + lsm * lse);
-      const float zl = a.lse_square_scale * lse * lse;
-      loss = (loss + zl) * scale;
-      if (a.loss_rows) a.loss_rows[row] = loss;
-      if (a.z_loss_rows) a.z_loss_rows[row] = zl * scale;
+      if (a.loss_rows) a.loss_rows[row] = rcf.loss;
+      if (a.z_loss_rows) a.z_loss_rows[row] = rcf.zl;
     }
     if (!a.compute_grad) continue;
     // ---- pass 2: gradient in place (LK/ops/cross_entropy.py:181-246) ----
-    const float coef = scale * (1.f + 2.f * a.lse_square_scale * lse) / se;
+    const float coef = rcf.pc / se;
     const float2 nmb = make_float2(-m * L2E, -m * L2E);
     const float2 coef2 = make_float2(coef, coef);
-    const float2 neps2 = make_float2(-eps * scale, -eps * scale);
-    const float hit_s = hit * scale;
+    const float2 neps2 = make_float2(rcf.ceps, rcf.ceps);
+    const float hit_s = rcf.chit;
     for (int64_t j = 0; j < npc; ++j, cur.next()) {
       const int s = cur.s;
       ring::wait(&full[s], cur.phase);

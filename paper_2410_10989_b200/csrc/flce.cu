@@ -254,7 +254,7 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   L.need_bias_acc = has_bias_grad;
   size_t off = 0;
   auto take = [&](size_t bytes) { off = align_up(off, 1024); size_t o = off; off += bytes; return o; };
-  L.off_counts = take(2 * sizeof(int64_t));
+  L.off_counts = take(4 * sizeof(int64_t));  // n_valid, n_out_of_range, class-weight sum
   L.off_sched = take((size_t)(2 * L.nchunks + 2 + 16) * sizeof(int));  // + per-slice counters
   L.off_z = take((size_t)L.C * L.ldz * elt_size(dtype));
   L.off_parts = take(tc ? (size_t)L.C * L.nparts * sizeof(float4) : 0);
@@ -330,6 +330,13 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   if (rc) return rc;
   if (a->target_stats)
     LK_CUDA(cudaMemcpyAsync(a->target_stats, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  LK_REQUIRE(!a->ce_weight || a->label_smoothing == 0.f, LK_UNSUPPORTED,
+             "ce_weight with label smoothing is not implemented in the B200 build");
+  LK_REQUIRE(!a->ce_weight || !a->mean_count, LK_UNSUPPORTED, "ce_weight in the token-sharded mode");
+  if (a->ce_weight && BT > 0) {  // MEAN denominator: sum of the valid targets' weights (after counts)
+    rc = launch_weight_sum(a->target, BT, a->ignore_index, a->ce_weight, reinterpret_cast<float*>(counts + 2), st);
+    if (rc) return rc;
+  }
   if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
   if (BT == 0) {
     if (a->loss_sum) LK_CUDA(cudaMemsetAsync(a->loss_sum, 0, sizeof(float), st));
@@ -377,6 +384,9 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     ce.n_valid = a->mean_count ? a->mean_count : counts;
     ce.loss_rows = a->loss_rows + lo; ce.z_loss_rows = a->z_loss_rows ? a->z_loss_rows + lo : nullptr;
     ce.correct_rows = a->token_correct_rows ? a->token_correct_rows + lo : nullptr;
+    ce.token_scaling = a->use_token_scaling;
+    ce.class_weight = a->ce_weight;
+    ce.sum_valid_weight = a->ce_weight ? reinterpret_cast<const float*>(counts + 2) : nullptr;
     ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {

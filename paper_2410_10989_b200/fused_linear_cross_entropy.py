@@ -83,10 +83,6 @@ def fused_linear_cross_entropy_forward(
     splits the last chunk's grad_w GEMM into that many vocab-row slices and records event s
     when slice s of grad_w is final (overlap of the token-sharded dW all-reduce).
     """
-    if ce_weight is not None:
-        raise errors.UnsupportedOption("ce_weight is not implemented in the B200 build")
-    if use_token_scaling:
-        raise errors.UnsupportedOption("use_token_scaling is not implemented in the B200 build")
     if not (0.0 <= label_smoothing <= 1.0):
         raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
     if reduction not in _capi.REDUCTIONS:
@@ -124,6 +120,13 @@ def fused_linear_cross_entropy_forward(
     stats = torch.empty(2, dtype=torch.int64, device=dev)
     correct = torch.empty(bt, dtype=torch.float32, device=dev) if return_token_accuracy else None
     pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None
+    cw = None
+    if ce_weight is not None:  # Liger class weights (LK/ops/fused_linear_cross_entropy.py:86-98)
+        if ce_weight.shape != (v,) or not torch.is_floating_point(ce_weight):
+            raise errors.ShapeMismatch(f"ce_weight must be a floating tensor of size V={v}")
+        if label_smoothing > 0:
+            raise errors.UnsupportedOption("ce_weight with label_smoothing is not implemented in the B200 build")
+        cw = ce_weight.detach().to(device=dev, dtype=torch.float32).contiguous()
     L = lib()
     dt = dtype_code(x)
     cr = int(chunk_rows or 0)
@@ -147,7 +150,8 @@ def fused_linear_cross_entropy_forward(
         grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=ptr(ws), workspace_bytes=ws.numel(),
         stream=stream_of(x), force_simt=int(bool(force_simt)),
         mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
-        token_correct_rows=ptr(correct), predicted_tokens=ptr(pred),
+        token_correct_rows=ptr(correct), predicted_tokens=ptr(pred), use_token_scaling=int(bool(use_token_scaling)),
+        ce_weight=ptr(cw),
     )
     ev_arr = None
     if grad_w_slice_events:

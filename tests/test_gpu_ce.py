@@ -249,3 +249,29 @@ def test_ce_int64_offsets_beyond_2_31_elements():
     ok, err = rel_close(x.grad[sel].float().cpu().numpy(), rgrad, 2e-2)
     assert ok, err
     assert torch.all(x.grad[rows - 3] == 0) and loss[rows - 3].item() == 0.0
+
+
+@pytest.mark.parametrize("impl", ["ring", "block"])
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+@pytest.mark.parametrize("kw", [dict(), dict(softcap=20.0, lse_square_scale=1e-4)])
+def test_ce_class_weights(impl, reduction, kw, monkeypatch):
+    """Liger `weight` (class weights, LK/ops/cross_entropy.py:122-124, 220-239, 278-288) vs the
+    float64 oracle (itself pinned to torch F.cross_entropy(weight=...))."""
+    monkeypatch.setenv("LK_CE_IMPL", impl)
+    rows, v = 300, 4096
+    g = torch.Generator(device="cuda").manual_seed(13)
+    z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    t[::6] = -100
+    w = torch.rand(v, device="cuda", generator=g) + 0.1
+    x = z.clone().requires_grad_(True)
+    loss = lk.LigerCrossEntropyLoss(weight=w, reduction=reduction, **kw)(x, t)
+    loss.sum().backward()
+    rl, _, _, rg = liger_ref.ce(z.double().cpu().numpy(), t.cpu().numpy(), weight=w.double().cpu().numpy(),
+                                reduction=reduction, **kw)
+    ok, err = rel_close(loss.detach().float().cpu().numpy(), rl, 2e-2)
+    assert ok, err
+    ok, err = rel_close(x.grad.float().cpu().numpy(), rg, 2e-2)
+    assert ok, err
+    with pytest.raises(errors.UnsupportedOption):
+        lk.LigerCrossEntropyLoss(weight=w, label_smoothing=0.1)(z.clone().requires_grad_(True), t)

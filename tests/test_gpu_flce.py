@@ -323,3 +323,44 @@ def test_grad_w_slices_with_events_bitwise(slices, accum_dtype):
     torch.cuda.synchronize()
     assert a[0].item() == b_loss.item()
     assert torch.equal(a[2], b_gx) and torch.equal(a[3], b_gw)
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0, lse_square_scale=1e-4)])
+def test_flce_use_token_scaling(simt, kw):
+    """Liger use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139, 187-206): loss and
+    gradients of each row scaled by its detached target probability, vs the float64 oracle."""
+    xb, wb, tb, x, w, t = bf16_problem(600, 128, 3000, seed=41, wscale=4.0)
+    if simt:
+        xb, wb = xb.float(), wb.float()
+        x, w = xb.double().cpu().numpy(), wb.double().cpu().numpy()
+    loss, _, _, _, gx, gw, _ = flce_fwd(xb, wb, tb, compute_grad_input=True, compute_grad_weight=True,
+                                        use_token_scaling=True, force_simt=simt, chunk_rows=256, **kw)
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, token_scaling=True, **kw)
+    tol = 1e-4 if simt else 2e-2
+    assert rel_close(loss.item(), ref_loss, tol)[0], (loss.item(), ref_loss)
+    ok, err = rel_close(gx.float().cpu().numpy(), rgx, tol)
+    assert ok, err
+    ok, err = rel_close(gw.float().cpu().numpy(), rgw, tol)
+    assert ok, err
+
+
+@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("reduction", ["mean", "sum"])
+def test_flce_ce_weight(simt, reduction):
+    """Liger ce_weight on the FLCE head vs the float64 oracle (no label smoothing)."""
+    xb, wb, tb, x, w, t = bf16_problem(700, 128, 3000, seed=43, wscale=3.0)
+    if simt:
+        xb, wb = xb.float(), wb.float()
+        x, w = xb.double().cpu().numpy(), wb.double().cpu().numpy()
+    cw = torch.rand(3000, device="cuda") + 0.2
+    loss, _, _, _, gx, gw, _ = flce_fwd(xb, wb, tb, cw, compute_grad_input=True, compute_grad_weight=True,
+                                        reduction=reduction, force_simt=simt, chunk_rows=256, lse_square_scale=1e-4)
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, weight=cw.double().cpu().numpy(), reduction=reduction,
+                                                 lse_square_scale=1e-4)
+    tol = 1e-4 if simt else 2e-2
+    assert rel_close(loss.item(), ref_loss, tol)[0], (loss.item(), ref_loss)
+    ok, err = rel_close(gx.float().cpu().numpy(), rgx, tol)
+    assert ok, err
+    ok, err = rel_close(gw.float().cpu().numpy(), rgw, tol)
+    assert ok, err

@@ -244,3 +244,42 @@ def test_target_out_of_range_raises():
         rp.cross_entropy_(np.zeros((2, 4)), [0, 4])
     with pytest.raises(rp.TargetOutOfRange):
         rp.cross_entropy_(np.zeros((1, 4)), [-100])
+
+
+def test_liger_ref_token_scaling_matches_liger_formula():
+    """use_token_scaling restated per LK/ops/fused_linear_cross_entropy.py:109-139, 187-206 with
+    torch-CPU float64: loss_i * p_t (detached), gradient rows scaled alike."""
+    import torch
+
+    rng = np.random.default_rng(3)
+    z = rng.normal(size=(12, 30)) * 2
+    t = rng.integers(0, 30, 12)
+    t[4] = -100
+    loss, rows, _, g = liger_ref.ce(z, t, reduction="sum", token_scaling=True, label_smoothing=0.1)
+    zt = torch.tensor(z, requires_grad=True)
+    tt = torch.tensor(t)
+    per = torch.nn.functional.cross_entropy(zt, tt, reduction="none", ignore_index=-100, label_smoothing=0.1)
+    p = torch.softmax(zt.detach(), -1).gather(1, tt.clamp(min=0)[:, None])[:, 0] * (tt != -100)
+    (per * p).sum().backward()
+    np.testing.assert_allclose(loss, float((per * p).sum()), rtol=1e-12)
+    np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
+def test_liger_ref_class_weights_match_torch(reduction):
+    """Class weights (no smoothing) restated per LK/ops/cross_entropy.py:122-124, 220-239,
+    278-288 equal torch-CPU float64 F.cross_entropy(weight=...) (+ z-loss over the count)."""
+    import torch
+
+    rng = np.random.default_rng(4)
+    z = rng.normal(size=(16, 25)) * 2
+    t = rng.integers(0, 25, 16)
+    t[[3, 9]] = -100
+    w = rng.random(25) + 0.2
+    loss, _, _, g = liger_ref.ce(z, t, weight=w, reduction=reduction)
+    zt = torch.tensor(z, requires_grad=True)
+    ref = torch.nn.functional.cross_entropy(zt, torch.tensor(t), weight=torch.tensor(w), ignore_index=-100,
+                                            reduction=reduction)
+    ref.sum().backward()
+    np.testing.assert_allclose(loss, ref.detach().numpy(), rtol=1e-12)
+    np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
