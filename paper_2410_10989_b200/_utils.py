@@ -55,6 +55,22 @@ def lib():
     return _capi.load()
 
 
+def device_guard(fn):
+    """Run `fn` with the current CUDA device set to that of its first CUDA tensor argument: the
+    library launches on the current device (as torch ops do under their device guard)."""
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        for a in list(args) + list(kwargs.values()):
+            if isinstance(a, torch.Tensor) and a.is_cuda:
+                with torch.cuda.device(a.device):
+                    return fn(*args, **kwargs)
+        return fn(*args, **kwargs)
+
+    return wrapped
+
+
 def check(rc: int) -> None:
     _capi.check(rc)
 

@@ -19,6 +19,7 @@ from . import _capi, errors
 from ._utils import (
     as_targets,
     check,
+    device_guard,
     dtype_code,
     lib,
     ptr,
@@ -46,6 +47,7 @@ def _validate(label_smoothing, reduction, softcap):
         raise ValueError(f"softcap must greater than 0.0 or None. Got: {softcap}")
 
 
+@device_guard
 def cross_entropy_forward(
     _input: torch.Tensor,
     target: torch.Tensor,
@@ -111,6 +113,7 @@ def cross_entropy_forward(
     return loss, z_loss, acc, pred, _input
 
 
+@device_guard
 def cross_entropy_backward(_input: torch.Tensor, grad_output: torch.Tensor) -> torch.Tensor:
     """Scale the stored gradient by grad_output in place (LK/ops/cross_entropy.py:410-440)."""
     L = lib()

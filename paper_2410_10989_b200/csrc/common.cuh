@@ -62,11 +62,14 @@ inline int sm_count() {
 }
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel (per size increase).
-inline cudaError_t ensure_smem(const void* fn, int bytes) {
+inline cudaError_t ensure_smem(const void* fn, int bytes) {  // per (kernel, device): attributes are per device
   static std::mutex mu;
-  static std::unordered_map<const void*, int> done;
+  static std::unordered_map<uint64_t, int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = reinterpret_cast<uint64_t>(fn) * 64u + (uint64_t)dev;
   std::lock_guard<std::mutex> g(mu);
-  int& have = done[fn];
+  int& have = done[key];
   if (have >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
   if (e == cudaSuccess) have = bytes;

@@ -146,19 +146,13 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
   args.total_tiles = total;
   args.counter = counter;
   if (total == 0) return LK_OK;
-  static std::once_flag attr_once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(attr_once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(gemm_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(tc2::gemm2_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      tc2::SMEM_BYTES);
-    if (attr_err == cudaSuccess)
-      attr_err = cudaFuncSetAttribute(tc2::gemm2_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      tc2::SMEM_BYTES);
-  });
+  // dynamic shared-memory opt-in, per device (ensure_smem caches per (kernel, device))
+  cudaError_t attr_err = ensure_smem(reinterpret_cast<const void*>(gemm_kernel<__nv_bfloat16>), SMEM_BYTES);
+  if (attr_err == cudaSuccess) attr_err = ensure_smem(reinterpret_cast<const void*>(gemm_kernel<__half>), SMEM_BYTES);
+  if (attr_err == cudaSuccess)
+    attr_err = ensure_smem(reinterpret_cast<const void*>(tc2::gemm2_kernel<__nv_bfloat16>), tc2::SMEM_BYTES);
+  if (attr_err == cudaSuccess)
+    attr_err = ensure_smem(reinterpret_cast<const void*>(tc2::gemm2_kernel<__half>), tc2::SMEM_BYTES);
   LK_REQUIRE(attr_err == cudaSuccess, LK_CUDA_ERROR,
              std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(attr_err));
   if (cta_group == 1) {

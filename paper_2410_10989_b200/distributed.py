@@ -28,7 +28,7 @@ import torch
 import torch.distributed as dist
 
 from . import _capi
-from ._utils import as_targets, check, dtype_code, lib, ptr, stream_of, workspace
+from ._utils import as_targets, check, device_guard, dtype_code, lib, ptr, stream_of, workspace
 
 
 # ------------------------------------------------------------- token sharded
@@ -39,6 +39,7 @@ def shard_rows(n_rows: int, rank: int, world: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
+@device_guard
 def _count_cuda(t: torch.Tensor, vocab: int, ignore_index: int) -> torch.Tensor:
     out = torch.empty(2, dtype=torch.int64, device=t.device)
     check(lib().lk_count_targets(t.data_ptr(), t.numel(), vocab, ignore_index, out.data_ptr(), stream_of(t)))

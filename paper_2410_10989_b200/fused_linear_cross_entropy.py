@@ -19,6 +19,7 @@ from . import _capi, errors
 from ._utils import (
     as_targets,
     check,
+    device_guard,
     dtype_code,
     lib,
     ptr,
@@ -47,6 +48,7 @@ def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=Non
                                                 int(accum)))
 
 
+@device_guard
 def fused_linear_cross_entropy_forward(
     _input: torch.Tensor,
     weight: torch.Tensor,
@@ -179,6 +181,7 @@ def fused_linear_cross_entropy_forward(
     return loss, z_loss, acc, pred, grad_x, grad_w, grad_b
 
 
+@device_guard
 def fused_linear_cross_entropy_backward(grad_output, grad_input, grad_weight, grad_bias):
     """Scale the forward-computed gradients by grad_output (LK/ops/fused_linear_cross_entropy.py:247-291).
 

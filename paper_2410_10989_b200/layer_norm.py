@@ -12,9 +12,10 @@ import torch
 import torch.nn as nn
 
 from . import errors
-from ._utils import check, dtype_code, lib, ptr, require_cuda, stream_of, workspace
+from ._utils import check, device_guard, dtype_code, lib, ptr, require_cuda, stream_of, workspace
 
 
+@device_guard
 def layer_norm_forward(X, W, B, eps):
     require_cuda(X, W, B)
     shape = X.shape
@@ -32,6 +33,7 @@ def layer_norm_forward(X, W, B, eps):
     return Y.view(shape), X2, mean, rstd
 
 
+@device_guard
 def layer_norm_backward(dY, X2, W, B, mean, rstd):
     shape = dY.shape
     dY2 = dY.reshape(-1, shape[-1]).contiguous()

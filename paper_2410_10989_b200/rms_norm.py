@@ -12,9 +12,10 @@ import torch
 import torch.nn as nn
 
 from . import _capi
-from ._utils import check, dtype_code, lib, ptr, require_cuda, stream_of, workspace
+from ._utils import check, device_guard, dtype_code, lib, ptr, require_cuda, stream_of, workspace
 
 
+@device_guard
 def rms_norm_forward(X, W, eps, offset=0.0, casting_mode="llama"):
     require_cuda(X, W)
     mode = _capi.CASTING[casting_mode] if isinstance(casting_mode, str) else int(casting_mode)
@@ -31,6 +32,7 @@ def rms_norm_forward(X, W, eps, offset=0.0, casting_mode="llama"):
     return Y.view(shape), X2, rstd, mode
 
 
+@device_guard
 def rms_norm_backward(dY, X2, W, rstd, offset, mode, in_place):
     shape = dY.shape
     dY2 = dY.reshape(-1, shape[-1]).contiguous()

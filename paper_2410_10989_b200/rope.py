@@ -11,9 +11,10 @@ from __future__ import annotations
 import torch
 
 from . import errors
-from ._utils import check, dtype_code, lib, require_cuda, stream_of
+from ._utils import check, device_guard, dtype_code, lib, require_cuda, stream_of
 
 
+@device_guard
 def _rope(q, k, cos, sin, backward: bool):
     require_cuda(q, k, cos, sin)
     qt = q.transpose(1, 2).contiguous()  # physical (B, T, nq, d); no-op for HF layouts

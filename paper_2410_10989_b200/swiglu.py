@@ -12,9 +12,10 @@ import torch
 import torch.nn as nn
 
 from . import errors
-from ._utils import check, dtype_code, lib, require_cuda, stream_of
+from ._utils import check, device_guard, dtype_code, lib, require_cuda, stream_of
 
 
+@device_guard
 def _fwd(fn_name, a, b):
     require_cuda(a, b)
     if a.shape != b.shape or a.dtype != b.dtype:
@@ -26,6 +27,7 @@ def _fwd(fn_name, a, b):
     return a, b, c
 
 
+@device_guard
 def _bwd(fn_name, a, b, dc):
     dc = dc.contiguous()
     check(getattr(lib(), fn_name)(dc.data_ptr(), a.data_ptr(), b.data_ptr(), a.numel(), dtype_code(a), stream_of(a)))
