@@ -176,6 +176,7 @@ class CudaVocabOps:
         return _count_cuda(t, vocab, ignore_index)
 
 
+@device_guard
 def vocab_parallel_flce(
     x: torch.Tensor,
     w_shard: torch.Tensor,
