@@ -364,3 +364,22 @@ def test_flce_ce_weight(simt, reduction):
     assert ok, err
     ok, err = rel_close(gw.float().cpu().numpy(), rgw, tol)
     assert ok, err
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0)])
+def test_fp16_tcgen05_path_vs_oracle(kw):
+    """fp16 operands through the tcgen05 path (kind::f16 with the f16 descriptor format)."""
+    rng = np.random.default_rng(51)
+    bt, h, v = 700, 256, 3000
+    x = rng.uniform(-1, 1, (bt, h))
+    w = rng.uniform(-1, 1, (v, h)) / math.sqrt(h) * 3
+    t = rng.integers(0, v, bt)
+    t[rng.random(bt) < 0.1] = -100
+    xh, wh = cuda(x, torch.float16), cuda(w, torch.float16)
+    loss, _, gx, gw, _ = flce(xh, wh, cuda(t, torch.long), chunk_rows=256, **kw)
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(xh.double().cpu().numpy(), wh.double().cpu().numpy(), t, **kw)
+    assert rel_close(loss.item(), ref_loss, 2e-2)[0]
+    ok, err = rel_close(gx.float().cpu().numpy(), rgx, 2e-2)
+    assert ok, err
+    ok, err = rel_close(gw.float().cpu().numpy(), rgw, 2e-2)
+    assert ok, err

@@ -321,3 +321,22 @@ def test_empty_inputs_all_ops():
     loss = lk.LigerFusedLinearCrossEntropyLoss(reduction="sum")(W, xw, t)
     loss.backward()
     assert loss.item() == 0.0 and torch.all(W.grad == 0)
+
+
+@pytest.mark.parametrize("kind", ["swiglu", "geglu"])
+def test_glu_fp16_vs_oracle(kind):
+    g = torch.Generator(device="cuda").manual_seed(61)
+    a = (torch.rand(300, 1000, device="cuda", generator=g) * 8 - 4).to(torch.float16)
+    b = (torch.rand(300, 1000, device="cuda", generator=g) * 2 - 1).to(torch.float16)
+    dc = (torch.rand(300, 1000, device="cuda", generator=g) * 2 - 1).to(torch.float16)
+    f = lk.LigerSiLUMulFunction if kind == "swiglu" else lk.LigerGELUMulFunction
+    ar, br = a.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    c = f.apply(ar, br)
+    c.backward(dc)
+    fwd = rp.swiglu_forward if kind == "swiglu" else rp.geglu_forward
+    bwd = rp.swiglu_backward if kind == "swiglu" else rp.geglu_backward
+    a64, b64, dc64 = a.double().cpu().numpy(), b.double().cpu().numpy(), dc.double().cpu().numpy()
+    rda, rdb = bwd(dc64, a64, b64)
+    for name, got, ref in (("c", c.detach(), fwd(a64, b64)), ("da", ar.grad, rda), ("db", br.grad, rdb)):
+        ok, err = rel_close(got.float().cpu().numpy(), ref, 2e-2)
+        assert ok, (name, err)
