@@ -130,7 +130,9 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     const int64_t yl = y - a.col_offset;
     if (tid == 0) {
       float zt = 0.f;
-      if (yl >= 0 && yl < n) {
+      if (PART && a.row_stats) {
+        zt = a.row_stats[row].w;  // global target logit (the target may live on another shard)
+      } else if (yl >= 0 && yl < n) {
         zt = to_f<T>(xr[yl]);  // read before any pass-2 write of this row (after the barrier below)
         if (CAP && !PART) zt = cap * tanhf(zt * inv_cap);
       }
@@ -142,12 +144,19 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     float av = -INFINITY;  // argmax (option): value, first column
     int ai = 0x7fffffff;
     if constexpr (PART) {
-      const float4* pp = a.partials + row * a.n_parts;
-      for (int64_t jp = tid; jp < a.n_parts; jp += NC * 32) {
-        const float4 q = pp[jp];
-        ms_combine(m, se, q.x, q.y);
-        sz2.x += q.z;
-        if (want_arg) am_merge(av, ai, q.x, __float_as_int(q.w));
+      if (a.row_stats) {  // vocab-parallel: the all-reduced global row statistics
+        if (tid == 0) {
+          const float4 st = a.row_stats[row];
+          m = st.x; se = st.y; sz2.x = st.z;
+        }
+      } else {
+        const float4* pp = a.partials + row * a.n_parts;
+        for (int64_t jp = tid; jp < a.n_parts; jp += NC * 32) {
+          const float4 q = pp[jp];
+          ms_combine(m, se, q.x, q.y);
+          sz2.x += q.z;
+          if (want_arg) am_merge(av, ai, q.x, __float_as_int(q.w));
+        }
       }
     }
     for (int64_t j = 0; j < (PART ? 0 : npc); ++j, cur.next()) {
@@ -346,8 +355,9 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
 
 int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
   // raw logits (standalone CE) or FLCE finalize (partials + capped logits); not vocab-parallel
-  const bool part = a.partials != nullptr;
-  if (a.rows <= 0 || a.row_stats || (part && !a.input_capped) || (!part && a.input_capped)) return LK_UNSUPPORTED;
+  const bool part = a.partials != nullptr || a.row_stats != nullptr;  // FLCE / vocab-parallel finalize
+  if (a.rows <= 0 || (part && !a.input_capped) || (!part && a.input_capped)) return LK_UNSUPPORTED;
+  if (a.row_stats && (a.correct_rows || a.pred_rows)) return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   if ((a.n_cols * esz) % 16 || (a.ld * esz) % 16 || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;
   const int stages = 13;

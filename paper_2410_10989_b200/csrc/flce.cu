@@ -556,7 +556,8 @@ extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, cons
   ce.label_smoothing = label_smoothing; ce.lse_square_scale = lse_square_scale; ce.softcap = softcap;
   ce.input_capped = 1; ce.reduction = reduction; ce.compute_grad = 1; ce.n_valid = n_non_ignore;
   ce.loss_rows = loss_rows; ce.row_stats = reinterpret_cast<const float4*>(row_stats_global);
-  int rc = launch_ce_rows(ce, dtype, st);
+  int rc = launch_ce_ring(ce, dtype, st);  // persistent TMA ring; the block kernel for other shapes
+  if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dtype, st);
   if (rc) return rc;
   // dX partial (fp32, all-reduced by the caller) and local dW shard (fp32 accumulator)
   EpiArgs xe{};
