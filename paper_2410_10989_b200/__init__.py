@@ -30,24 +30,38 @@ from .swiglu import (
 __version__ = "0.1.0"
 
 
+def __getattr__(name):
+    """apply_liger_kernel_to_* live in .monkey_patch (imports transformers lazily)."""
+    if name.startswith("apply_liger_kernel_to_") or name in ("_apply_liger_kernel", "_apply_liger_kernel_to_instance"):
+        from . import monkey_patch
+
+        return getattr(monkey_patch, name)
+    raise AttributeError(f"module {__name__!r} has no attribute {name!r}")
+
+
 def liger_cross_entropy(input, target, weight=None, size_average=None, ignore_index=-100, reduce=None,
                         reduction="mean", label_smoothing=0.0, lse_square_scale=0.0, softcap=None,
-                        return_z_loss=False):
-    """Functional form (LK/transformers/functional.py:43-75)."""
-    loss, z_loss, _, _ = LigerCrossEntropyFunction.apply(input, target, weight, ignore_index, lse_square_scale,
-                                                         label_smoothing, reduction, softcap, return_z_loss,
-                                                         False, False)
-    return (loss, z_loss) if return_z_loss else loss
+                        return_z_loss=False, return_token_accuracy=False, return_predicted_tokens=False):
+    """Functional form (LK/transformers/functional.py:41-77)."""
+    loss, z_loss, acc, pred = LigerCrossEntropyFunction.apply(input, target, weight, ignore_index, lse_square_scale,
+                                                              label_smoothing, reduction, softcap, return_z_loss,
+                                                              return_token_accuracy, return_predicted_tokens)
+    if not return_z_loss and not return_token_accuracy and not return_predicted_tokens:
+        return loss
+    return CrossEntropyOutput(loss=loss, z_loss=z_loss, token_accuracy=acc, predicted_tokens=pred)
 
 
 def liger_fused_linear_cross_entropy(input, weight, target, bias=None, ce_weight=None, ignore_index=-100,
                                      lse_square_scale=0.0, label_smoothing=0.0, reduction="mean", softcap=None,
-                                     return_z_loss=False, accum_dtype=None, use_token_scaling=False):
-    """Functional form (LK/transformers/functional.py:78-120)."""
-    loss, z_loss, _, _ = LigerFusedLinearCrossEntropyFunction.apply(
+                                     return_z_loss=False, accum_dtype=None, use_token_scaling=False,
+                                     return_token_accuracy=False, return_predicted_tokens=False):
+    """Functional form (LK/transformers/functional.py:80-120)."""
+    loss, z_loss, acc, pred = LigerFusedLinearCrossEntropyFunction.apply(
         input, weight, target, bias, ce_weight, ignore_index, lse_square_scale, label_smoothing, reduction,
-        softcap, return_z_loss, accum_dtype, use_token_scaling, False, False)
-    return (loss, z_loss) if return_z_loss else loss
+        softcap, return_z_loss, accum_dtype, use_token_scaling, return_token_accuracy, return_predicted_tokens)
+    if not return_z_loss and not return_token_accuracy and not return_predicted_tokens:
+        return loss
+    return CrossEntropyOutput(loss=loss, z_loss=z_loss, token_accuracy=acc, predicted_tokens=pred)
 
 
 def liger_rms_norm(X, W, eps, offset=0.0, casting_mode="llama", in_place=True):
