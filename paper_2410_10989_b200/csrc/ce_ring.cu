@@ -28,9 +28,9 @@ namespace cer {
 
 constexpr int NC = 16;
 constexpr int THREADS = (NC + 1) * 32;
-constexpr uint32_t PIECE = 16384;             // bytes per ring stage
-constexpr int VPW = PIECE / 16 / NC;          // 16-byte vectors per warp per piece (64)
-constexpr int KPL = VPW / 32;                 // per lane (2)
+constexpr uint32_t PIECE = 32768;             // bytes per ring stage
+constexpr int VPW = PIECE / 16 / NC;          // 16-byte vectors per warp per piece (128)
+constexpr int KPL = VPW / 32;                 // per lane (4)
 constexpr float L2E = 1.4426950408889634f;
 
 __device__ __forceinline__ float ex2(float x) {
@@ -112,6 +112,12 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   const bool want_arg = a.correct_rows || a.pred_rows;
   ring::Cursor cur(stages);
   int par = 0;
+  // per-piece bookkeeping in 32-bit shared-window addresses and int column offsets
+  const uint32_t sbase = ring::s_u32(sm) + (uint32_t)(warp * VPW + lane) * 16u;
+  const uint32_t full_a = ring::s_u32(full), empty_a = ring::s_u32(empty);
+  const int npc32 = (int)npc;
+  const int tail_nvec = (int)((row_bytes - (npc - 1) * (int64_t)PIECE) / 16);
+  const int v0 = warp * VPW + lane;
   for (int64_t i = 0; i < n_local; ++i) {
     const int64_t row = b + i * G;
     T* xr = static_cast<T*>(a.x) + row * a.ld;
@@ -159,17 +165,16 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         }
       }
     }
-    for (int64_t j = 0; j < (PART ? 0 : npc); ++j, cur.next()) {
+    for (int j = 0; j < (PART ? 0 : npc32); ++j, cur.next()) {
       const int s = cur.s;
-      ring::wait(&full[s], cur.phase);
-      const int nvec = (int)(min((int64_t)PIECE, row_bytes - j * PIECE) / 16);
-      const uint8_t* st = sm + (size_t)s * PIECE;
-      const int v0 = warp * VPW + lane;
+      ring::wait(full_a + 8u * (uint32_t)s, cur.phase);
+      const int nvec = j == npc32 - 1 ? tail_nvec : (int)(PIECE / 16);
+      const uint32_t st = sbase + (uint32_t)s * PIECE;
       uint4 raw[KPL];
 #pragma unroll
-      for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + (v0 + 32 * k) * 16) : make_uint4(0, 0, 0, 0);
+      for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + 512u * k) : make_uint4(0, 0, 0, 0);
       __syncwarp();
-      if (lane == 0) ring::arrive(&empty[s]);
+      if (lane == 0) ring::arrive(empty_a + 8u * (uint32_t)s);
       float2 z[KPL][NP];
       float lmax = -INFINITY;
       if (nvec == (int)(PIECE / 16)) {  // whole piece (all but a ragged row tail): no masking
@@ -195,7 +200,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         se = se * ex2((m - mn) * L2E) + (acc.x + acc.y);  // m = -inf: ex2(-inf) = 0, se = 0
         m = mn;
         if (want_arg && lmax > av) {  // option; strict: earlier columns keep ties
-          const int cbase = (int)(j * (int64_t)(PIECE / sizeof(T)));
+          const int cbase = j * (int)(PIECE / sizeof(T));
 #pragma unroll
           for (int k = KPL - 1; k >= 0; --k)
 #pragma unroll
@@ -233,7 +238,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         se = (m == -INFINITY ? 0.f : se * ex2((m - mn) * L2E)) + (acc.x + acc.y);
         m = mn;
         if (want_arg && lmax > av) {
-          const int cbase = (int)(j * (int64_t)(PIECE / sizeof(T)));
+          const int cbase = j * (int)(PIECE / sizeof(T));
 #pragma unroll
           for (int k = KPL - 1; k >= 0; --k)
 #pragma unroll
@@ -286,18 +291,21 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     const float2 coef2 = make_float2(coef, coef);
     const float2 neps2 = make_float2(rcf.ceps, rcf.ceps);
     const float hit_s = rcf.chit;
-    for (int64_t j = 0; j < npc; ++j, cur.next()) {
+    for (int j = 0; j < npc32; ++j, cur.next()) {
       const int s = cur.s;
-      ring::wait(&full[s], cur.phase);
-      const int nvec = (int)(min((int64_t)PIECE, row_bytes - j * PIECE) / 16);
-      const uint8_t* st = sm + (size_t)s * PIECE;
-      const int v0 = warp * VPW + lane;
+      ring::wait(full_a + 8u * (uint32_t)s, cur.phase);
+      const int nvec = j == npc32 - 1 ? tail_nvec : (int)(PIECE / 16);
+      const uint32_t st = sbase + (uint32_t)s * PIECE;
       uint4 raw[KPL];
 #pragma unroll
-      for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + (v0 + 32 * k) * 16) : make_uint4(0, 0, 0, 0);
+      for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + 512u * k) : make_uint4(0, 0, 0, 0);
       __syncwarp();
-      if (lane == 0) ring::arrive(&empty[s]);
-      const int64_t col0 = j * (int64_t)(PIECE / sizeof(T));
+      if (lane == 0) ring::arrive(empty_a + 8u * (uint32_t)s);
+      const int64_t col0 = (int64_t)j * (PIECE / sizeof(T));
+      T* xp = xr + col0 + (int64_t)v0 * NV;  // this lane's first vector of the piece
+      // target column relative to that vector, as a 32-bit value (far away when not in the piece)
+      const int64_t trel64 = yl - col0 - (int64_t)v0 * NV;
+      const int trel = trel64 >= -(int64_t)(PIECE / sizeof(T)) && trel64 < (int64_t)(PIECE / sizeof(T)) ? (int)trel64 : INT_MIN / 2;
 #pragma unroll
       for (int k = 0; k < KPL; ++k) {
         const int v = v0 + 32 * k;
@@ -320,11 +328,11 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
             if (CAP) g = __fmul2_rn(g, dc);
             z[e] = g;
           }
-          ring::stg128(xr + col0 + (int64_t)v * NV, P::pack(z));
+          ring::stg128(xp + 32 * k * NV, P::pack(z));
           // the target column: rewrite that one element after the vector store (same thread,
           // program order) -- keeps the per-element path free of the compare
-          const uint64_t off = (uint64_t)(yl - col0 - (int64_t)v * NV);
-          if (off < (uint64_t)NV) {
+          const uint32_t off = (uint32_t)(trel - 32 * k * NV);
+          if (off < (uint32_t)NV) {
             const uint32_t word = off * sizeof(T) / 4;
             const uint32_t u = word == 0 ? raw[k].x : word == 1 ? raw[k].y : word == 2 ? raw[k].z : raw[k].w;
             float zt;
@@ -360,7 +368,7 @@ int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
   if (a.row_stats && (a.correct_rows || a.pred_rows)) return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   if ((a.n_cols * esz) % 16 || (a.ld * esz) % 16 || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;
-  const int stages = 13;
+  const int stages = 6;  // 192 KB in flight per SM
   const size_t smem = (size_t)stages * cer::PIECE + 2 * stages * sizeof(uint64_t) + sizeof(cer::Smem);
   const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(a.rows, sm_count()));
   const bool cap = a.softcap > 0.f, ls = a.label_smoothing > 0.f;

@@ -38,6 +38,21 @@ __device__ __forceinline__ void wait(uint64_t* b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// 32-bit shared-window address forms (hot consumer loops: no generic<->shared conversions)
+__device__ __forceinline__ void arrive(uint32_t b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
+}
+__device__ __forceinline__ void wait(uint32_t b, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(b), "r"(parity)
+        : "memory");
+  } while (!done);
+}
 // global -> shared 1D bulk copy, completion counted on `bar` (bytes multiple of 16).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
