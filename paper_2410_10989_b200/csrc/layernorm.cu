@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
                                                          const T* __restrict__ w, const float* __restrict__ mean,
                                                          const float* __restrict__ rstd, T* dx,
                                                          float* __restrict__ dw_part, float* __restrict__ db_part,
-                                                         int rows, int cols, int slots) {
+                                                         int rows, int cols, int slots, T* dw_out, T* db_out) {
   using P = ring::Pairs<T>;
   constexpr int NP = P::NP, NV = 16 / sizeof(T);
   __shared__ float sh[128];
@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
       }
     }
   }
+  if (dw_out) rc::grid_colsums<T>(dw_part, dw_out, db_part, db_out, (int)gridDim.x, cols);  // cooperative launch
 }
 
 static int vpt_for(int64_t nvec, int* threads) {
@@ -263,6 +264,9 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
   const int vpt = ln::vpt_for(cols / nv, &threads);
   LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
   int64_t grid = 1;
+  bool done = false;
+  const char* cs = getenv("LK_NORM_COLSUM");  // "kernel": separate column-sum launches
+  const bool fused = !(cs && !strcmp(cs, "kernel"));
   if (rows == 0) {
     LK_CUDA(cudaMemsetAsync(pw, 0, (size_t)2 * gmax * cols * sizeof(float), st));
   } else {
@@ -277,13 +281,25 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
         int per_sm = 0;
         LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         grid = std::max<int64_t>(1, std::min<int64_t>({rows, gmax, (int64_t)std::max(1, per_sm) * sm_count()}));
-        kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
-                                                    static_cast<const T*>(weight), mean, rstd, static_cast<T*>(dx), pw,
-                                                    db ? pb : nullptr, (int)rows, (int)cols, slots);
+        const T *dyp = static_cast<const T*>(dy), *xp = static_cast<const T*>(x), *wp = static_cast<const T*>(weight);
+        T* dxp = static_cast<T*>(dx);
+        float* pbp = db ? pb : nullptr;
+        int rows_i = (int)rows, cols_i = (int)cols, slots_i = slots;
+        if (fused && per_sm > 0) {
+          // column sums inside the kernel behind a grid barrier: every CTA must be resident
+          T *dwp = static_cast<T*>(dw), *dbp = static_cast<T*>(db);
+          void* args[] = {&dyp, &xp, &wp, &mean, &rstd, &dxp, &pw, &pbp, &rows_i, &cols_i, &slots_i, &dwp, &dbp};
+          LK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid), dim3(threads),
+                                              args, (size_t)smem, st));
+          done = true;
+        } else {
+          kern<<<(unsigned)grid, threads, smem, st>>>(dyp, xp, wp, mean, rstd, dxp, pw, pbp, rows_i, cols_i, slots,
+                                                      nullptr, nullptr);
+        }
       });
     });
     int rc = check_launch("layernorm_bwd_cta");
-    if (rc) return rc;
+    if (rc || done) return rc;
   }
   int rc = launch_colsum_partials(pw, grid, cols, dw, dtype, st);
   if (rc || !db) return rc;

@@ -342,7 +342,10 @@ static int rms_fwd_cta_launch(const T* x, const T* w, T* y, R* rstd, int64_t row
 template <typename T, typename R>
 static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part,
                               int64_t rows, int64_t cols, float offset, int mode, int64_t g, cudaStream_t st,
-                              int64_t* g_used) {
+                              int64_t* g_used, T* dw, bool* colsum_done) {
+  // dgamma column sums inside the kernel (cooperative launch) unless LK_NORM_COLSUM=kernel
+  const char* cs = getenv("LK_NORM_COLSUM");
+  T* dw_out = (part && dw && !(cs && !strcmp(cs, "kernel"))) ? dw : nullptr;
   constexpr int NV = Vec16<T>::N;
   if (cols % NV || !aligned16_all({dy, x, w, dx}) || rows > 0x7fffffff) return LK_UNSUPPORTED;
   const int64_t nvec = cols / NV;
@@ -368,7 +371,9 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
         const unsigned grid =
             (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
         *g_used = grid;
-        kern<<<grid, threads, smem, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, slots);
+        LK_CUDA(launch_kernel(reinterpret_cast<const void*>(kern), dw_out != nullptr, grid, threads, smem, st, dy, x, w,
+                              rstd, dx, part, (int)rows, (int)cols, slots, dw_out));
+        *colsum_done = dw_out != nullptr;
         rc = check_launch("rmsnorm_bwd_cta_bf16_llama");
       });
       return rc;
@@ -384,7 +389,9 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
     per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
     *g_used = grid;
-    kern<<<grid, threads, 0, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, offset, mode);
+    LK_CUDA(launch_kernel(reinterpret_cast<const void*>(kern), dw_out != nullptr, grid, threads, 0, st, dy, x, w, rstd,
+                          dx, part, (int)rows, (int)cols, offset, mode, dw_out));
+    *colsum_done = dw_out != nullptr;
     rc = check_launch("rmsnorm_bwd_cta");
   });
   return rc;
@@ -498,10 +505,12 @@ static int64_t rms_bwd_grid(int64_t rows) {  // upper bound of the partial rows 
 
 template <typename T, typename R>
 static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
-                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used) {
+                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used, T* dw,
+                          bool* colsum_done) {
   const int impl = norm_impl();
   if (impl == IMPL_CTA) {
-    int rc = rms_bwd_cta_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used);
+    int rc = rms_bwd_cta_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used, dw,
+                                      colsum_done);
     if (rc != LK_UNSUPPORTED) return rc;
   }
   if (impl == IMPL_CTA || impl == IMPL_RING) {
@@ -575,17 +584,19 @@ extern "C" int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight,
   LK_DISPATCH_FLOAT(dtype, T, {
     const T* w = static_cast<const T*>(weight);
     int64_t g_used = g;
+    bool colsum_done = false;
     if (rows > 0) {
+      T* dwt = static_cast<T*>(dw);
       int rc = casting_mode == LK_CAST_NONE
                    ? rms_bwd_launch<T, T>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                           static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols,
-                                          offset, casting_mode, g, st, &g_used)
+                                          offset, casting_mode, g, st, &g_used, dwt, &colsum_done)
                    : rms_bwd_launch<T, float>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                               static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows,
-                                              cols, offset, casting_mode, g, st, &g_used);
+                                              cols, offset, casting_mode, g, st, &g_used, dwt, &colsum_done);
       if (rc) return rc;
     }
-    if (part) {
+    if (part && !colsum_done) {
       colsum_partials_kernel<T><<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(part, g_used, cols,
                                                                               static_cast<T*>(dw));
       return check_launch("colsum_partials_kernel");
