@@ -59,6 +59,10 @@ inline cudaError_t launch_kernel(const void* kern, bool cooperative, unsigned gr
                      : cudaLaunchKernel(kern, dim3(grid), dim3(threads), arr, smem, st);
 }
 
+inline int env_int(const char* name, int dflt) {  // tuning knobs read per call
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int sm_count() {

@@ -190,9 +190,9 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
   if (dw_out) rc::grid_colsums<T>(dw_part, dw_out, db_part, db_out, (int)gridDim.x, cols);  // cooperative launch
 }
 
-static int vpt_for(int64_t nvec, int* threads) {
+static int vpt_for(int64_t nvec, int* threads, int target = 256) {
   int v = 1;
-  while (v < 8 && (nvec + v - 1) / v > 256) v *= 2;
+  while (v < 8 && (nvec + v - 1) / v > target) v *= 2;
   if ((nvec + v - 1) / v > 256) return 0;
   *threads = (int)(((nvec + v - 1) / v + 31) / 32 * 32);
   return v;
@@ -228,7 +228,7 @@ extern "C" int lk_layernorm_fwd(const void* x, const void* weight, const void* b
                reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(y)) & 15) == 0,
              LK_NON_CONTIGUOUS, "buffers must be 16-byte aligned");
   int threads = 0;
-  const int vpt = ln::vpt_for(cols / nv, &threads);
+  const int vpt = ln::vpt_for(cols / nv, &threads, env_int("LK_LN_FWD_THREADS", 128));
   LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
   cudaStream_t st = as_stream(stream);
   LK_DISPATCH_FLOAT(dtype, T, {

@@ -317,10 +317,6 @@ static int cta_vpt(int64_t nvec, int target, int max_threads) {
   while (v < 8 && (nvec + v - 1) / v > target) v *= 2;
   return (nvec + v - 1) / v <= max_threads ? v : 0;
 }
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
 
 template <typename T, typename R>
 static int rms_fwd_cta_launch(const T* x, const T* w, T* y, R* rstd, int64_t rows, int64_t cols, float eps,
