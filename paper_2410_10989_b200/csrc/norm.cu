@@ -349,7 +349,8 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
   if constexpr (std::is_same<T, __nv_bfloat16>::value && std::is_same<R, float>::value) {
     if (mode == LK_CAST_LLAMA && offset == 0.f && w && !getenv("LK_NORM_NO_BF16_FAST")) {
       // 128-thread CTAs (VPT = 4 at H = 4096): 82% of HBM vs 78% with 256 threads (profiles/)
-      const int vpt = cta_vpt(nvec, env_int("LK_NORM_BWD_THREADS", 128), 512);
+      // <= 128 threads up to VPT 4, <= 256 at VPT 8 (the launch bounds)
+      const int vpt = cta_vpt(nvec, 128, 256);
       if (!vpt) return LK_UNSUPPORTED;
       const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
       const int64_t rb = cols * 2;

@@ -340,3 +340,31 @@ def test_glu_fp16_vs_oracle(kind):
     for name, got, ref in (("c", c.detach(), fwd(a64, b64)), ("da", ar.grad, rda), ("db", br.grad, rdb)):
         ok, err = rel_close(got.float().cpu().numpy(), ref, 2e-2)
         assert ok, (name, err)
+
+
+@pytest.mark.parametrize("cols", [8192, 16384, 24576])
+def test_norms_wide_rows_vs_torch(cols):
+    """Wide hidden sizes: the VPT-8 CTA kernels, their launch bounds, and the fallbacks past them."""
+    rows = 96
+    g = torch.Generator(device="cuda").manual_seed(cols)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(torch.bfloat16)
+    b = (torch.rand(cols, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    xr, wr = x.clone().requires_grad_(True), w.clone().requires_grad_(True)
+    lk.liger_rms_norm(xr, wr, 1e-6, 0.0, "llama", False).backward(dy)
+    xf, wf = x.float().requires_grad_(True), w.float().requires_grad_(True)
+    (xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-6) * wf).backward(dy.float())
+    assert close(xr.grad, xf.grad, 2e-2) and close(wr.grad, wf.grad, 2e-2)
+    if cols > 16384:  # beyond the register LayerNorm: a typed error, not a wrong answer
+        with pytest.raises(Exception):
+            lk.liger_layer_norm(x.clone(), w, b, 1e-6)
+        return
+    xr, wr, br = x.clone().requires_grad_(True), w.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    y = lk.liger_layer_norm(xr, wr, br, 1e-6)
+    y.backward(dy)
+    xf, wf, bf = x.float().requires_grad_(True), w.float().requires_grad_(True), b.float().requires_grad_(True)
+    yf = torch.nn.functional.layer_norm(xf, (cols,), wf, bf, eps=1e-6)
+    yf.backward(dy.float())
+    assert close(y, yf, 2e-2) and close(xr.grad, xf.grad, 2e-2)
+    assert close(wr.grad, wf.grad, 2e-2) and close(br.grad, bf.grad, 2e-2)
