@@ -368,3 +368,36 @@ def test_norms_wide_rows_vs_torch(cols):
     yf.backward(dy.float())
     assert close(y, yf, 2e-2) and close(xr.grad, xf.grad, 2e-2)
     assert close(wr.grad, wf.grad, 2e-2) and close(br.grad, bf.grad, 2e-2)
+
+
+def test_norm_backward_in_cuda_graph():
+    """The in-kernel column sums use a cooperative launch: it must capture and replay in a CUDA graph."""
+    rows, cols = 1024, 4096
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(torch.bfloat16)
+    b = (torch.rand(cols, device="cuda", generator=g) - 0.5).to(torch.bfloat16)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    xs = x.clone().requires_grad_(True)
+    ws, bs = w.clone().requires_grad_(True), b.clone().requires_grad_(True)
+
+    def step():
+        xs.grad = ws.grad = bs.grad = None
+        lk.liger_rms_norm(xs, ws, 1e-6, 0.0, "llama", False).backward(dy)
+        gx, gw = xs.grad.clone(), ws.grad.clone()
+        xs.grad = None
+        lk.liger_layer_norm(xs, ws, bs, 1e-6).backward(dy)
+        return gx, gw, xs.grad.clone(), ws.grad.clone(), bs.grad.clone()
+
+    eager = step()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()  # warm-up on the side stream (allocator pools)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        out = step()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b_) for a, b_ in zip(eager, out))
