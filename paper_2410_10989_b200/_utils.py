@@ -85,7 +85,11 @@ def as_targets(target: torch.Tensor) -> torch.Tensor:
 
 
 def raise_if_out_of_range(stats: torch.Tensor, vocab: int) -> None:
-    if CHECK_TARGETS and int(stats[1].item()) > 0:
+    # Under CUDA-graph capture the host read is not allowed: the check is skipped (the kernels
+    # never index outside the row for such targets; the device-side count stays in `stats`).
+    if not CHECK_TARGETS or torch.cuda.is_current_stream_capturing():
+        return
+    if int(stats[1].item()) > 0:
         raise errors.TargetOutOfRange(
             f"{int(stats[1].item())} target(s) outside [0, {vocab}) that are not ignore_index"
         )
