@@ -80,6 +80,66 @@ __global__ void __launch_bounds__(256) rope_kernel(T* __restrict__ q, T* __restr
   }
 }
 
+// Token-major variant (the common shapes): one thread per (head, vector) of a token -- its
+// head / vector / cos-offset decomposition is computed once -- and each CTA walks a
+// contiguous token range two tokens at a time (both tokens' loads issued before either's
+// stores), so the per-item 64-bit index divisions of the grid-stride kernel disappear.
+template <typename T, typename C>
+__global__ void __launch_bounds__(1024) rope_tok_kernel(T* __restrict__ q, T* __restrict__ k,
+                                                        const C* __restrict__ cosp, const C* __restrict__ sinp,
+                                                        int tokens, int seq, int nq, int nk, int d, int cos_per_tok,
+                                                        int tok_per_cta, int backward) {
+  constexpr int NV = Vec16<T>::N;
+  const int half = d / 2, vph = half / NV;
+  const int h = threadIdx.x / vph, i0 = (threadIdx.x - h * vph) * NV;
+  const float sgn = backward ? -1.f : 1.f;
+  const int t0 = blockIdx.x * tok_per_cta, t1 = min(tokens, t0 + tok_per_cta);
+  T* const hb = h < nq ? q + (int64_t)h * d : k + (int64_t)(h - nq) * d;
+  const int64_t tstride = (int64_t)(h < nq ? nq : nk) * d;
+  int t = t0 % seq;  // position of token t0 inside its sequence (cos/sin row when shared by the batch)
+  auto rot = [&](int tok, int pos, Vec16<T>& a, Vec16<T>& b) {
+    const int64_t crow = (int64_t)(cos_per_tok ? tok : pos) * d + i0;
+    float c[NV], sn[NV];
+    if constexpr (sizeof(C) == sizeof(T)) {
+      Vec16<C> vc, vs;
+      vc.load(cosp + crow);
+      vs.load(sinp + crow);
+#pragma unroll
+      for (int e = 0; e < NV; ++e) { c[e] = vc.v[e]; sn[e] = sgn * vs.v[e]; }
+    } else {
+#pragma unroll
+      for (int e = 0; e < NV; ++e) { c[e] = to_f<C>(cosp[crow + e]); sn[e] = sgn * to_f<C>(sinp[crow + e]); }
+    }
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      const float x1 = a.v[e], x2 = b.v[e];
+      a.v[e] = x1 * c[e] - x2 * sn[e];
+      b.v[e] = x2 * c[e] + x1 * sn[e];
+    }
+  };
+  int tok = t0;
+  for (; tok + 1 < t1; tok += 2) {
+    T* p0 = hb + (int64_t)tok * tstride;
+    T* p1 = p0 + tstride;
+    const int pos0 = t, pos1 = t + 1 == seq ? 0 : t + 1;
+    Vec16<T> a0, b0, a1, b1;
+    a0.load(p0 + i0); b0.load(p0 + half + i0);
+    a1.load(p1 + i0); b1.load(p1 + half + i0);
+    rot(tok, pos0, a0, b0);
+    rot(tok + 1, pos1, a1, b1);
+    a0.store(p0 + i0); b0.store(p0 + half + i0);
+    a1.store(p1 + i0); b1.store(p1 + half + i0);
+    t = pos1 + 1 == seq ? 0 : pos1 + 1;
+  }
+  if (tok < t1) {
+    T* p0 = hb + (int64_t)tok * tstride;
+    Vec16<T> a0, b0;
+    a0.load(p0 + i0); b0.load(p0 + half + i0);
+    rot(tok, t, a0, b0);
+    a0.store(p0 + i0); b0.store(p0 + half + i0);
+  }
+}
+
 template <typename T, typename C>
 static int launch_rope(void* q, void* k, const void* cs, const void* sn, int64_t batch, int64_t seq,
                        int64_t nq, int64_t nk, int64_t d, int64_t cb, int backward, cudaStream_t st) {
@@ -88,6 +148,17 @@ static int launch_rope(void* q, void* k, const void* cs, const void* sn, int64_t
              ((reinterpret_cast<uintptr_t>(k) & 15) == 0);
   if (sizeof(C) == sizeof(T))  // vector cos/sin loads need 16-byte aligned tables
     vec = vec && ((reinterpret_cast<uintptr_t>(cs) & 15) == 0) && ((reinterpret_cast<uintptr_t>(sn) & 15) == 0);
+  const int64_t per_tok = (nq + nk) * ((d / 2) / NV), tokens = batch * seq;
+  if (vec && per_tok % 32 == 0 && per_tok <= 1024 && tokens <= 0x7fffffff && !getenv("LK_ROPE_FLAT")) {
+    const int threads = (int)per_tok;
+    const int64_t ctas = std::max<int64_t>(1, (int64_t)sm_count() * std::max(1, 2048 / threads));
+    const int tpc = (int)std::max<int64_t>(1, (tokens + ctas - 1) / ctas);
+    const unsigned g = (unsigned)((tokens + tpc - 1) / tpc);
+    rope_tok_kernel<T, C><<<g, threads, 0, st>>>(static_cast<T*>(q), static_cast<T*>(k), static_cast<const C*>(cs),
+                                                 static_cast<const C*>(sn), (int)tokens, (int)seq, (int)nq, (int)nk,
+                                                 (int)d, cb == 1 ? 0 : 1, tpc, backward);
+    return check_launch("rope_tok_kernel");
+  }
   const int64_t items = batch * seq * (nq + nk) * ((d / 2) / (vec ? NV : 1));
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)sm_count()));
   if (vec)

@@ -401,3 +401,32 @@ def test_norm_backward_in_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert all(torch.equal(a, b_) for a, b_ in zip(eager, out))
+
+
+@pytest.mark.parametrize("b,t,nq,nk,d,dtype,per_batch", [
+    (3, 37, 4, 4, 64, torch.bfloat16, False),   # token-major kernel, CTA token ranges crossing sequences
+    (2, 50, 6, 2, 64, torch.float32, True),     # token-major, per-batch cos/sin rows
+    (5, 7, 3, 1, 128, torch.float16, False),    # 64 items per token, odd token count
+    (2, 9, 3, 2, 48, torch.bfloat16, False),    # items per token not a warp multiple: grid-stride kernel
+])
+def test_rope_all_tokens_vs_torch(b, t, nq, nk, d, dtype, per_batch):
+    g = torch.Generator(device="cuda").manual_seed(b * 1000 + t)
+    q0 = torch.randn(b, t, nq, d, device="cuda", generator=g).to(dtype)
+    k0 = torch.randn(b, t, nk, d, device="cuda", generator=g).to(dtype)
+    ang = torch.rand(b if per_batch else 1, t, d // 2, device="cuda", generator=g) * 6.0
+    emb = torch.cat([ang, ang], -1)
+    cos, sin = emb.cos().to(dtype), emb.sin().to(dtype)
+
+    def rot(x, c, s, sign):  # x (B, T, nh, d); tables (B|1, T, d)
+        c, s = c[:, :, None].float(), s[:, :, None].float() * sign
+        h = x.shape[-1] // 2
+        xf = x.float()
+        return xf * c + torch.cat([-xf[..., h:], xf[..., :h]], -1) * s
+
+    qo, ko = lk.liger_rotary_pos_emb(q0.clone().transpose(1, 2), k0.clone().transpose(1, 2), cos, sin)
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    assert close(qo.transpose(1, 2), rot(q0, cos, sin, 1.0), tol)
+    assert close(ko.transpose(1, 2), rot(k0, cos, sin, 1.0), tol)
+    dq, dk, _, _ = lk.rope._rope(q0.clone().transpose(1, 2), k0.clone().transpose(1, 2), cos, sin, backward=True)
+    assert close(dq.transpose(1, 2), rot(q0, cos, sin, -1.0), tol)
+    assert close(dk.transpose(1, 2), rot(k0, cos, sin, -1.0), tol)
