@@ -26,8 +26,9 @@ def ce(logits, target, ignore_index=-100, label_smoothing=0.0, lse_square_scale=
 
     token_scaling: Liger FLCE use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139,
     187-206): each row's loss, z-loss and gradient times its detached target probability.
-    weight: class weights without label smoothing (LK/ops/cross_entropy.py:122-124, 220-239,
-    278-288): loss_i = w[y_i](lse - z_y), MEAN over sum_valid w[y_i]; z-loss still over the count."""
+    weight: class weights (LK/ops/cross_entropy.py:122-124, 165-171, 220-239, 278-288):
+    loss_i = (1-ls) w[y_i](lse - z_y) + eps sum_c w_c (lse - z_c), MEAN over sum_valid w[y_i];
+    z-loss still over the count (torch F.cross_entropy(weight=, label_smoothing=) semantics)."""
     z = np.asarray(logits, dtype=np.float64)
     y = np.asarray(target, dtype=np.int64)
     rows, vocab = z.shape
@@ -53,19 +54,21 @@ def ce(logits, target, ignore_index=-100, label_smoothing=0.0, lse_square_scale=
     scale = 1.0 / max(n, 1) if reduction == "mean" else 1.0
     ts = np.exp(zy - lse) if token_scaling else np.ones(rows)  # per row, detached
     if weight is not None:
-        assert label_smoothing == 0.0
         wv = np.asarray(weight, dtype=np.float64)
         wy = np.where(valid, wv[ysafe], 0.0)
         swn = wy.sum() if reduction == "mean" else 1.0
         s1 = ts / (swn if swn != 0 else 1.0)
         s2 = ts * scale
-        loss = wy * (lse - zy) * s1 + zl * s2
+        ls = label_smoothing
+        base = (1.0 - ls) * wy * (lse - zy) + eps * (wv[None, :] * (lse[:, None] - zc)).sum(axis=1)
+        loss = base * s1 + zl * s2
         zl = zl * s2
         loss = np.where(valid, loss, 0.0)
         zl = np.where(valid, zl, 0.0)
         p = e / s
-        g = p * (wy * s1 + 2.0 * lse_square_scale * lse * s2)[:, None]
-        g[np.arange(rows), ysafe] -= np.where(valid, wy * s1, 0.0)
+        g = p * (((1.0 - ls) * wy + eps * wv.sum()) * s1 + 2.0 * lse_square_scale * lse * s2)[:, None]
+        g -= eps * wv[None, :] * s1[:, None] if np.ndim(s1) else eps * wv[None, :] * s1
+        g[np.arange(rows), ysafe] -= np.where(valid, (1.0 - ls) * wy * s1, 0.0)
         if t is not None:
             g *= 1.0 - t * t
         g[~valid] = 0.0

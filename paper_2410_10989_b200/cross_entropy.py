@@ -83,8 +83,6 @@ def cross_entropy_forward(
     if weight is not None:  # Liger class weights (LK/ops/cross_entropy.py:369-378)
         if weight.shape != (v,) or not torch.is_floating_point(weight):
             raise errors.ShapeMismatch(f"weight must be a floating tensor of size V={v}, got {tuple(weight.shape)}")
-        if label_smoothing > 0:
-            raise errors.UnsupportedOption("class weights with label_smoothing are not implemented in the B200 build")
         cw = weight.detach().to(device=dev, dtype=torch.float32).contiguous()
     correct = torch.empty(bt, dtype=torch.float32, device=dev) if return_token_accuracy else None
     pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None

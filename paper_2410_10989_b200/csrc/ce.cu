@@ -21,26 +21,38 @@ __global__ void reduce_sum_kernel(const float* __restrict__ v, int64_t n, float*
 
 // sum_{i valid} w[y_i] in a fixed order (one CTA, double accumulation): the MEAN denominator with
 // class weights (LK/ops/cross_entropy.py:369-375, sum_non_ignore_weight).
+// out = sum over valid targets of w[y] (the weighted MEAN denominator); with `total`, also
+// *total = sum_c w[c] over the vocabulary (the smoothing term's weight_sum).  One CTA,
+// fixed-order double tree: deterministic.
 __global__ void weight_sum_kernel(const int64_t* __restrict__ t, int64_t rows, int64_t ignore_index,
-                                  const float* __restrict__ w, float* out) {
-  __shared__ double sh[1024];
-  double acc = 0.0;
+                                  const float* __restrict__ w, float* out, int64_t vocab, float* total) {
+  __shared__ double sh[2][1024];
+  double acc = 0.0, tot = 0.0;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
     const int64_t y = t[i];
     if (y != ignore_index) acc += (double)w[y];
   }
-  sh[threadIdx.x] = acc;
+  if (total)
+    for (int64_t c = threadIdx.x; c < vocab; c += blockDim.x) tot += (double)w[c];
+  sh[0][threadIdx.x] = acc;
+  sh[1][threadIdx.x] = tot;
   __syncthreads();
   for (int k = blockDim.x / 2; k > 0; k >>= 1) {
-    if ((int)threadIdx.x < k) sh[threadIdx.x] += sh[threadIdx.x + k];
+    if ((int)threadIdx.x < k) {
+      sh[0][threadIdx.x] += sh[0][threadIdx.x + k];
+      sh[1][threadIdx.x] += sh[1][threadIdx.x + k];
+    }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *out = (float)sh[0];
+  if (threadIdx.x == 0) {
+    *out = (float)sh[0][0];
+    if (total) *total = (float)sh[1][0];
+  }
 }
 
 int launch_weight_sum(const int64_t* t, int64_t rows, int64_t ignore_index, const float* w, float* out,
-                      cudaStream_t st) {
-  weight_sum_kernel<<<1, 1024, 0, st>>>(t, rows, ignore_index, w, out);
+                      cudaStream_t st, int64_t vocab, float* total) {
+  weight_sum_kernel<<<1, 1024, 0, st>>>(t, rows, ignore_index, w, out, vocab, total);
   return check_launch("weight_sum_kernel");
 }
 
@@ -165,7 +177,7 @@ using namespace lk;
 
 extern "C" size_t lk_cross_entropy_workspace_bytes(int64_t rows) {
   (void)rows;
-  return 256;  // two int64 counters (n_non_ignore, out-of-range)
+  return 256;  // two int64 counters (n_non_ignore, out-of-range), class-weight sums at +32 / +36
 }
 
 extern "C" int lk_count_targets(const int64_t* targets, int64_t rows, int64_t vocab,
@@ -202,15 +214,15 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
              "label_smoothing must be in [0, 1]");
   LK_REQUIRE(workspace && workspace_bytes >= lk_cross_entropy_workspace_bytes(rows),
              LK_INVALID_ARGUMENT, "workspace too small");
-  LK_REQUIRE(!class_weight || label_smoothing == 0.f, LK_UNSUPPORTED,
-             "class weights with label smoothing are not implemented in the B200 build");
   cudaStream_t st = as_stream(stream);
   int64_t* counts = static_cast<int64_t*>(workspace);
   float* wsum = reinterpret_cast<float*>(static_cast<char*>(workspace) + 32);
+  float* wtot = reinterpret_cast<float*>(static_cast<char*>(workspace) + 36);
+  const bool wls = class_weight && label_smoothing > 0.f;
   int rc = launch_count_targets(targets, rows, vocab, ignore_index, counts, st);
   if (rc) return rc;
   if (class_weight) {
-    rc = launch_weight_sum(targets, rows, ignore_index, class_weight, wsum, st);
+    rc = launch_weight_sum(targets, rows, ignore_index, class_weight, wsum, st, vocab, wls ? wtot : nullptr);
     if (rc) return rc;
   }
   CeRowArgs a{};
@@ -221,6 +233,7 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
   a.loss_rows = loss_rows; a.z_loss_rows = z_loss_rows;
   a.correct_rows = correct_rows; a.pred_rows = pred_rows;
   a.class_weight = class_weight; a.sum_valid_weight = class_weight ? wsum : nullptr;
+  a.weight_total = wls ? wtot : nullptr;
   // LK_CE_IMPL = ring (default) | cluster | block (one CTA per row, ce_rows_kernel)
   const char* impl_env = getenv("LK_CE_IMPL");  // read per call so tests can switch paths
   const char impl = impl_env ? impl_env[0] : 'r';

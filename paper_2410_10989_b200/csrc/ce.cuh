@@ -53,6 +53,10 @@ struct CeRowArgs {
   // label smoothing: loss_i = w[y_i] (lse - z_y) / sum_valid(w[y]) (MEAN), gradient likewise.
   const float* class_weight;      // [vocab_total] fp32 or null
   const float* sum_valid_weight;  // device scalar sum_{valid i} w[y_i] (MEAN with class_weight)
+  // class weights WITH label smoothing (LK/ops/cross_entropy.py:165-171, 227-233, 280-285):
+  // smooth term eps sum_c w_c (lse - z_c); the statistics pass then sums z_c w_c, and the
+  // gradient gains a per-column -eps w_c term (ce_rows_kernel only).
+  const float* weight_total;      // device scalar sum_c w[c]
 };
 
 // Per-row loss and gradient coefficients: grad = p * pc + ceps - [col == y] * chit (then the
@@ -81,10 +85,18 @@ __device__ __forceinline__ RowCoef ce_row_coefs(const CeRowArgs& a, float lse, f
     }
     const float s2 = inv_n * ts;
     c.zl = lss * lse * lse * s2;
-    c.loss = wy * (lse - zy) * s1 + c.zl;
-    c.pc = wy * s1 + 2.f * lss * lse * s2;
-    c.ceps = 0.f;
-    c.chit = wy * s1;
+    if (lsm > 0.f) {  // sz = sum_c w_c z_c; ceps is multiplied by w[col] in the gradient pass
+      const float wt = *a.weight_total;
+      c.loss = ((1.f - lsm) * wy * (lse - zy) + eps * (lse * wt - sz)) * s1 + c.zl;
+      c.pc = ((1.f - lsm) * wy + eps * wt) * s1 + 2.f * lss * lse * s2;
+      c.ceps = -eps * s1;
+      c.chit = (1.f - lsm) * wy * s1;
+    } else {
+      c.loss = wy * (lse - zy) * s1 + c.zl;
+      c.pc = wy * s1 + 2.f * lss * lse * s2;
+      c.ceps = 0.f;
+      c.chit = wy * s1;
+    }
   } else {
     const float rs = inv_n * ts;
     float loss = lse - zy;
@@ -152,6 +164,8 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
   }
   const int64_t yl = y - a.col_offset;  // local column of the target (may be outside [0, n))
   const bool vec_ok = ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  // class weights with smoothing: the smoothing sum is sum_c w_c z_c (weights by global column)
+  const float* wcol = (a.class_weight && a.label_smoothing > 0.f) ? a.class_weight + a.col_offset : nullptr;
 
   float m, s, sz, zy;
   if (a.row_stats) {
@@ -177,7 +191,7 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
         }
         float mn = fmaxf(lm, cm);
         float acc = 0.f;
-        for (int i = 0; i < cnt; ++i) { acc += __expf(v[i] - mn); lz += v[i]; }
+        for (int i = 0; i < cnt; ++i) { acc += __expf(v[i] - mn); lz += wcol ? v[i] * wcol[col + i] : v[i]; }
         ls = (lm == -INFINITY ? 0.f : ls * __expf(lm - mn)) + acc;
         lm = mn;
       };
@@ -228,6 +242,26 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
     __syncthreads();
     m = bcast[0]; s = bcast[1]; sz = bcast[2]; zy = bcast[3];
   }
+  if (wcol && a.partials) {
+    // the precomputed statistics carry the unweighted sum: one extra read of the row for
+    // sum_c w_c z_c (x holds capped logits on these paths)
+    float lz = 0.f;
+    for (int64_t i = tid; i < n; i += BLOCK) {
+      float v = to_f<T>(x[i]);
+      if (has_cap && !a.input_capped) v = cap_val<T>(v, cap, ACCURATE);
+      lz += v * wcol[i];
+    }
+    lz = warp_sum(lz);
+    if (lane == 0) red_z[warp] = lz;
+    __syncthreads();
+    if (warp == 0) {
+      float wz = lane < BLOCK / 32 ? red_z[lane] : 0.f;
+      wz = warp_sum(wz);
+      if (lane == 0) bcast[2] = wz;
+    }
+    __syncthreads();
+    sz = bcast[2];
+  }
 
   const float lse = m + logf(s);
   const RowCoef rc = ce_row_coefs<T>(a, lse, zy, sz, y);
@@ -254,7 +288,7 @@ __global__ void __launch_bounds__(BLOCK) ce_rows_kernel(CeRowArgs a) {
         z = cap * t;
       }
     }
-    float g = __expf(z - m) * pc + rc.ceps;
+    float g = __expf(z - m) * pc + (wcol ? rc.ceps * wcol[col] : rc.ceps);
     if (col == yl) g -= rc.chit;
     if (has_cap) g *= (1.f - t * t);
     return g;
@@ -290,7 +324,7 @@ int launch_count_targets(const int64_t* t, int64_t rows, int64_t vocab, int64_t 
 int launch_reduce_sum(const float* v, int64_t n, float* out, cudaStream_t st);
 // sum over non-ignored rows of class_weight[target] (MEAN denominator with class weights)
 int launch_weight_sum(const int64_t* t, int64_t rows, int64_t ignore_index, const float* w, float* out,
-                      cudaStream_t st);
+                      cudaStream_t st, int64_t vocab = 0, float* total = nullptr);
 // Vocab-parallel stage 1: per-row local (max, sumexp, sum_logits, target_logit).
 int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols, int dtype,
                         const int64_t* target, int64_t col_offset, int64_t ignore_index,

@@ -366,6 +366,7 @@ int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
   const bool part = a.partials != nullptr || a.row_stats != nullptr;  // FLCE / vocab-parallel finalize
   if (a.rows <= 0 || (part && !a.input_capped) || (!part && a.input_capped)) return LK_UNSUPPORTED;
   if (a.row_stats && (a.correct_rows || a.pred_rows)) return LK_UNSUPPORTED;
+  if (a.class_weight && a.label_smoothing > 0.f) return LK_UNSUPPORTED;  // per-column weights: ce_rows_kernel
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   if ((a.n_cols * esz) % 16 || (a.ld * esz) % 16 || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;
   const int stages = 6;  // 192 KB in flight per SM

@@ -324,11 +324,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   if (rc) return rc;
   if (a->target_stats)
     LK_CUDA(cudaMemcpyAsync(a->target_stats, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-  LK_REQUIRE(!a->ce_weight || a->label_smoothing == 0.f, LK_UNSUPPORTED,
-             "ce_weight with label smoothing is not implemented in the B200 build");
   LK_REQUIRE(!a->ce_weight || !a->mean_count, LK_UNSUPPORTED, "ce_weight in the token-sharded mode");
+  const bool wls = a->ce_weight && a->label_smoothing > 0.f;
   if (a->ce_weight && BT > 0) {  // MEAN denominator: sum of the valid targets' weights (after counts)
-    rc = launch_weight_sum(a->target, BT, a->ignore_index, a->ce_weight, reinterpret_cast<float*>(counts + 2), st);
+    rc = launch_weight_sum(a->target, BT, a->ignore_index, a->ce_weight, reinterpret_cast<float*>(counts + 2), st,
+                           V, wls ? reinterpret_cast<float*>(counts + 3) : nullptr);
     if (rc) return rc;
   }
   if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
@@ -381,6 +381,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     ce.token_scaling = a->use_token_scaling;
     ce.class_weight = a->ce_weight;
     ce.sum_valid_weight = a->ce_weight ? reinterpret_cast<const float*>(counts + 2) : nullptr;
+    ce.weight_total = wls ? reinterpret_cast<const float*>(counts + 3) : nullptr;
     ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {

@@ -126,8 +126,6 @@ def fused_linear_cross_entropy_forward(
     if ce_weight is not None:  # Liger class weights (LK/ops/fused_linear_cross_entropy.py:86-98)
         if ce_weight.shape != (v,) or not torch.is_floating_point(ce_weight):
             raise errors.ShapeMismatch(f"ce_weight must be a floating tensor of size V={v}")
-        if label_smoothing > 0:
-            raise errors.UnsupportedOption("ce_weight with label_smoothing is not implemented in the B200 build")
         cw = ce_weight.detach().to(device=dev, dtype=torch.float32).contiguous()
     L = lib()
     dt = dtype_code(x)

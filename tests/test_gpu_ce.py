@@ -253,10 +253,12 @@ def test_ce_int64_offsets_beyond_2_31_elements():
 
 @pytest.mark.parametrize("impl", ["ring", "block"])
 @pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
-@pytest.mark.parametrize("kw", [dict(), dict(softcap=20.0, lse_square_scale=1e-4)])
+@pytest.mark.parametrize("kw", [dict(), dict(softcap=20.0, lse_square_scale=1e-4), dict(label_smoothing=0.1),
+                                dict(label_smoothing=0.2, softcap=20.0, lse_square_scale=1e-4)])
 def test_ce_class_weights(impl, reduction, kw, monkeypatch):
-    """Liger `weight` (class weights, LK/ops/cross_entropy.py:122-124, 220-239, 278-288) vs the
-    float64 oracle (itself pinned to torch F.cross_entropy(weight=...))."""
+    """Liger `weight` (class weights, LK/ops/cross_entropy.py:122-124, 165-171, 220-239, 278-288),
+    with and without label smoothing, vs the float64 oracle (itself pinned to torch
+    F.cross_entropy(weight=, label_smoothing=))."""
     monkeypatch.setenv("LK_CE_IMPL", impl)
     rows, v = 300, 4096
     g = torch.Generator(device="cuda").manual_seed(13)
@@ -273,5 +275,3 @@ def test_ce_class_weights(impl, reduction, kw, monkeypatch):
     assert ok, err
     ok, err = rel_close(x.grad.float().cpu().numpy(), rg, 2e-2)
     assert ok, err
-    with pytest.raises(errors.UnsupportedOption):
-        lk.LigerCrossEntropyLoss(weight=w, label_smoothing=0.1)(z.clone().requires_grad_(True), t)

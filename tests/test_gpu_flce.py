@@ -345,19 +345,21 @@ def test_flce_use_token_scaling(simt, kw):
     assert ok, err
 
 
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1), dict(label_smoothing=0.1, softcap=30.0)])
 @pytest.mark.parametrize("simt", [False, True])
 @pytest.mark.parametrize("reduction", ["mean", "sum"])
-def test_flce_ce_weight(simt, reduction):
-    """Liger ce_weight on the FLCE head vs the float64 oracle (no label smoothing)."""
+def test_flce_ce_weight(simt, reduction, kw):
+    """Liger ce_weight on the FLCE head (with and without label smoothing) vs the float64 oracle."""
     xb, wb, tb, x, w, t = bf16_problem(700, 128, 3000, seed=43, wscale=3.0)
     if simt:
         xb, wb = xb.float(), wb.float()
         x, w = xb.double().cpu().numpy(), wb.double().cpu().numpy()
     cw = torch.rand(3000, device="cuda") + 0.2
     loss, _, _, _, gx, gw, _ = flce_fwd(xb, wb, tb, cw, compute_grad_input=True, compute_grad_weight=True,
-                                        reduction=reduction, force_simt=simt, chunk_rows=256, lse_square_scale=1e-4)
+                                        reduction=reduction, force_simt=simt, chunk_rows=256, lse_square_scale=1e-4,
+                                        **kw)
     ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, weight=cw.double().cpu().numpy(), reduction=reduction,
-                                                 lse_square_scale=1e-4)
+                                                 lse_square_scale=1e-4, **kw)
     tol = 1e-4 if simt else 2e-2
     assert rel_close(loss.item(), ref_loss, tol)[0], (loss.item(), ref_loss)
     ok, err = rel_close(gx.float().cpu().numpy(), rgx, tol)

@@ -265,10 +265,11 @@ def test_liger_ref_token_scaling_matches_liger_formula():
     np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
 
 
+@pytest.mark.parametrize("ls", [0.0, 0.1])
 @pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
-def test_liger_ref_class_weights_match_torch(reduction):
-    """Class weights (no smoothing) restated per LK/ops/cross_entropy.py:122-124, 220-239,
-    278-288 equal torch-CPU float64 F.cross_entropy(weight=...) (+ z-loss over the count)."""
+def test_liger_ref_class_weights_match_torch(reduction, ls):
+    """Class weights (with and without smoothing) restated per LK/ops/cross_entropy.py:122-124,
+    165-171, 220-239, 278-288 equal torch-CPU float64 F.cross_entropy(weight=, label_smoothing=)."""
     import torch
 
     rng = np.random.default_rng(4)
@@ -276,10 +277,10 @@ def test_liger_ref_class_weights_match_torch(reduction):
     t = rng.integers(0, 25, 16)
     t[[3, 9]] = -100
     w = rng.random(25) + 0.2
-    loss, _, _, g = liger_ref.ce(z, t, weight=w, reduction=reduction)
+    loss, _, _, g = liger_ref.ce(z, t, weight=w, reduction=reduction, label_smoothing=ls)
     zt = torch.tensor(z, requires_grad=True)
     ref = torch.nn.functional.cross_entropy(zt, torch.tensor(t), weight=torch.tensor(w), ignore_index=-100,
-                                            reduction=reduction)
+                                            reduction=reduction, label_smoothing=ls)
     ref.sum().backward()
     np.testing.assert_allclose(loss, ref.detach().numpy(), rtol=1e-12)
     np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
