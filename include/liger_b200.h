@@ -275,6 +275,11 @@ int lk_swiglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, v
 int lk_swiglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream);
 int lk_geglu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, void* stream);
 int lk_geglu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void* stream);
+/* Liger LigerSiLUMulFunction(a, b, gate_multiplier) (LK/ops/swiglu.py:16-62, 113-160):
+ * c = silu(gate_multiplier * a) * b; backward da = dc * silu'(gm * a) * b * gm, db = dc * silu(gm * a),
+ * written in place.  gate_multiplier == 1 is lk_swiglu_fwd / lk_swiglu_bwd. */
+int lk_swiglu_fwd_ex(const void* a, const void* b, void* c, int64_t n, float gate_multiplier, int dtype, void* stream);
+int lk_swiglu_bwd_ex(const void* dc, void* a, void* b, int64_t n, float gate_multiplier, int dtype, void* stream);
 
 /* ---- GEMM test hook ----------------------------------------------------- */
 /* D[M, N] (fp32, row-major) = A · B for the three operand layouts FLCE uses

@@ -123,6 +123,8 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "lk_swiglu_fwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_swiglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
+    "lk_swiglu_fwd_ex": (c_int, [c_void, c_void, c_void, c_i64, c_float, c_int, c_void]),
+    "lk_swiglu_bwd_ex": (c_int, [c_void, c_void, c_void, c_i64, c_float, c_int, c_void]),
     "lk_geglu_fwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_geglu_bwd": (c_int, [c_void, c_void, c_void, c_i64, c_int, c_void]),
     "lk_layernorm_fwd": (c_int, [c_void, c_void, c_void, c_void, c_void, c_void, c_i64, c_i64, c_float, c_int,

@@ -16,30 +16,33 @@ from ._utils import check, device_guard, dtype_code, lib, require_cuda, stream_o
 
 
 @device_guard
-def _fwd(fn_name, a, b):
+def _fwd(fn_name, a, b, *extra):
     require_cuda(a, b)
     if a.shape != b.shape or a.dtype != b.dtype:
         raise errors.ShapeMismatch("gate and up halves must match in shape and dtype (rowfuse/ops.py:99-106)")
     a = a.contiguous()
     b = b.contiguous()
     c = torch.empty_like(a)
-    check(getattr(lib(), fn_name)(a.data_ptr(), b.data_ptr(), c.data_ptr(), a.numel(), dtype_code(a), stream_of(a)))
+    check(getattr(lib(), fn_name)(a.data_ptr(), b.data_ptr(), c.data_ptr(), a.numel(), *extra, dtype_code(a),
+                                  stream_of(a)))
     return a, b, c
 
 
 @device_guard
-def _bwd(fn_name, a, b, dc):
+def _bwd(fn_name, a, b, dc, *extra):
     dc = dc.contiguous()
-    check(getattr(lib(), fn_name)(dc.data_ptr(), a.data_ptr(), b.data_ptr(), a.numel(), dtype_code(a), stream_of(a)))
+    check(getattr(lib(), fn_name)(dc.data_ptr(), a.data_ptr(), b.data_ptr(), a.numel(), *extra, dtype_code(a),
+                                  stream_of(a)))
     return a, b
 
 
-def swiglu_forward(a, b):
-    return _fwd("lk_swiglu_fwd", a, b)
+def swiglu_forward(a, b, gate_multiplier: float = 1.0):
+    """c = silu(gate_multiplier * a) * b (LK/ops/swiglu.py:65-86)."""
+    return _fwd("lk_swiglu_fwd_ex", a, b, float(gate_multiplier))
 
 
-def swiglu_backward(a, b, dc):
-    return _bwd("lk_swiglu_bwd", a, b, dc)
+def swiglu_backward(a, b, dc, gate_multiplier: float = 1.0):
+    return _bwd("lk_swiglu_bwd_ex", a, b, dc, float(gate_multiplier))
 
 
 def geglu_forward(a, b):
@@ -53,11 +56,11 @@ def geglu_backward(a, b, dc):
 class LigerSiLUMulFunction(torch.autograd.Function):
     @staticmethod
     def forward(ctx, a, b, gate_multiplier: float = 1.0, down_multiplier: float = 1.0):
-        if float(gate_multiplier) != 1.0:
-            raise errors.UnsupportedOption("gate_multiplier != 1.0 is not implemented in the B200 build")
-        a, b, c = swiglu_forward(a, b)
+        """LK/ops/swiglu.py:110-160: c = silu(gate_multiplier * a) * b * down_multiplier."""
+        a, b, c = swiglu_forward(a, b, gate_multiplier)
         if float(down_multiplier) != 1.0:
             c = c * down_multiplier
+        ctx.gate_multiplier = float(gate_multiplier)
         ctx.down_multiplier = float(down_multiplier)
         ctx.save_for_backward(a, b)
         return c
@@ -67,7 +70,7 @@ class LigerSiLUMulFunction(torch.autograd.Function):
         a, b = ctx.saved_tensors
         if ctx.down_multiplier != 1.0:
             dc = dc * ctx.down_multiplier
-        a, b = swiglu_backward(a, b, dc)
+        a, b = swiglu_backward(a, b, dc, ctx.gate_multiplier)
         return a, b, None, None
 
 

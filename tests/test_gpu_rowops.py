@@ -430,3 +430,24 @@ def test_rope_all_tokens_vs_torch(b, t, nq, nk, d, dtype, per_batch):
     dq, dk, _, _ = lk.rope._rope(q0.clone().transpose(1, 2), k0.clone().transpose(1, 2), cos, sin, backward=True)
     assert close(dq.transpose(1, 2), rot(q0, cos, sin, -1.0), tol)
     assert close(dk.transpose(1, 2), rot(k0, cos, sin, -1.0), tol)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("gm,dm", [(0.7, 1.0), (2.5, 1.5), (1.0, 0.5)])
+def test_swiglu_gate_and_down_multipliers(dtype, gm, dm):
+    """LigerSiLUMulFunction(a, b, gate_multiplier, down_multiplier) (LK/ops/swiglu.py:16-62, 110-160)
+    vs torch autograd of silu(gm * a).to(dtype) * b * dm in fp32."""
+    g = torch.Generator(device="cuda").manual_seed(int(gm * 10 + dm))
+    a = (torch.randn(96, 1000, device="cuda", generator=g) * 2).to(dtype)
+    b = torch.randn(96, 1000, device="cuda", generator=g).to(dtype)
+    dc = torch.randn(96, 1000, device="cuda", generator=g).to(dtype)
+    ar, br = a.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    c = lk.LigerSiLUMulFunction.apply(ar, br, gm, dm)
+    c.backward(dc)
+    af, bf = a.float().requires_grad_(True), b.float().requires_grad_(True)
+    act = torch.nn.functional.silu(gm * af)
+    cf = (act.to(dtype).float() if dtype != torch.float32 else act) * bf * dm
+    cf.backward(dc.float())
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    assert close(c, cf, tol)
+    assert close(ar.grad, af.grad, tol) and close(br.grad, bf.grad, tol)
