@@ -49,16 +49,6 @@ class ProfScope {
   int64_t mark_ = 0;
 };
 
-// Launch through cudaLaunchKernel / cudaLaunchCooperativeKernel (kernels that end in a grid
-// barrier must have every CTA resident).  The argument types must match the kernel's exactly.
-template <typename... A>
-inline cudaError_t launch_kernel(const void* kern, bool cooperative, unsigned grid, int threads, size_t smem,
-                                 cudaStream_t st, A... args) {
-  void* arr[] = {static_cast<void*>(&args)...};
-  return cooperative ? cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(threads), arr, smem, st)
-                     : cudaLaunchKernel(kern, dim3(grid), dim3(threads), arr, smem, st);
-}
-
 inline int env_int(const char* name, int dflt) {  // tuning knobs read per call
   const char* e = getenv(name);
   return e ? atoi(e) : dflt;

@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
                                                          const T* __restrict__ w, const float* __restrict__ mean,
                                                          const float* __restrict__ rstd, T* dx,
                                                          float* __restrict__ dw_part, float* __restrict__ db_part,
-                                                         int rows, int cols, int slots, T* dw_out, T* db_out) {
+                                                         int rows, int cols, int slots) {
+  rc::allow_dependents();
   using P = ring::Pairs<T>;
   constexpr int NP = P::NP, NV = 16 / sizeof(T);
   __shared__ float sh[128];
@@ -187,7 +188,6 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
       }
     }
   }
-  if (dw_out) rc::grid_colsums<T>(dw_part, dw_out, db_part, db_out, (int)gridDim.x, cols);  // cooperative launch
 }
 
 static int vpt_for(int64_t nvec, int* threads, int target = 256) {
@@ -202,7 +202,8 @@ static int64_t bwd_grid(int64_t rows) { return std::max<int64_t>(1, std::min<int
 }  // namespace ln
 
 // defined in norm.cu
-int launch_colsum_partials(const float* part, int64_t g, int64_t cols, void* out, int dtype, cudaStream_t st);
+int launch_colsum_partials(const float* p0, void* o0, const float* p1, void* o1, int64_t g, int64_t cols, int dtype,
+                           cudaStream_t st);
 
 }  // namespace lk
 
@@ -264,9 +265,6 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
   const int vpt = ln::vpt_for(cols / nv, &threads);
   LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
   int64_t grid = 1;
-  bool done = false;
-  const char* cs = getenv("LK_NORM_COLSUM");  // "kernel": separate column-sum launches
-  const bool fused = !(cs && !strcmp(cs, "kernel"));
   if (rows == 0) {
     LK_CUDA(cudaMemsetAsync(pw, 0, (size_t)2 * gmax * cols * sizeof(float), st));
   } else {
@@ -281,27 +279,13 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
         int per_sm = 0;
         LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
         grid = std::max<int64_t>(1, std::min<int64_t>({rows, gmax, (int64_t)std::max(1, per_sm) * sm_count()}));
-        const T *dyp = static_cast<const T*>(dy), *xp = static_cast<const T*>(x), *wp = static_cast<const T*>(weight);
-        T* dxp = static_cast<T*>(dx);
-        float* pbp = db ? pb : nullptr;
-        int rows_i = (int)rows, cols_i = (int)cols, slots_i = slots;
-        if (fused && per_sm > 0) {
-          // column sums inside the kernel behind a grid barrier: every CTA must be resident
-          T *dwp = static_cast<T*>(dw), *dbp = static_cast<T*>(db);
-          void* args[] = {&dyp, &xp, &wp, &mean, &rstd, &dxp, &pw, &pbp, &rows_i, &cols_i, &slots_i, &dwp, &dbp};
-          LK_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid), dim3(threads),
-                                              args, (size_t)smem, st));
-          done = true;
-        } else {
-          kern<<<(unsigned)grid, threads, smem, st>>>(dyp, xp, wp, mean, rstd, dxp, pw, pbp, rows_i, cols_i, slots,
-                                                      nullptr, nullptr);
-        }
+        kern<<<(unsigned)grid, threads, smem, st>>>(static_cast<const T*>(dy), static_cast<const T*>(x),
+                                                    static_cast<const T*>(weight), mean, rstd, static_cast<T*>(dx), pw,
+                                                    db ? pb : nullptr, (int)rows, (int)cols, slots);
       });
     });
     int rc = check_launch("layernorm_bwd_cta");
-    if (rc || done) return rc;
+    if (rc) return rc;
   }
-  int rc = launch_colsum_partials(pw, grid, cols, dw, dtype, st);
-  if (rc || !db) return rc;
-  return launch_colsum_partials(pb, grid, cols, db, dtype, st);
+  return launch_colsum_partials(pw, dw, db ? pb : nullptr, db, grid, cols, dtype, st);
 }

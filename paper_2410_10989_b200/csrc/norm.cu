@@ -221,9 +221,15 @@ rmsnorm_bwd_stream(const T* dy, const T* __restrict__ x, const T* __restrict__ w
 // thread's loads in flight at once), then the 32 group sums are added in ty order.
 // (One thread per column walking ~450 partial rows serially was latency-bound at 16 us.)
 template <typename T>
-__global__ void __launch_bounds__(1024) colsum_partials_kernel(const float* __restrict__ part, int64_t g,
-                                                               int64_t cols, T* __restrict__ out) {
+__global__ void __launch_bounds__(1024) colsum_partials_kernel(const float* __restrict__ p0, T* __restrict__ o0,
+                                                               const float* __restrict__ p1, T* __restrict__ o1,
+                                                               int64_t g, int64_t cols) {
+  // launched as a programmatic dependent of the backward kernel: the launch and this
+  // prologue overlap the backward's tail; the partials are read only after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ float red[32][33];
+  const float* part = blockIdx.y ? p1 : p0;
+  T* out = blockIdx.y ? o1 : o0;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32 + tx;
   float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -247,9 +253,23 @@ __global__ void __launch_bounds__(1024) colsum_partials_kernel(const float* __re
   }
 }
 
-int launch_colsum_partials(const float* part, int64_t g, int64_t cols, void* out, int dtype, cudaStream_t st) {
+// Fixed-order column sums of one or two [g, cols] fp32 partial arrays (dgamma, dbeta),
+// deterministic for a given g; a programmatic dependent launch of the preceding kernel.
+int launch_colsum_partials(const float* p0, void* o0, const float* p1, void* o1, int64_t g, int64_t cols, int dtype,
+                           cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)((cols + 31) / 32), p1 ? 2u : 1u);
+  cfg.blockDim = dim3(1024);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   LK_DISPATCH_FLOAT(dtype, T, {
-    colsum_partials_kernel<T><<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(part, g, cols, static_cast<T*>(out));
+    LK_CUDA(cudaLaunchKernelEx(&cfg, colsum_partials_kernel<T>, p0, static_cast<T*>(o0), p1, static_cast<T*>(o1), g,
+                               cols));
   });
   return check_launch("colsum_partials_kernel");
 }
@@ -338,10 +358,7 @@ static int rms_fwd_cta_launch(const T* x, const T* w, T* y, R* rstd, int64_t row
 template <typename T, typename R>
 static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part,
                               int64_t rows, int64_t cols, float offset, int mode, int64_t g, cudaStream_t st,
-                              int64_t* g_used, T* dw, bool* colsum_done) {
-  // dgamma column sums inside the kernel (cooperative launch) unless LK_NORM_COLSUM=kernel
-  const char* cs = getenv("LK_NORM_COLSUM");
-  T* dw_out = (part && dw && !(cs && !strcmp(cs, "kernel"))) ? dw : nullptr;
+                              int64_t* g_used) {
   constexpr int NV = Vec16<T>::N;
   if (cols % NV || !aligned16_all({dy, x, w, dx}) || rows > 0x7fffffff) return LK_UNSUPPORTED;
   const int64_t nvec = cols / NV;
@@ -368,9 +385,7 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
         const unsigned grid =
             (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
         *g_used = grid;
-        LK_CUDA(launch_kernel(reinterpret_cast<const void*>(kern), dw_out != nullptr, grid, threads, smem, st, dy, x, w,
-                              rstd, dx, part, (int)rows, (int)cols, slots, dw_out));
-        *colsum_done = dw_out != nullptr;
+        kern<<<grid, threads, smem, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, slots);
         rc = check_launch("rmsnorm_bwd_cta_bf16_llama");
       });
       return rc;
@@ -386,9 +401,7 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
     per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
     *g_used = grid;
-    LK_CUDA(launch_kernel(reinterpret_cast<const void*>(kern), dw_out != nullptr, grid, threads, 0, st, dy, x, w, rstd,
-                          dx, part, (int)rows, (int)cols, offset, mode, dw_out));
-    *colsum_done = dw_out != nullptr;
+    kern<<<grid, threads, 0, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, offset, mode);
     rc = check_launch("rmsnorm_bwd_cta");
   });
   return rc;
@@ -502,12 +515,10 @@ static int64_t rms_bwd_grid(int64_t rows) {  // upper bound of the partial rows 
 
 template <typename T, typename R>
 static int rms_bwd_launch(const T* dy, const T* x, const T* w, const R* rstd, T* dx, float* part, int64_t rows,
-                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used, T* dw,
-                          bool* colsum_done) {
+                          int64_t cols, float offset, int mode, int64_t g, cudaStream_t st, int64_t* g_used) {
   const int impl = norm_impl();
   if (impl == IMPL_CTA) {
-    int rc = rms_bwd_cta_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used, dw,
-                                      colsum_done);
+    int rc = rms_bwd_cta_launch<T, R>(dy, x, w, rstd, dx, part, rows, cols, offset, mode, g, st, g_used);
     if (rc != LK_UNSUPPORTED) return rc;
   }
   if (impl == IMPL_CTA || impl == IMPL_RING) {
@@ -581,23 +592,17 @@ extern "C" int lk_rmsnorm_bwd(const void* dy, const void* x, const void* weight,
   LK_DISPATCH_FLOAT(dtype, T, {
     const T* w = static_cast<const T*>(weight);
     int64_t g_used = g;
-    bool colsum_done = false;
     if (rows > 0) {
-      T* dwt = static_cast<T*>(dw);
       int rc = casting_mode == LK_CAST_NONE
                    ? rms_bwd_launch<T, T>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                           static_cast<const T*>(rstd), static_cast<T*>(dx), part, rows, cols,
-                                          offset, casting_mode, g, st, &g_used, dwt, &colsum_done)
+                                          offset, casting_mode, g, st, &g_used)
                    : rms_bwd_launch<T, float>(static_cast<const T*>(dy), static_cast<const T*>(x), w,
                                               static_cast<const float*>(rstd), static_cast<T*>(dx), part, rows,
-                                              cols, offset, casting_mode, g, st, &g_used, dwt, &colsum_done);
+                                              cols, offset, casting_mode, g, st, &g_used);
       if (rc) return rc;
     }
-    if (part && !colsum_done) {
-      colsum_partials_kernel<T><<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(part, g_used, cols,
-                                                                              static_cast<T*>(dw));
-      return check_launch("colsum_partials_kernel");
-    }
+    if (part) return launch_colsum_partials(part, dw, nullptr, nullptr, g_used, cols, dtype, st);
   });
   return LK_OK;
 }

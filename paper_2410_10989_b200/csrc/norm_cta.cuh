@@ -12,50 +12,14 @@
 // once per CTA, then the fixed-order column sum (rowfuse's _tree_sum role,
 // rowfuse/ops.py:138-152): bitwise deterministic for a given grid.
 #pragma once
-#include <cooperative_groups.h>
 #include "ring.cuh"
 
 namespace lk {
 namespace rc {
 
-// In-kernel dgamma/dbeta column sums for a cooperative (all CTAs co-resident) launch:
-// every CTA has written its fp32 partial row(s); after the grid barrier the CTAs split the
-// 32-column slices of the `narr` partial arrays between them and each sums its slice over
-// the g partial rows in a fixed order (warps stride the rows, then warp order): the same
-// bits for a given grid, and no separate column-sum launch on the critical path.
-// Partials are read through L2 (ld.global.cg): they were written by other SMs in this
-// kernel, so the non-coherent path must not be used.
-template <typename T>
-__device__ __forceinline__ void grid_colsums(const float* p0, T* o0, const float* p1, T* o1, int g, int cols) {
-  cooperative_groups::this_grid().sync();
-  __shared__ float red[32][33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int per = (cols + 31) / 32, total = (p1 ? 2 : 1) * per;
-  for (int sl = blockIdx.x; sl < total; sl += gridDim.x) {
-    const bool second = sl >= per;
-    const float* p = second ? p1 : p0;
-    const int c = (second ? sl - per : sl) * 32 + lane;
-    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-    if (c < cols) {
-      int i = w;
-      for (; i + 7 * nw < g; i += 8 * nw) {
-#pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += __ldcg(p + (int64_t)(i + u * nw) * cols + c);
-      }
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (i + u * nw < g) a[u] += __ldcg(p + (int64_t)(i + u * nw) * cols + c);
-    }
-    red[w][lane] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
-    __syncthreads();
-    if (w == 0 && c < cols) {
-      float t = 0.f;
-      for (int k = 0; k < nw; ++k) t += red[k][lane];
-      (second ? o1 : o0)[c] = from_f<T>(t);
-    }
-    __syncthreads();
-  }
-}
+// Programmatic dependent launch: let the column-sum grid queued behind this kernel be
+// scheduled while this one runs (it waits in griddepcontrol.wait for our completion).
+__device__ __forceinline__ void allow_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
 __device__ __forceinline__ uint4 ldg_stream(const void* p) {
   uint4 v;
@@ -152,7 +116,8 @@ rmsnorm_fwd_cta(const T* __restrict__ x, const T* __restrict__ w, T* __restrict_
 template <typename T, typename R, int VPT>
 __global__ void __launch_bounds__(512)
 rmsnorm_bwd_cta(const T* dy, const T* __restrict__ x, const T* __restrict__ w, const R* __restrict__ rstd, T* dx,
-                float* __restrict__ dw_part, int rows, int cols, float offset, int mode, T* dw_out) {
+                float* __restrict__ dw_part, int rows, int cols, float offset, int mode) {
+  allow_dependents();
   using P = ring::Pairs<T>;
   constexpr int NP = P::NP, NV = 16 / sizeof(T);
   __shared__ float sh[64];
@@ -241,7 +206,6 @@ rmsnorm_bwd_cta(const T* dy, const T* __restrict__ x, const T* __restrict__ w, c
       for (int e = 0; e < NP; e += 2) q[e / 2] = make_float4(acc[k][e].x, acc[k][e].y, acc[k][e + 1].x, acc[k][e + 1].y);
     }
   }
-  if (dw_out) grid_colsums<T>(dw_part, dw_out, nullptr, static_cast<T*>(nullptr), (int)gridDim.x, cols);
 }
 
 // bf16, llama casting, offset 0 (the Llama-3 configuration): m = bf16(dy * w) is exactly one
@@ -257,7 +221,8 @@ template <int VPT, bool EXACT>  // EXACT: nvec == VPT * blockDim.x (no column gu
 __global__ void __launch_bounds__(VPT == 1 ? 512 : 256, VPT == 1 ? 2 : (VPT == 2 ? 3 : 1))
 rmsnorm_bwd_cta_bf16_llama(const __nv_bfloat16* dy, const __nv_bfloat16* __restrict__ x,
                            const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd, __nv_bfloat16* dx,
-                           float* __restrict__ dw_part, int rows, int cols, int slots, __nv_bfloat16* dw_out) {
+                           float* __restrict__ dw_part, int rows, int cols, int slots) {
+  allow_dependents();
   using P = ring::Pairs<__nv_bfloat16>;
   __shared__ float sh[64];
   __shared__ uint64_t full[8];
@@ -358,7 +323,6 @@ rmsnorm_bwd_cta_bf16_llama(const __nv_bfloat16* dy, const __nv_bfloat16* __restr
       q[1] = make_float4(acc[k][2].x, acc[k][2].y, acc[k][3].x, acc[k][3].y);
     }
   }
-  if (dw_out) grid_colsums<__nv_bfloat16>(dw_part, dw_out, nullptr, static_cast<__nv_bfloat16*>(nullptr), (int)gridDim.x, cols);
 }
 
 }  // namespace rc

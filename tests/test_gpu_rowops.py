@@ -371,7 +371,7 @@ def test_norms_wide_rows_vs_torch(cols):
 
 
 def test_norm_backward_in_cuda_graph():
-    """The in-kernel column sums use a cooperative launch: it must capture and replay in a CUDA graph."""
+    """The column sums are a programmatic dependent launch: they must capture and replay in a CUDA graph."""
     rows, cols = 1024, 4096
     g = torch.Generator(device="cuda").manual_seed(11)
     x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
