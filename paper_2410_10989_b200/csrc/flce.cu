@@ -115,7 +115,7 @@ int default_cta_group() {
 }
 
 int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
-                   int* counter, cudaStream_t st, int cta_group) {
+                   int* counter, cudaStream_t st, int cta_group, bool register_epilogue) {
   LK_REQUIRE(dtype == LK_BF16 || dtype == LK_F16, LK_UNSUPPORTED, "tcgen05 path takes bf16/fp16");
   if (cta_group <= 0) cta_group = default_cta_group();
   const int tile_m = cta_group == 2 ? tc2::PBM : BM;
@@ -135,7 +135,7 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     if (rc) return rc;
     rc = encode_operand(&maps[2 * p + 1], b[p], dtype, b_rows_in_box, &P.b_mode);
     if (rc) return rc;
-    P.tma_out = getenv("LK_NO_TMA_EPILOGUE") ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
+    P.tma_out = register_epilogue ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
     args.prob[p] = P;
     args.idesc[p] = cta_group == 2 ? tc2::make_idesc2(dtype, a[p].mn_major, b[p].mn_major)
                                    : make_idesc(dtype, a[p].mn_major, b[p].mn_major);
@@ -650,10 +650,7 @@ extern "C" int lk_gemm_test_accum16(const void* a, const void* b, void* d16, int
   tc::TmaOperand A{a, k, m, k, 0}, B{b, k, n, k, 0};
   tc::Problem P{};
   P.M = m; P.N = n; P.K = k; P.n_fast = 0; P.epi = e;
-  if (!use_tma_reduce) setenv("LK_NO_TMA_EPILOGUE", "1", 1);
-  int rc = tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st);
-  if (!use_tma_reduce) unsetenv("LK_NO_TMA_EPILOGUE");
-  return rc;
+  return tc::launch_tc_gemm(&A, &B, &P, 1, dtype, static_cast<int*>(workspace), st, 0, !use_tma_reduce);
 #else
   return fail(LK_UNSUPPORTED, "built without tcgen05");
 #endif

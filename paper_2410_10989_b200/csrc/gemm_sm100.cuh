@@ -903,8 +903,9 @@ bool tma_ok(const TmaOperand& op);
 // Launch one or two problems in a single persistent launch.
 // Problem p: C[M, N] = A·B with A given by `a[p]` and B by `b[p]`.
 // cta_group: 1 = single-CTA 128x256 tiles, 2 = CTA-pair 256x256 tiles, 0 = default (pair).
+// register_epilogue: force the register-path epilogue (test hook for the 16-bit read-add path)
 int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
-                   int* counter, cudaStream_t st, int cta_group = 0);
+                   int* counter, cudaStream_t st, int cta_group = 0, bool register_epilogue = false);
 
 }  // namespace tc
 }  // namespace lk

@@ -229,7 +229,7 @@ extern "C" int lk_layernorm_fwd(const void* x, const void* weight, const void* b
                reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(y)) & 15) == 0,
              LK_NON_CONTIGUOUS, "buffers must be 16-byte aligned");
   int threads = 0;
-  const int vpt = ln::vpt_for(cols / nv, &threads, env_int("LK_LN_FWD_THREADS", 128));
+  const int vpt = ln::vpt_for(cols / nv, &threads, 128);
   LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
   cudaStream_t st = as_stream(stream);
   LK_DISPATCH_FLOAT(dtype, T, {

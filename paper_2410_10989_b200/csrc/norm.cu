@@ -308,12 +308,11 @@ static bool aligned16_all(std::initializer_list<const void*> ptrs) {
   return true;
 }
 
-// Implementation choice: LK_NORM_IMPL = ring (default) | warp | generic.
-// LK_NORM_IMPL = cta (default) | ring | warp | generic; read per call so tests can switch.
+// Implementation choice: LK_NORM_IMPL = cta (default) | ring | warp | generic; read per call so
+// the parity tests can run every path against the others.
 enum { IMPL_CTA = 0, IMPL_WARP = 1, IMPL_GENERIC = 2, IMPL_RING = 3 };
 static int norm_impl() {
   const char* e = getenv("LK_NORM_IMPL");
-  if (getenv("LK_NORM_NO_FAST")) return IMPL_GENERIC;
   if (!e) return IMPL_CTA;
   switch (e[0]) {
     case 'w': return IMPL_WARP;
@@ -345,7 +344,7 @@ static int rms_fwd_cta_launch(const T* x, const T* w, T* y, R* rstd, int64_t row
   if (cols % NV || !aligned16_all({x, w, y}) || rows > 0x7fffffff || rows * cols > ((int64_t)1 << 40))
     return LK_UNSUPPORTED;
   const int64_t nvec = cols / NV;
-  const int vpt = cta_vpt(nvec, env_int("LK_NORM_FWD_THREADS", 128), 256);
+  const int vpt = cta_vpt(nvec, 128, 256);
   if (!vpt) return LK_UNSUPPORTED;
   const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
   LK_VPT8_DISPATCH(vpt, VPT, {
@@ -364,14 +363,14 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
   const int64_t nvec = cols / NV;
   int rc = LK_OK;
   if constexpr (std::is_same<T, __nv_bfloat16>::value && std::is_same<R, float>::value) {
-    if (mode == LK_CAST_LLAMA && offset == 0.f && w && !getenv("LK_NORM_NO_BF16_FAST")) {
+    if (mode == LK_CAST_LLAMA && offset == 0.f && w) {
       // 128-thread CTAs (VPT = 4 at H = 4096): 82% of HBM vs 78% with 256 threads (profiles/)
       // <= 128 threads up to VPT 4, <= 256 at VPT 8 (the launch bounds)
       const int vpt = cta_vpt(nvec, 128, 256);
       if (!vpt) return LK_UNSUPPORTED;
       const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
       const int64_t rb = cols * 2;
-      const int slots = (int)std::max<int64_t>(2, std::min<int64_t>(env_int("LK_NORM_BWD_SLOTS", 3),
+      const int slots = (int)std::max<int64_t>(2, std::min<int64_t>(3,
                                                                     (96 * 1024) / (2 * rb)));
       const int smem = (int)(slots * 2 * rb);
       if (rb % 16 || smem > 200 * 1024) return LK_UNSUPPORTED;
@@ -381,7 +380,7 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
         LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), smem));
         int per_sm = 0;
         LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
-        per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
+        per_sm = std::max(1, std::min(per_sm, 8));
         const unsigned grid =
             (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
         *g_used = grid;
@@ -391,14 +390,14 @@ static int rms_bwd_cta_launch(const T* dy, const T* x, const T* w, const R* rstd
       return rc;
     }
   }
-  const int vpt = cta_vpt(nvec, env_int("LK_NORM_BWD_THREADS", 256), 512);
+  const int vpt = cta_vpt(nvec, 256, 512);
   if (!vpt) return LK_UNSUPPORTED;
   const int threads = (int)(((nvec + vpt - 1) / vpt + 31) / 32 * 32);
   LK_VPT8_DISPATCH(vpt, VPT, {
     auto kern = rc::rmsnorm_bwd_cta<T, R, VPT>;
     int per_sm = 0;
     LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0));
-    per_sm = std::max(1, std::min(per_sm, env_int("LK_NORM_BWD_CTAS_PER_SM", 8)));
+    per_sm = std::max(1, std::min(per_sm, 8));
     const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>({rows, g, (int64_t)per_sm * sm_count()}));
     *g_used = grid;
     kern<<<grid, threads, 0, st>>>(dy, x, w, rstd, dx, part, (int)rows, (int)cols, offset, mode);

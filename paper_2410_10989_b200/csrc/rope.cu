@@ -149,7 +149,7 @@ static int launch_rope(void* q, void* k, const void* cs, const void* sn, int64_t
   if (sizeof(C) == sizeof(T))  // vector cos/sin loads need 16-byte aligned tables
     vec = vec && ((reinterpret_cast<uintptr_t>(cs) & 15) == 0) && ((reinterpret_cast<uintptr_t>(sn) & 15) == 0);
   const int64_t per_tok = (nq + nk) * ((d / 2) / NV), tokens = batch * seq;
-  if (vec && per_tok % 32 == 0 && per_tok <= 1024 && tokens <= 0x7fffffff && !getenv("LK_ROPE_FLAT")) {
+  if (vec && per_tok % 32 == 0 && per_tok <= 1024 && tokens <= 0x7fffffff) {
     const int threads = (int)per_tok;
     const int64_t ctas = std::max<int64_t>(1, (int64_t)sm_count() * std::max(1, 2048 / threads));
     const int tpc = (int)std::max<int64_t>(1, (tokens + ctas - 1) / ctas);
