@@ -67,9 +67,9 @@ struct Glu {
 
 template <typename T, int ACT>
 __global__ void __launch_bounds__(256) glu_fwd_kernel(const T* __restrict__ a, const T* __restrict__ b,
-                                                      T* __restrict__ c, int64_t n, float gm) {
+                                                      T* __restrict__ c, int64_t n, float gm, bool vec) {
   constexpr int NV = Vec16<T>::N;
-  const int64_t nvec = n / NV;
+  const int64_t nvec = vec ? n / NV : 0;  // unaligned buffers: everything through the scalar loop
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   // two vectors per thread per iteration: four 16-byte loads in flight before any math
@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(256) glu_fwd_kernel(const T* __restrict__ a, c
 
 template <typename T, int ACT>
 __global__ void __launch_bounds__(256) glu_bwd_kernel(const T* __restrict__ dc, T* __restrict__ a,
-                                                      T* __restrict__ b, int64_t n, float gm) {
+                                                      T* __restrict__ b, int64_t n, float gm, bool vec) {
   constexpr int NV = Vec16<T>::N;
-  const int64_t nvec = n / NV;
+  const int64_t nvec = vec ? n / NV : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nvec; i += stride) {
     Vec16<T> vd, va, vb;
@@ -142,12 +142,11 @@ static int glu_fwd(const void* a, const void* b, void* c, int64_t n, int dtype, 
   LK_REQUIRE(n >= 0, LK_SIZE_MISMATCH, "n must be >= 0");
   if (n == 0) return LK_OK;
   LK_REQUIRE(a && b && c, LK_INVALID_ARGUMENT, "null pointer");
-  LK_REQUIRE(aligned16(a) && aligned16(b) && aligned16(c), LK_NON_CONTIGUOUS,
-             "GLU operands must be 16-byte aligned contiguous buffers");
+  const bool vec = aligned16(a) && aligned16(b) && aligned16(c);
   cudaStream_t st = as_stream(stream);
   LK_DISPATCH_FLOAT(dtype, T, {
     glu_fwd_kernel<T, ACT><<<grid_for(n, Vec16<T>::N), 256, 0, st>>>(
-        static_cast<const T*>(a), static_cast<const T*>(b), static_cast<T*>(c), n, gm);
+        static_cast<const T*>(a), static_cast<const T*>(b), static_cast<T*>(c), n, gm, vec);
   });
   return check_launch("glu_fwd_kernel");
 }
@@ -157,12 +156,11 @@ static int glu_bwd(const void* dc, void* a, void* b, int64_t n, int dtype, void*
   LK_REQUIRE(n >= 0, LK_SIZE_MISMATCH, "n must be >= 0");
   if (n == 0) return LK_OK;
   LK_REQUIRE(a && b && dc, LK_INVALID_ARGUMENT, "null pointer");
-  LK_REQUIRE(aligned16(a) && aligned16(b) && aligned16(dc), LK_NON_CONTIGUOUS,
-             "GLU operands must be 16-byte aligned contiguous buffers");
+  const bool vec = aligned16(a) && aligned16(b) && aligned16(dc);
   cudaStream_t st = as_stream(stream);
   LK_DISPATCH_FLOAT(dtype, T, {
     glu_bwd_kernel<T, ACT><<<grid_for(n, Vec16<T>::N), 256, 0, st>>>(
-        static_cast<const T*>(dc), static_cast<T*>(a), static_cast<T*>(b), n, gm);
+        static_cast<const T*>(dc), static_cast<T*>(a), static_cast<T*>(b), n, gm, vec);
   });
   return check_launch("glu_bwd_kernel");
 }

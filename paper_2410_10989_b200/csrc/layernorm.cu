@@ -190,6 +190,76 @@ __global__ void __launch_bounds__(256) layernorm_bwd_cta(const T* dy, const T* _
   }
 }
 
+// Generic fallbacks (any width, any alignment; Liger's Triton LayerNorm takes any hidden size):
+// scalar loads, the row re-read from L2 in the second pass.  Forward: one 256-thread CTA per
+// row.  Backward: persistent CTAs over row ranges; each thread owns columns tid, tid + 256, ...
+// of its CTA's dgamma / dbeta partial row in global memory (no races), summed by the same
+// fixed-order column-sum launch as the fast path.
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_fwd_generic(const T* __restrict__ x, const T* __restrict__ w,
+                                                             const T* __restrict__ b, T* __restrict__ y,
+                                                             float* __restrict__ mean, float* __restrict__ rstd,
+                                                             int cols, float eps) {
+  __shared__ float sh[128];
+  const int64_t row = blockIdx.x;
+  const T* xr = x + row * cols;
+  const float K = to_f<T>(xr[0]);
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float d = to_f<T>(xr[c]) - K;
+    s1 += d;
+    s2 = fmaf(d, d, s2);
+  }
+  const float2 tot = cta_sum2(s1, s2, sh, 0);
+  const float dm = tot.x / (float)cols, mu = K + dm;
+  const float r = rsqrtf(fmaxf(tot.y - tot.x * dm, 0.f) / (float)cols + eps);
+  if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = r; }
+  T* yr = y + row * cols;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    const float v = (to_f<T>(xr[c]) - mu) * r * to_f<T>(w[c]);
+    yr[c] = from_f<T>(b ? v + to_f<T>(b[c]) : v);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_bwd_generic(const T* dy, const T* __restrict__ x,
+                                                             const T* __restrict__ w, const float* __restrict__ mean,
+                                                             const float* __restrict__ rstd, T* dx,
+                                                             float* __restrict__ dw_part, float* __restrict__ db_part,
+                                                             int rows, int cols) {
+  rc::allow_dependents();
+  __shared__ float sh[128];
+  const int per = (rows + gridDim.x - 1) / gridDim.x;
+  const int r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float* pw = dw_part + (int64_t)blockIdx.x * cols;
+  float* pb = db_part ? db_part + (int64_t)blockIdx.x * cols : nullptr;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+    pw[c] = 0.f;
+    if (pb) pb[c] = 0.f;
+  }
+  int par = 0;
+  for (int row = r0; row < r1; ++row, par ^= 1) {
+    const float mu = mean[row], r = rstd[row];
+    const T* xr = x + (int64_t)row * cols;
+    const T* gr = dy + (int64_t)row * cols;
+    float pj = 0.f, sf = 0.f;
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+      const float g = to_f<T>(gr[c]), xt = (to_f<T>(xr[c]) - mu) * r, gy = g * to_f<T>(w[c]);
+      pj = fmaf(xt, gy, pj);
+      sf += gy;
+      pw[c] = fmaf(g, xt, pw[c]);
+      if (pb) pb[c] += g;
+    }
+    const float2 t = cta_sum2(pj, sf, sh, par);
+    const float proj = t.x / (float)cols, shift = t.y / (float)cols;
+    T* dxr = dx + (int64_t)row * cols;
+    for (int c = threadIdx.x; c < cols; c += blockDim.x) {  // dx may alias dy: read before write
+      const float xt = (to_f<T>(xr[c]) - mu) * r, gy = to_f<T>(gr[c]) * to_f<T>(w[c]);
+      dxr[c] = from_f<T>((gy - proj * xt - shift) * r);
+    }
+  }
+}
+
 static int vpt_for(int64_t nvec, int* threads, int target = 256) {
   int v = 1;
   while (v < 8 && (nvec + v - 1) / v > target) v *= 2;
@@ -223,15 +293,21 @@ extern "C" int lk_layernorm_fwd(const void* x, const void* weight, const void* b
   if (rows == 0) return LK_OK;
   LK_REQUIRE(x && weight && y && mean && rstd, LK_INVALID_ARGUMENT, "null pointer");
   LK_REQUIRE(rows <= 0x7fffffff, LK_SIZE_MISMATCH, "too many rows");
+  LK_REQUIRE(cols <= 0x7fffffff, LK_SIZE_MISMATCH, "hidden size too large");
   const int64_t nv = dtype == LK_F32 ? 4 : 8;
-  LK_REQUIRE(cols % nv == 0, LK_SIZE_MISMATCH, "hidden size must be a multiple of 16 bytes");
-  LK_REQUIRE(((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(weight) |
-               reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(y)) & 15) == 0,
-             LK_NON_CONTIGUOUS, "buffers must be 16-byte aligned");
+  const bool aligned = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(weight) |
+                         reinterpret_cast<uintptr_t>(bias) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
   int threads = 0;
-  const int vpt = ln::vpt_for(cols / nv, &threads, 128);
-  LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
+  const int vpt = cols % nv == 0 && aligned ? ln::vpt_for(cols / nv, &threads, 128) : 0;
   cudaStream_t st = as_stream(stream);
+  if (vpt == 0) {  // ragged / unaligned / wider than the register kernel
+    LK_DISPATCH_FLOAT(dtype, T, {
+      ln::layernorm_fwd_generic<T><<<(unsigned)rows, 256, 0, st>>>(
+          static_cast<const T*>(x), static_cast<const T*>(weight), static_cast<const T*>(bias), static_cast<T*>(y),
+          mean, rstd, (int)cols, eps);
+    });
+    return check_launch("layernorm_fwd_generic");
+  }
   LK_DISPATCH_FLOAT(dtype, T, {
     LK_LN_VPT(vpt, VPT, {
       ln::layernorm_fwd_cta<T, VPT><<<(unsigned)rows, threads, 0, st>>>(
@@ -255,18 +331,30 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
   LK_REQUIRE(workspace && workspace_bytes >= lk_layernorm_bwd_workspace_bytes(rows, cols), LK_INVALID_ARGUMENT,
              "workspace too small");
   LK_REQUIRE(rows == 0 || (dy && x && mean && rstd && dx), LK_INVALID_ARGUMENT, "null pointer");
+  LK_REQUIRE(cols <= 0x7fffffff, LK_SIZE_MISMATCH, "hidden size too large");
   const int64_t nv = dtype == LK_F32 ? 4 : 8;
-  LK_REQUIRE(cols % nv == 0, LK_SIZE_MISMATCH, "hidden size must be a multiple of 16 bytes");
   cudaStream_t st = as_stream(stream);
   float* pw = static_cast<float*>(workspace);
   const int64_t gmax = ln::bwd_grid(rows);
   float* pb = pw + gmax * cols;
+  const bool aligned = ((reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x) |
+                         reinterpret_cast<uintptr_t>(weight) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0;
   int threads = 0;
-  const int vpt = ln::vpt_for(cols / nv, &threads);
-  LK_REQUIRE(vpt > 0, LK_UNSUPPORTED, "hidden size too large for the register LayerNorm");
+  int vpt = cols % nv == 0 && aligned ? ln::vpt_for(cols / nv, &threads) : 0;
+  // the TMA ring needs >= 2 slots of (dy, x) rows in <= 200 KB of shared memory
+  if (vpt && 2 * 2 * cols * (dtype == LK_F32 ? 4 : 2) > 200 * 1024) vpt = 0;
   int64_t grid = 1;
   if (rows == 0) {
     LK_CUDA(cudaMemsetAsync(pw, 0, (size_t)2 * gmax * cols * sizeof(float), st));
+  } else if (vpt == 0) {  // ragged / unaligned / wide rows
+    grid = std::max<int64_t>(1, std::min<int64_t>({rows, gmax, 4 * (int64_t)sm_count()}));
+    LK_DISPATCH_FLOAT(dtype, T, {
+      ln::layernorm_bwd_generic<T><<<(unsigned)grid, 256, 0, st>>>(
+          static_cast<const T*>(dy), static_cast<const T*>(x), static_cast<const T*>(weight), mean, rstd,
+          static_cast<T*>(dx), pw, db ? pb : nullptr, (int)rows, (int)cols);
+    });
+    int rc = check_launch("layernorm_bwd_generic");
+    if (rc) return rc;
   } else {
     LK_DISPATCH_FLOAT(dtype, T, {
       LK_LN_VPT(vpt, VPT, {
@@ -274,7 +362,6 @@ extern "C" int lk_layernorm_bwd(const void* dy, const void* x, const void* weigh
         const int64_t rbytes = cols * (int64_t)sizeof(T);
         const int slots = (int)std::max<int64_t>(2, std::min<int64_t>(3, (96 * 1024) / (2 * rbytes)));
         const int smem = (int)(slots * 2 * rbytes);
-        LK_REQUIRE(smem <= 200 * 1024, LK_UNSUPPORTED, "row too wide for the LayerNorm backward ring");
         LK_CUDA(ensure_smem(reinterpret_cast<const void*>(kern), smem));
         int per_sm = 0;
         LK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));

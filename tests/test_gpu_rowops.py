@@ -356,10 +356,7 @@ def test_norms_wide_rows_vs_torch(cols):
     xf, wf = x.float().requires_grad_(True), w.float().requires_grad_(True)
     (xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-6) * wf).backward(dy.float())
     assert close(xr.grad, xf.grad, 2e-2) and close(wr.grad, wf.grad, 2e-2)
-    if cols > 16384:  # beyond the register LayerNorm: a typed error, not a wrong answer
-        with pytest.raises(Exception):
-            lk.liger_layer_norm(x.clone(), w, b, 1e-6)
-        return
+    # LayerNorm: register/TMA-ring kernels up to 16384 columns, the generic kernels beyond
     xr, wr, br = x.clone().requires_grad_(True), w.clone().requires_grad_(True), b.clone().requires_grad_(True)
     y = lk.liger_layer_norm(xr, wr, br, 1e-6)
     y.backward(dy)
@@ -451,3 +448,48 @@ def test_swiglu_gate_and_down_multipliers(dtype, gm, dm):
     tol = 1e-4 if dtype == torch.float32 else 2e-2
     assert close(c, cf, tol)
     assert close(ar.grad, af.grad, tol) and close(br.grad, bf.grad, tol)
+
+
+@pytest.mark.parametrize("cols,dtype,offset", [(1001, torch.bfloat16, 0), (4096, torch.float16, 1), (77, torch.float32, 3)])
+def test_layernorm_ragged_and_unaligned_vs_torch(cols, dtype, offset):
+    """Hidden sizes that are not a 16-byte multiple and storage offsets that break 16-byte
+    alignment take the generic LayerNorm kernels (Liger's Triton LayerNorm takes any shape)."""
+    rows = 130
+    g = torch.Generator(device="cuda").manual_seed(cols + offset)
+    base = (torch.rand(rows * cols + offset, device="cuda", generator=g) * 2 - 0.5).to(dtype)
+    x = base[offset:].view(rows, cols)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(dtype)
+    b = (torch.rand(cols, device="cuda", generator=g) - 0.5).to(dtype)
+    dbase = (torch.rand(rows * cols + offset, device="cuda", generator=g) * 2 - 1).to(dtype)
+    dy = dbase[offset:].view(rows, cols)
+    xr, wr, br = x.clone().requires_grad_(True), w.clone().requires_grad_(True), b.clone().requires_grad_(True)
+    y = lk.LigerLayerNormFunction.apply(x, wr, br, 1e-6)  # x itself: the storage offset reaches the kernel
+    y.backward(dy)
+    xf, wf, bf = x.float().requires_grad_(True), w.float().requires_grad_(True), b.float().requires_grad_(True)
+    yf = torch.nn.functional.layer_norm(xf, (cols,), wf, bf, eps=1e-6)
+    yf.backward(dy.float())
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    assert close(y, yf, tol)
+    assert close(wr.grad, wf.grad, tol) and close(br.grad, bf.grad, tol)
+
+
+
+@pytest.mark.parametrize("kind", ["swiglu", "geglu"])
+def test_glu_unaligned_views_vs_torch(kind):
+    """Buffers whose storage offset breaks 16-byte alignment take the scalar loop of the GLU
+    kernels (Liger accepts any contiguous tensor)."""
+    n = 300 * 1001
+    g = torch.Generator(device="cuda").manual_seed(9)
+    ab = torch.randn(n + 3, device="cuda", generator=g).to(torch.bfloat16)
+    bb = torch.randn(n + 5, device="cuda", generator=g).to(torch.bfloat16)
+    a, b = ab[3:].view(300, 1001), bb[5:].view(300, 1001)
+    dc = torch.randn(300, 1001, device="cuda", generator=g).to(torch.bfloat16)
+    f = lk.LigerSiLUMulFunction if kind == "swiglu" else lk.LigerGELUMulFunction
+    ar, br = ab.clone()[3:].view(300, 1001).requires_grad_(True), bb.clone()[5:].view(300, 1001).requires_grad_(True)
+    c = f.apply(ar, br)
+    c.backward(dc)
+    af, bf = a.float().requires_grad_(True), b.float().requires_grad_(True)
+    act = torch.nn.functional.silu(af) if kind == "swiglu" else torch.nn.functional.gelu(af, approximate="tanh")
+    cf = act.to(torch.bfloat16).float() * bf
+    cf.backward(dc.float())
+    assert close(c, cf, 2e-2) and close(ar.grad, af.grad, 2e-2) and close(br.grad, bf.grad, 2e-2)
