@@ -275,3 +275,21 @@ def test_ce_class_weights(impl, reduction, kw, monkeypatch):
     assert ok, err
     ok, err = rel_close(x.grad.float().cpu().numpy(), rg, 2e-2)
     assert ok, err
+
+
+def test_ce_unaligned_logits_vs_oracle():
+    """Logits at a storage offset that breaks 16-byte alignment: the ring kernel declines, the
+    block kernel's scalar path takes the rows."""
+    rows, v = 64, 3001
+    g = torch.Generator(device="cuda").manual_seed(17)
+    base = (torch.randn(rows * v + 1, device="cuda", generator=g) * 3).to(torch.bfloat16)
+    z = base[1:].view(rows, v)
+    t = torch.randint(0, v, (rows,), device="cuda", generator=g)
+    t[::5] = -100
+    x = base.clone()[1:].view(rows, v).requires_grad_(True)
+    loss = lk.LigerCrossEntropyLoss(label_smoothing=0.1)(x, t)
+    loss.backward()
+    rl, _, _, rg = liger_ref.ce(z.double().cpu().numpy(), t.cpu().numpy(), label_smoothing=0.1)
+    assert rel_close(loss.item(), rl, 2e-2)[0]
+    ok, err = rel_close(x.grad.float().cpu().numpy(), rg, 2e-2)
+    assert ok, err

@@ -493,3 +493,23 @@ def test_glu_unaligned_views_vs_torch(kind):
     cf = act.to(torch.bfloat16).float() * bf
     cf.backward(dc.float())
     assert close(c, cf, 2e-2) and close(ar.grad, af.grad, 2e-2) and close(br.grad, bf.grad, 2e-2)
+
+
+@pytest.mark.parametrize("mode", ["llama", "gemma"])
+def test_rmsnorm_unaligned_views_vs_torch(mode):
+    """A storage offset that breaks 16-byte alignment falls through to the generic RMSNorm kernels."""
+    rows, cols = 64, 2048
+    g = torch.Generator(device="cuda").manual_seed(21)
+    xb = torch.randn(rows * cols + 1, device="cuda", generator=g).to(torch.bfloat16)
+    dyb = torch.randn(rows * cols + 1, device="cuda", generator=g).to(torch.bfloat16)
+    x, dy = xb[1:].view(rows, cols), dyb[1:].view(rows, cols)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(torch.bfloat16)
+    off = 0.0 if mode == "llama" else 1.0
+    xr = xb.clone()[1:].view(rows, cols).requires_grad_(True)
+    wr = w.clone().requires_grad_(True)
+    y = lk.liger_rms_norm(xr, wr, 1e-6, off, mode, False)
+    y.backward(dy)
+    xf, wf = x.float().requires_grad_(True), w.float().requires_grad_(True)
+    yf = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-6) * (off + wf)
+    yf.backward(dy.float())
+    assert close(y, yf, 2e-2) and close(xr.grad, xf.grad, 2e-2) and close(wr.grad, wf.grad, 2e-2)
