@@ -44,6 +44,7 @@ using ring::Pairs;
 
 struct Smem {
   float4 red[2][NC];
+  float wz[2][NC];   // class weights + smoothing, FLCE finalize: per-warp sum_c w_c z_c after pass 2
   float2 am[2][NC];  // per-warp argmax (value, index bits) for token accuracy / predicted tokens
   float zt[2];
 };
@@ -64,7 +65,9 @@ __device__ __forceinline__ float2 capped(float2 z, float cap, float inv_cap) {
 // (max, sumexp, sum) partials and the softcapped, rounded logits, so the statistics pass is a
 // combine of ~V/256 partials and only the gradient pass streams the row (one read + one
 // write per logit, rowfuse/flce.py:155-157).
-template <typename T, bool CAP, bool LS, bool PART>
+// W: class weights together with label smoothing (compile-time, so the common variants carry
+// no per-element weight branch).
+template <typename T, bool CAP, bool LS, bool PART, bool W>
 __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int stages) {
   using P = Pairs<T>;
   constexpr int NP = P::NP;
@@ -118,6 +121,9 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   const int npc32 = (int)npc;
   const int tail_nvec = (int)((row_bytes - (npc - 1) * (int64_t)PIECE) / 16);
   const int v0 = warp * VPW + lane;
+  // class weights with label smoothing: the smoothing sum is sum_c w_c z_c and the gradient
+  // gains -eps w_c per column (weights by global column; runtime-uniform branch)
+  const float* wcol = W ? a.class_weight + a.col_offset : nullptr;
   for (int64_t i = 0; i < n_local; ++i) {
     const int64_t row = b + i * G;
     T* xr = static_cast<T*>(a.x) + row * a.ld;
@@ -190,12 +196,14 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         const float mn = fmaxf(m, lmax);
         const float2 nmb = make_float2(-mn * L2E, -mn * L2E);
         float2 acc = make_float2(0.f, 0.f);
+        const float* wp = W ? wcol + (int64_t)j * (PIECE / sizeof(T)) + v0 * NV : nullptr;
 #pragma unroll
         for (int k = 0; k < KPL; ++k)
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             acc = __fadd2_rn(acc, ex2(__ffma2_rn(z[k][e], l2e2, nmb)));
-            if (LS) sz2 = __fadd2_rn(sz2, z[k][e]);
+            if constexpr (W) sz2 = __ffma2_rn(z[k][e], __ldg(reinterpret_cast<const float2*>(wp + 32 * k * NV + 2 * e)), sz2);
+            else if (LS) sz2 = __fadd2_rn(sz2, z[k][e]);
           }
         se = se * ex2((m - mn) * L2E) + (acc.x + acc.y);  // m = -inf: ex2(-inf) = 0, se = 0
         m = mn;
@@ -226,13 +234,15 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
         const float mn = fmaxf(m, lmax);
         const float2 nmb = make_float2(-mn * L2E, -mn * L2E);
         float2 acc = make_float2(0.f, 0.f);
+        const float* wp = W ? wcol + (int64_t)j * (PIECE / sizeof(T)) + v0 * NV : nullptr;
 #pragma unroll
         for (int k = 0; k < KPL; ++k) {
           if (v0 + 32 * k >= nvec) continue;
 #pragma unroll
           for (int e = 0; e < NP; ++e) {
             acc = __fadd2_rn(acc, ex2(__ffma2_rn(z[k][e], l2e2, nmb)));
-            if (LS) sz2 = __fadd2_rn(sz2, z[k][e]);
+            if constexpr (W) sz2 = __ffma2_rn(z[k][e], __ldg(reinterpret_cast<const float2*>(wp + 32 * k * NV + 2 * e)), sz2);
+            else if (LS) sz2 = __fadd2_rn(sz2, z[k][e]);
           }
         }
         se = (m == -INFINITY ? 0.f : se * ex2((m - mn) * L2E)) + (acc.x + acc.y);
@@ -280,7 +290,10 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     const float lse = m + logf(se);
     // reduction (MEAN), token scaling and class weights folded into per-row coefficients
     const RowCoef rcf = ce_row_coefs<T>(a, lse, zy, sz, y);
-    if (tid == 0) {  // LK/ops/cross_entropy.py:259-289
+    // FLCE finalize with class weights + smoothing: the epilogue partials carry the unweighted
+    // sum, so sum_c w_c z_c is accumulated in pass 2 and the loss written after it
+    constexpr bool late_loss = PART && W;
+    if (tid == 0 && !late_loss) {  // LK/ops/cross_entropy.py:259-289
       if (a.loss_rows) a.loss_rows[row] = rcf.loss;
       if (a.z_loss_rows) a.z_loss_rows[row] = rcf.zl;
     }
@@ -291,6 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     const float2 coef2 = make_float2(coef, coef);
     const float2 neps2 = make_float2(rcf.ceps, rcf.ceps);
     const float hit_s = rcf.chit;
+    float2 wz2 = make_float2(0.f, 0.f);  // late_loss: sum_c w_c z_c
     for (int j = 0; j < npc32; ++j, cur.next()) {
       const int s = cur.s;
       ring::wait(full_a + 8u * (uint32_t)s, cur.phase);
@@ -303,6 +317,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       if (lane == 0) ring::arrive(empty_a + 8u * (uint32_t)s);
       const int64_t col0 = (int64_t)j * (PIECE / sizeof(T));
       T* xp = xr + col0 + (int64_t)v0 * NV;  // this lane's first vector of the piece
+      const float* wp = W ? wcol + col0 + (int64_t)v0 * NV : nullptr;
       // target column relative to that vector, as a 32-bit value (far away when not in the piece)
       const int64_t trel64 = yl - col0 - (int64_t)v0 * NV;
       const int trel = trel64 >= -(int64_t)(PIECE / sizeof(T)) && trel64 < (int64_t)(PIECE / sizeof(T)) ? (int)trel64 : INT_MIN / 2;
@@ -324,7 +339,14 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
               }
               dc = __ffma2_rn(__fmul2_rn(t, t), make_float2(-1.f, -1.f), make_float2(1.f, 1.f));  // 1 - t^2
             }
-            float2 g = __ffma2_rn(ex2(__ffma2_rn(zz, l2e2, nmb)), coef2, neps2);
+            float2 g;
+            if constexpr (W) {
+              const float2 wv = __ldg(reinterpret_cast<const float2*>(wp + 32 * k * NV + 2 * e));
+              g = __ffma2_rn(ex2(__ffma2_rn(zz, l2e2, nmb)), coef2, __fmul2_rn(neps2, wv));
+              if (late_loss) wz2 = __ffma2_rn(zz, wv, wz2);
+            } else {
+              g = __ffma2_rn(ex2(__ffma2_rn(zz, l2e2, nmb)), coef2, neps2);
+            }
             if (CAP) g = __fmul2_rn(g, dc);
             z[e] = g;
           }
@@ -350,10 +372,23 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
               }
               dct = 1.f - t * t;
             }
-            const float gt = (ex2(fmaf(zt, L2E, nmb.x)) * coef + neps2.x - hit_s) * dct;
+            const float ce = W ? neps2.x * wcol[yl] : neps2.x;
+            const float gt = (ex2(fmaf(zt, L2E, nmb.x)) * coef + ce - hit_s) * dct;
             xr[yl] = from_f<T>(gt);
           }
         }
+      }
+    }
+    if constexpr (late_loss) {  // one more consumer barrier per row
+      float wz = warp_sum(wz2.x + wz2.y);
+      if (lane == 0) sh->wz[par][warp] = wz;
+      ring::consumers_sync(1, NC * 32);
+      if (tid == 0) {
+        float t = 0.f;
+        for (int c = 0; c < NC; ++c) t += sh->wz[par][c];  // fixed warp order
+        const RowCoef lc = ce_row_coefs<T>(a, lse, zy, t, y);
+        if (a.loss_rows) a.loss_rows[row] = lc.loss;
+        if (a.z_loss_rows) a.z_loss_rows[row] = lc.zl;
       }
     }
   }
@@ -366,7 +401,8 @@ int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
   const bool part = a.partials != nullptr || a.row_stats != nullptr;  // FLCE / vocab-parallel finalize
   if (a.rows <= 0 || (part && !a.input_capped) || (!part && a.input_capped)) return LK_UNSUPPORTED;
   if (a.row_stats && (a.correct_rows || a.pred_rows)) return LK_UNSUPPORTED;
-  if (a.class_weight && a.label_smoothing > 0.f) return LK_UNSUPPORTED;  // per-column weights: ce_rows_kernel
+  // class weights + smoothing in the FLCE finalize need pass 2 for the weighted sum
+  if (part && a.class_weight && a.label_smoothing > 0.f && (!a.compute_grad || a.row_stats)) return LK_UNSUPPORTED;
   const int64_t esz = dtype == LK_F32 ? 4 : 2;
   if ((a.n_cols * esz) % 16 || (a.ld * esz) % 16 || (reinterpret_cast<uintptr_t>(a.x) & 15)) return LK_UNSUPPORTED;
   const int stages = 6;  // 192 KB in flight per SM
@@ -378,17 +414,22 @@ int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st) {
     kern<<<grid, cer::THREADS, smem, st>>>(a, stages);
     return check_launch("ce_ring_kernel");
   };
+  const bool wls = ls && a.class_weight;
   LK_DISPATCH_FLOAT(dtype, T, {
     if (part) {
-      if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, true>);
-      if (cap) return go(cer::ce_ring_kernel<T, true, false, true>);
-      if (ls) return go(cer::ce_ring_kernel<T, false, true, true>);
-      return go(cer::ce_ring_kernel<T, false, false, true>);
+      if (wls) return cap ? go(cer::ce_ring_kernel<T, true, true, true, true>)
+                          : go(cer::ce_ring_kernel<T, false, true, true, true>);
+      if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, true, false>);
+      if (cap) return go(cer::ce_ring_kernel<T, true, false, true, false>);
+      if (ls) return go(cer::ce_ring_kernel<T, false, true, true, false>);
+      return go(cer::ce_ring_kernel<T, false, false, true, false>);
     }
-    if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, false>);
-    if (cap) return go(cer::ce_ring_kernel<T, true, false, false>);
-    if (ls) return go(cer::ce_ring_kernel<T, false, true, false>);
-    return go(cer::ce_ring_kernel<T, false, false, false>);
+    if (wls) return cap ? go(cer::ce_ring_kernel<T, true, true, false, true>)
+                        : go(cer::ce_ring_kernel<T, false, true, false, true>);
+    if (cap && ls) return go(cer::ce_ring_kernel<T, true, true, false, false>);
+    if (cap) return go(cer::ce_ring_kernel<T, true, false, false, false>);
+    if (ls) return go(cer::ce_ring_kernel<T, false, true, false, false>);
+    return go(cer::ce_ring_kernel<T, false, false, false, false>);
   });
   return LK_OK;
 }
