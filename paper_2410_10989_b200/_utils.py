@@ -44,7 +44,9 @@ def ptr(t: torch.Tensor | None) -> int | None:
 
 
 def stream_of(t: torch.Tensor) -> int:
-    return torch.cuda.current_stream(t.device).cuda_stream
+    # raw cudaStream_t of the tensor's device's current stream (the C call behind
+    # torch.cuda.current_stream(dev).cuda_stream, without building a Stream object)
+    return torch._C._cuda_getCurrentRawStream(t.get_device())
 
 
 def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
@@ -62,9 +64,12 @@ def device_guard(fn):
 
     @functools.wraps(fn)
     def wrapped(*args, **kwargs):
-        for a in list(args) + list(kwargs.values()):
+        for a in args if not kwargs else list(args) + list(kwargs.values()):
             if isinstance(a, torch.Tensor) and a.is_cuda:
-                with torch.cuda.device(a.device):
+                dev = a.get_device()
+                if dev == torch.cuda.current_device():  # common case: no device switch
+                    return fn(*args, **kwargs)
+                with torch.cuda.device(dev):
                     return fn(*args, **kwargs)
         return fn(*args, **kwargs)
 
