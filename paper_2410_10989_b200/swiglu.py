@@ -20,8 +20,11 @@ def _fwd(fn_name, a, b, *extra):
     require_cuda(a, b)
     if a.shape != b.shape or a.dtype != b.dtype:
         raise errors.ShapeMismatch("gate and up halves must match in shape and dtype (rowfuse/ops.py:99-106)")
-    a = a.contiguous()
-    b = b.contiguous()
+    # fresh view objects (same storage): the backward writes da/db into them and returns them,
+    # and autograd can then take them as leaf .grad without a defensive copy (as Liger's
+    # a.view(-1, n) does)
+    a = a.contiguous().view(a.shape)
+    b = b.contiguous().view(b.shape)
     c = torch.empty_like(a)
     check(getattr(lib(), fn_name)(a.data_ptr(), b.data_ptr(), c.data_ptr(), a.numel(), *extra, dtype_code(a),
                                   stream_of(a)))
