@@ -43,10 +43,15 @@ def ptr(t: torch.Tensor | None) -> int | None:
     return None if t is None else t.data_ptr()
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_of(t: torch.Tensor) -> int:
     # raw cudaStream_t of the tensor's device's current stream (the C call behind
     # torch.cuda.current_stream(dev).cuda_stream, without building a Stream object)
-    return torch._C._cuda_getCurrentRawStream(t.get_device())
+    if _raw_stream is not None:
+        return _raw_stream(t.get_device())
+    return torch.cuda.current_stream(t.device).cuda_stream
 
 
 def workspace(nbytes: int, device: torch.device) -> torch.Tensor:
