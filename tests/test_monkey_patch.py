@@ -186,3 +186,22 @@ def test_patched_llama_num_items_and_accuracy():
         torch.testing.assert_close(scaled, base / 2, rtol=1e-5, atol=1e-6)
         out = model(input_ids=ids, labels=ids, return_token_accuracy=True)
         assert out.token_accuracy is not None and 0.0 <= float(out.token_accuracy) <= 1.0
+
+
+@pytest.mark.gpu
+def test_patched_llama_cross_entropy_path_matches_stock():
+    """cross_entropy=True: the stock HF loss_function runs with nn.functional.cross_entropy
+    swapped for the library's CE (materialised logits)."""
+    dev = torch.device("cuda")
+    ref = _tiny("llama", torch.float32, dev).train()
+    fused = copy.deepcopy(ref)
+    ids = torch.randint(0, 1024, (2, 80), device=dev)
+    with restored("llama"):
+        out_r = ref(input_ids=ids, labels=ids)
+        out_r.loss.backward()
+        mp.apply_liger_kernel_to_llama(cross_entropy=True, fused_linear_cross_entropy=False, model=fused)
+        out_f = fused(input_ids=ids, labels=ids)
+        assert out_f.logits is not None
+        out_f.loss.backward()
+    assert abs(out_f.loss.item() - out_r.loss.item()) <= 1e-4 * abs(out_r.loss.item())
+    assert _grad_gap(ref, fused) <= 2e-3
