@@ -8,6 +8,7 @@
 #include <string>
 #include <algorithm>
 #include <cmath>
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 #include <type_traits>
@@ -55,12 +56,15 @@ inline int env_int(const char* name, int dflt) {  // tuning knobs read per call
 }
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
-inline int sm_count() {
-  static int n = -1;
-  if (n < 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
+inline int sm_count() {  // of the current device; cached per device, thread-safe
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
     if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
