@@ -232,6 +232,15 @@ int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* 
                         void* logits_buf, float* loss_rows, void* grad_x_partial_f32,
                         float* grad_w_accum, int accumulate, void* workspace,
                         size_t workspace_bytes, void* stream);
+/* As lk_flce_vp_backward, with the dW shard accumulated either in fp32 (grad_w_dtype = LK_F32)
+ * or in place in the weight dtype (grad_w_dtype = dtype: dtype(acc + dtype(chunk product)),
+ * Liger's accum_dtype=None order, as lk_flce_args.grad_w_accum = LK_ACCUM_WEIGHT_DTYPE). */
+int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                           int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total, int dtype,
+                           int64_t ignore_index, float label_smoothing, float lse_square_scale, float softcap,
+                           int reduction, const int64_t* n_non_ignore, const float* row_stats_global,
+                           void* logits_buf, float* loss_rows, void* grad_x_partial_f32, void* grad_w_accum,
+                           int grad_w_dtype, int accumulate, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- RMSNorm ----------------------------------------------------------- */
 /* rowfuse/ops.py:190-241 and LK/ops/rms_norm.py (forward 58-112, backward 115-210).

@@ -107,6 +107,11 @@ SIGNATURES: dict[str, tuple] = {
         [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_float, c_float,
          c_float, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_int, c_void, c_size, c_void],
     ),
+    "lk_flce_vp_backward_ex": (
+        c_int,
+        [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_float, c_float,
+         c_float, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_int, c_int, c_void, c_size, c_void],
+    ),
     "lk_rmsnorm_fwd": (
         c_int, [c_void, c_void, c_void, c_void, c_i64, c_i64, c_float, c_float, c_int, c_int, c_void]
     ),

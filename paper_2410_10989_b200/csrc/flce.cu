@@ -540,12 +540,12 @@ extern "C" int lk_flce_vp_logits(const void* x, const void* weight_shard, const 
                              tc ? parts : nullptr, nparts, tgt, reinterpret_cast<float4*>(row_stats), st);
 }
 
-extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
                                    int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
                                    int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
                                    float softcap, int reduction, const int64_t* n_non_ignore,
                                    const float* row_stats_global, void* logits_buf, float* loss_rows,
-                                   void* grad_x_partial_f32, float* grad_w_accum, int accumulate, void* workspace,
+                                   void* grad_x_partial_f32, void* grad_w_accum, int grad_w_dtype, int accumulate, void* workspace,
                                    size_t workspace_bytes, void* stream) {
   LK_REQUIRE(rows >= 0 && hidden >= 1 && vocab_local >= 1, LK_SIZE_MISMATCH, "bad sizes");
   if (rows == 0) return LK_OK;
@@ -565,8 +565,15 @@ extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, cons
   xe.kind = EPI_STORE; xe.out_dtype = LK_F32; xe.out = grad_x_partial_f32; xe.ldo = hidden; xe.alpha = 1.f;
   xe.M = rows; xe.N = hidden;
   EpiArgs we{};
-  we.kind = EPI_ACCUM; we.out_dtype = LK_F32; we.acc = grad_w_accum; we.ldacc = hidden;
+  LK_REQUIRE(grad_w_dtype == LK_F32 || grad_w_dtype == dtype, LK_INVALID_ARGUMENT,
+             "grad_w accumulator must be fp32 or the weight dtype");
+  we.kind = EPI_ACCUM; we.ldacc = hidden; we.ldo = hidden; we.alpha = 1.f;
   we.beta = accumulate ? 1 : 0; we.M = vocab_local; we.N = hidden;
+  if (grad_w_dtype == LK_F32) {  // fp32 accumulator
+    we.out_dtype = LK_F32; we.acc = static_cast<float*>(grad_w_accum);
+  } else {  // weight-dtype accumulation in place (Liger accum_dtype=None order; TMA reduce-add)
+    we.out_dtype = dtype; we.acc = nullptr; we.out = grad_w_accum; we.final_out = 0;
+  }
   const bool tc = use_tc_path(dtype, hidden, x, weight_shard, 0) && workspace && workspace_bytes >= 64;
   if (tc) {
     // both GEMMs in one persistent tcgen05 launch, as in the token-local FLCE backward:
@@ -604,6 +611,19 @@ extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, cons
     rc = launch_simt_gemm(A, B, vocab_local, hidden, rows, dtype, we, st);
   }
   return rc;
+}
+
+extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                                   int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
+                                   int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
+                                   float softcap, int reduction, const int64_t* n_non_ignore,
+                                   const float* row_stats_global, void* logits_buf, float* loss_rows,
+                                   void* grad_x_partial_f32, float* grad_w_accum, int accumulate, void* workspace,
+                                   size_t workspace_bytes, void* stream) {
+  return lk_flce_vp_backward_ex(x, weight_shard, target, rows, hidden, vocab_local, vocab_offset, vocab_total, dtype,
+                                ignore_index, label_smoothing, lse_square_scale, softcap, reduction, n_non_ignore,
+                                row_stats_global, logits_buf, loss_rows, grad_x_partial_f32, grad_w_accum, LK_F32,
+                                accumulate, workspace, workspace_bytes, stream);
 }
 
 // ------------------------------------------------------------ GEMM test ----

@@ -62,6 +62,11 @@ __device__ __forceinline__ void epi_elem(const EpiArgs& e, int64_t r, int64_t c,
       store_any(e.out, r * e.ldo + c, e.out_dtype, e.alpha * v);
       break;
     case EPI_ACCUM: {
+      if (!e.acc) {  // accumulate in the output dtype: out = dtype(out + dtype(tile)) (Liger's order)
+        const float t = round_any(v, e.out_dtype);
+        store_any(e.out, r * e.ldo + c, e.out_dtype, e.beta ? load_any(e.out, r * e.ldo + c, e.out_dtype) + t : t);
+        break;
+      }
       float a = e.beta ? e.acc[r * e.ldacc + c] : 0.f;
       a += v;
       if (e.final_out) store_any(e.out, r * e.ldo + c, e.out_dtype, a);

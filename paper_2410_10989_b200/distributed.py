@@ -165,11 +165,11 @@ class CudaVocabOps:
         loss_rows = torch.empty(rows, dtype=torch.float32, device=x.device)
         gx = torch.empty(rows, h, dtype=torch.float32, device=x.device)
         ws = workspace(256, x.device)
-        check(lib().lk_flce_vp_backward(
+        check(lib().lk_flce_vp_backward_ex(
             ptr(x), ptr(w_shard), ptr(t), rows, h, shard.size, shard.offset, shard.total, self.dt, ignore_index,
             float(label_smoothing), float(lse_square_scale), float(softcap or 0.0), _capi.REDUCTIONS[reduction],
-            ptr(n_valid), ptr(stats_g), ptr(buf), ptr(loss_rows), ptr(gx), ptr(gw_acc), int(accumulate), ptr(ws),
-            ws.numel(), stream_of(x)))
+            ptr(n_valid), ptr(stats_g), ptr(buf), ptr(loss_rows), ptr(gx), ptr(gw_acc), dtype_code(gw_acc),
+            int(accumulate), ptr(ws), ws.numel(), stream_of(x)))
         return loss_rows, gx
 
     def count(self, t, vocab, ignore_index):
@@ -190,16 +190,24 @@ def vocab_parallel_flce(
     reduction: str = "mean",
     chunk_rows: int = 2048,
     ops=None,
+    accum_dtype: Optional[torch.dtype] = None,
 ):
     """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
 
     Every rank holds all rows of x and the targets; only W is sharded by vocab rows.
+    `accum_dtype` follows Liger's FLCE option: None accumulates the dW shard across chunks
+    in the weight dtype (16-bit weights), torch.float32 in an fp32 buffer.
     """
     ops = ops or CudaVocabOps(x.dtype, x.device)
     t = target.reshape(-1).to(torch.int64).contiguous()
     bt, h = x.shape
     n_valid = ops.count(t, shard.total, ignore_index)
-    acc_dtype = torch.float64 if w_shard.dtype == torch.float64 else torch.float32  # fp32 for the kernels
+    if w_shard.dtype == torch.float64:
+        acc_dtype = torch.float64
+    elif accum_dtype is None and w_shard.dtype in (torch.bfloat16, torch.float16) and isinstance(ops, CudaVocabOps):
+        acc_dtype = w_shard.dtype  # in-place weight-dtype accumulation (lk_flce_vp_backward_ex)
+    else:
+        acc_dtype = torch.float32
     gw_acc = torch.zeros(shard.size, h, dtype=acc_dtype, device=x.device)
     gx = torch.empty(bt, h, dtype=x.dtype, device=x.device)
     loss_rows = torch.empty(bt, dtype=torch.float32, device=x.device)
