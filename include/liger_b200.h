@@ -192,8 +192,12 @@ typedef struct {
   /* Liger use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139, 187-206): each
    * row's loss, z-loss and gradient scaled by its detached target probability. */
   int use_token_scaling;
-  /* Liger ce_weight: [vocab] fp32 class weights or NULL (no label smoothing with weights). */
+  /* Liger ce_weight: [vocab] fp32 class weights or NULL. */
   const float* ce_weight;
+  /* Token-sharded mode with ce_weight: device fp32 holding the GLOBAL sum of the valid
+   * targets' weights (the weighted MEAN denominator, all-reduced by the caller); NULL =
+   * local sum. */
+  const float* mean_weight_sum;
 } lk_flce_args;
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };

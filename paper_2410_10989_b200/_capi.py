@@ -69,6 +69,7 @@ class FlceArgs(C.Structure):
         ("grad_w_slice_events", c_void),
         ("use_token_scaling", c_int),
         ("ce_weight", c_void),
+        ("mean_weight_sum", c_void),
     ]
 
 

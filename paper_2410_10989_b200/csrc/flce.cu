@@ -324,7 +324,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   if (rc) return rc;
   if (a->target_stats)
     LK_CUDA(cudaMemcpyAsync(a->target_stats, counts, 2 * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
-  LK_REQUIRE(!a->ce_weight || !a->mean_count, LK_UNSUPPORTED, "ce_weight in the token-sharded mode");
+  LK_REQUIRE(!a->ce_weight || !a->mean_count || a->mean_weight_sum || a->reduction != LK_REDUCTION_MEAN,
+             LK_INVALID_ARGUMENT, "token-sharded MEAN with ce_weight needs the global weight sum (mean_weight_sum)");
   const bool wls = a->ce_weight && a->label_smoothing > 0.f;
   if (a->ce_weight && BT > 0) {  // MEAN denominator: sum of the valid targets' weights (after counts)
     rc = launch_weight_sum(a->target, BT, a->ignore_index, a->ce_weight, reinterpret_cast<float*>(counts + 2), st,
@@ -380,7 +381,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     ce.correct_rows = a->token_correct_rows ? a->token_correct_rows + lo : nullptr;
     ce.token_scaling = a->use_token_scaling;
     ce.class_weight = a->ce_weight;
-    ce.sum_valid_weight = a->ce_weight ? reinterpret_cast<const float*>(counts + 2) : nullptr;
+    ce.sum_valid_weight = !a->ce_weight ? nullptr
+                          : a->mean_weight_sum ? a->mean_weight_sum : reinterpret_cast<const float*>(counts + 2);
     ce.weight_total = wls ? reinterpret_cast<const float*>(counts + 3) : nullptr;
     ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }

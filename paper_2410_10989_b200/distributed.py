@@ -101,6 +101,14 @@ def token_sharded_flce(
     if reduction == "mean":
         dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     kw = dict(kw, ignore_index=ignore_index, reduction=reduction)
+    cw = kw.get("ce_weight")
+    if cw is not None and reduction == "mean" and local_fn is _local_flce_cuda:
+        # weighted MEAN: the denominator is the GLOBAL sum of the valid targets' weights
+        valid = (t != ignore_index) & (t >= 0) & (t < cw.numel())
+        wsum = cw.detach().to(device=t.device, dtype=torch.float32)[t.clamp(0, cw.numel() - 1)]
+        wsum = (wsum * valid).sum(dtype=torch.float32).reshape(1)
+        dist.all_reduce(wsum, op=dist.ReduceOp.SUM, group=group)
+        kw["mean_weight_sum"] = wsum
     if overlap:
         loss, gx, gw = _allreduce_grad_w_overlapped(x_local, weight, t, counts, group, dw_slices, local_fn, kw)
     else:

@@ -71,6 +71,7 @@ def fused_linear_cross_entropy_forward(
     compute_grad_weight: Optional[bool] = None,
     mean_count: Optional[torch.Tensor] = None,
     grad_w_slice_events=None,
+    mean_weight_sum: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -152,6 +153,7 @@ def fused_linear_cross_entropy_forward(
         mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
         token_correct_rows=ptr(correct), predicted_tokens=ptr(pred), use_token_scaling=int(bool(use_token_scaling)),
         ce_weight=ptr(cw),
+        mean_weight_sum=ptr(mean_weight_sum) if mean_weight_sum is not None else None,
     )
     ev_arr = None
     if grad_w_slice_events:
@@ -163,6 +165,8 @@ def fused_linear_cross_entropy_forward(
         args.grad_w_slice_events = _capi.C.cast(ev_arr, _capi.C.c_void_p)
     if mean_count is not None and (mean_count.dtype != torch.int64 or not mean_count.is_cuda):
         raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")
+    if mean_weight_sum is not None and (mean_weight_sum.dtype != torch.float32 or not mean_weight_sum.is_cuda):
+        raise errors.ShapeMismatch("mean_weight_sum must be a CUDA float32 tensor")
     check(L.lk_flce_forward_backward(_capi.C.byref(args)))
     del ws
     raise_if_out_of_range(stats, v)

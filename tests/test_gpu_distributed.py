@@ -53,7 +53,12 @@ def _worker(rank, port, mode, kw, out):
         xb = torch.tensor(x, dtype=torch.bfloat16, device=dev)
         wb = torch.tensor(w, dtype=torch.bfloat16, device=dev)
         tb = torch.tensor(t, device=dev)
-        ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(xb.double().cpu().numpy(), wb.double().cpu().numpy(), t, **kw)
+        kw = dict(kw)
+        ref_kw = dict(kw)
+        if "ce_weight" in kw:  # numpy class weights: the oracle's `weight`, the library's ce_weight tensor
+            ref_kw["weight"] = ref_kw.pop("ce_weight")
+            kw["ce_weight"] = torch.tensor(kw["ce_weight"], dtype=torch.float32, device=dev)
+        ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(xb.double().cpu().numpy(), wb.double().cpu().numpy(), t, **ref_kw)
         if mode == "token":
             lo, hi = shard_rows(len(t), rank, WORLD)
             loss, gx, gw = token_sharded_flce(xb[lo:hi].contiguous(), wb, tb[lo:hi], chunk_rows=128, **kw)
@@ -85,7 +90,11 @@ def _run(mode, kw):
     assert dict(out) == {0: "ok", 1: "ok"}, dict(out)
 
 
-@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0)])
+_CW = np.random.default_rng(5).random(3000) + 0.2
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(ce_weight=_CW),
+                                dict(ce_weight=_CW, label_smoothing=0.1)])
 def test_token_sharded_cuda_world2(kw):
     _run("token", kw)
 
