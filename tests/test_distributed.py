@@ -35,12 +35,14 @@ def free_port():
     return p
 
 
-def problem(bt=24, h=6, v=11, seed=0):
+def problem(bt=24, h=6, v=11, seed=0, ignore_first_half=False):
     rng = np.random.default_rng(seed)
     x = rng.uniform(-1, 1, (bt, h))
     w = rng.uniform(-1, 1, (v, h)) * 1.5
     t = rng.integers(0, v, bt)
     t[rng.random(bt) < 0.25] = -100
+    if ignore_first_half:
+        t[: bt // 2] = -100  # at world 2, rank 0's whole token shard is ignore_index
     return x, w, t
 
 
@@ -106,22 +108,22 @@ class OracleVocabOps:
 
 
 # ------------------------------------------------------------------ workers
-def _worker(rank, port, mode, kw, out):
+def _worker(rank, port, mode, kw, out, world=WORLD, prob=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        x, w, t = problem()
+        x, w, t = problem(**(prob or {}))
         ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, **kw)
         if mode == "token":
-            lo, hi = shard_rows(len(t), rank, WORLD)
+            lo, hi = shard_rows(len(t), rank, world)
             loss, gx, gw = token_sharded_flce(torch.tensor(x[lo:hi]), torch.tensor(w), torch.tensor(t[lo:hi]),
                                               count_fn=oracle_count, local_fn=oracle_local_flce, **kw)
             np.testing.assert_allclose(loss.item(), ref_loss, rtol=1e-12)
             np.testing.assert_allclose(gx.numpy(), rgx[lo:hi], rtol=1e-10, atol=1e-14)
             np.testing.assert_allclose(gw.numpy(), rgw, rtol=1e-10, atol=1e-14)
         else:
-            sh = vocab_shard(w.shape[0], rank, WORLD)
+            sh = vocab_shard(w.shape[0], rank, world)
             loss, gx, gw = vocab_parallel_flce(torch.tensor(x), torch.tensor(w[sh.offset:sh.offset + sh.size]),
                                                torch.tensor(t), sh, chunk_rows=7, ops=OracleVocabOps(), **kw)
             np.testing.assert_allclose(loss.item(), ref_loss, rtol=1e-6)  # per-row losses are kept in fp32
@@ -134,12 +136,12 @@ def _worker(rank, port, mode, kw, out):
         dist.destroy_process_group()
 
 
-def run_world(mode, kw):
+def run_world(mode, kw, world=WORLD, prob=None):
     port = free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(port, mode, kw, out), nprocs=WORLD, join=True)
-    assert dict(out) == {0: "ok", 1: "ok"}, dict(out)
+    mp.spawn(_worker, args=(port, mode, kw, out, world, prob), nprocs=world, join=True)
+    assert dict(out) == {r: "ok" for r in range(world)}, dict(out)
 
 
 def test_shard_rows_cover_exactly():
@@ -159,3 +161,16 @@ def test_token_sharded_world2_matches_single_process(kw):
 @pytest.mark.parametrize("kw", [dict(), dict(softcap=3.0, label_smoothing=0.1), dict(lse_square_scale=1e-3)])
 def test_vocab_parallel_world2_matches_single_process(kw):
     run_world("vocab", kw)
+
+
+@pytest.mark.parametrize("mode", ["token", "vocab"])
+def test_world3_ragged_shards(mode):
+    """Uneven splits on both axes: 25 tokens -> 9/8/8 rows, 11 classes -> 4/4/3 vocab columns."""
+    run_world(mode, dict(label_smoothing=0.05), world=3, prob=dict(bt=25))
+
+
+@pytest.mark.parametrize("mode", ["token", "vocab"])
+def test_world2_rank_with_only_ignored_tokens(mode):
+    """A rank whose token shard is all ignore_index contributes zero loss/dX but still joins
+    every collective; the mean denominator is the global valid count."""
+    run_world(mode, dict(), prob=dict(ignore_first_half=True))
