@@ -49,11 +49,13 @@ def _worker(rank, port, mode, kw, out):
         from tests.conftest import rel_close
 
         dev = torch.device("cuda:0")
+        kw = dict(kw)
         x, w, t = _problem()
+        if kw.pop("_ignore_first_half", False):
+            t[: len(t) // 2] = -100  # rank 0's whole token shard is ignore_index
         xb = torch.tensor(x, dtype=torch.bfloat16, device=dev)
         wb = torch.tensor(w, dtype=torch.bfloat16, device=dev)
         tb = torch.tensor(t, device=dev)
-        kw = dict(kw)
         ref_kw = dict(kw)
         if "ce_weight" in kw:  # numpy class weights: the oracle's `weight`, the library's ce_weight tensor
             ref_kw["weight"] = ref_kw.pop("ce_weight")
@@ -94,11 +96,12 @@ _CW = np.random.default_rng(5).random(3000) + 0.2
 
 
 @pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(ce_weight=_CW),
-                                dict(ce_weight=_CW, label_smoothing=0.1)])
+                                dict(ce_weight=_CW, label_smoothing=0.1), dict(_ignore_first_half=True)])
 def test_token_sharded_cuda_world2(kw):
     _run("token", kw)
 
 
-@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(lse_square_scale=1e-4)])
+@pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(lse_square_scale=1e-4),
+                                dict(_ignore_first_half=True)])
 def test_vocab_parallel_cuda_world2(kw):
     _run("vocab", kw)
