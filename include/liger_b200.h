@@ -84,6 +84,23 @@ void lk_profile_enable(int on);
 int lk_profile_collect(double* ms4, int64_t* launches4);
 int64_t lk_launch_count(void);
 
+/* TEST-ONLY path selection.  The library runs one product path per shape; the kernels it
+ * replaced stay selectable here so the parity tests can run each against the others.  Knobs
+ * are process-wide and default to 0 = the product path; nothing reads the environment.
+ *   LK_PATH_CTA_GROUP          0 = CTA-pair tcgen05 GEMM, 1 = single-CTA GEMM
+ *   LK_PATH_FLCE_FINALIZE      0 = TMA-ring finalize, 1 = one CTA per row (ce_rows_kernel)
+ *   LK_PATH_FLCE_SEPARATE_CAST 0 = fp32 dW accumulator folded into the last chunk's epilogue,
+ *                              1 = separate cast kernel after the loop
+ *   LK_PATH_CE_IMPL            0 = TMA-ring CE, 1 = one CTA per row
+ *   LK_PATH_NORM_IMPL          0 = CTA-per-row RMSNorm, 1 = warp per row, 2 = generic, 3 = TMA ring
+ * Returns the previous value, or -1 for an unknown knob / value. */
+#define LK_PATH_CTA_GROUP 0
+#define LK_PATH_FLCE_FINALIZE 1
+#define LK_PATH_FLCE_SEPARATE_CAST 2
+#define LK_PATH_CE_IMPL 3
+#define LK_PATH_NORM_IMPL 4
+int lk_test_select_path(int knob, int value);
+
 /* ---- cross entropy (standalone) ---------------------------------------- */
 /*
  * Replaces rowfuse.ops.cross_entropy (rowfuse/ops.py:502-560) and
@@ -182,11 +199,13 @@ typedef struct {
    * NULL = not computed (the epilogue then skips the argmax search). */
   float* token_correct_rows;  /* [BT] fp32 or NULL */
   int64_t* predicted_tokens;  /* [BT] or NULL      */
-  /* Token-sharded overlap: when > 1 (tcgen05 path, at most 16), the last
-   * chunk's grad_w GEMM runs as this many launches over contiguous vocab-row slices and
-   * grad_w_slice_events[s] (cudaEvent_t, created by the caller) is recorded on `stream` as
-   * soon as rows [s*V/S, (s+1)*V/S) (rounded to 256) of grad_w are final, so the caller can
-   * all-reduce slice s while later slices are still being computed. */
+  /* Token-sharded overlap: grad_w_slice_events[0 .. grad_w_slices) are
+   * cudaEvents created by the caller; slice s = grad_w rows [s*R, min(V, (s+1)*R)) with
+   * R = round_up(ceil(V/S), 256).  Contract: event s is recorded on `stream` after slice s of
+   * grad_w is final, on EVERY successful path.  On the tcgen05 path with
+   * 2 <= S <= LK_MAX_GRAD_W_SLICES the last chunk's grad_w GEMM runs as S launches and event s
+   * follows launch s (so the caller all-reduces slice s while later slices compute); on any
+   * other path (SIMT/fp32, BT == 0, other S) every event is recorded after all of grad_w. */
   int grad_w_slices;
   void* const* grad_w_slice_events;
   /* Liger use_token_scaling (LK/ops/fused_linear_cross_entropy.py:109-139, 187-206): each
@@ -202,6 +221,7 @@ typedef struct {
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };
 #define LK_ACCUM_AUTO_MAX_CHUNKS 8
+#define LK_MAX_GRAD_W_SLICES 16
 
 /* B200 chunk policy.  Writes the chunk row count and number of chunks. */
 int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t* chunk_rows,
@@ -245,6 +265,20 @@ int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, const int64_
                            int reduction, const int64_t* n_non_ignore, const float* row_stats_global,
                            void* logits_buf, float* loss_rows, void* grad_x_partial_f32, void* grad_w_accum,
                            int grad_w_dtype, int accumulate, void* workspace, size_t workspace_bytes, void* stream);
+
+/* As lk_flce_vp_backward_ex with the dX partial written in grad_x_dtype (LK_F32, or the input
+ * dtype so the caller all-reduces it in place in 16-bit: half the bytes of the fp32 partial). */
+int lk_flce_vp_backward2(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                         int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total, int dtype,
+                         int64_t ignore_index, float label_smoothing, float lse_square_scale, float softcap,
+                         int reduction, const int64_t* n_non_ignore, const float* row_stats_global,
+                         void* logits_buf, float* loss_rows, void* grad_x_partial, int grad_x_dtype,
+                         void* grad_w_accum, int grad_w_dtype, int accumulate, void* workspace,
+                         size_t workspace_bytes, void* stream);
+/* Combine the all-gathered per-rank row statistics gathered[world][rows][4] into the global
+ * row_stats[rows][4] (max; sumexp rescaled to the global max; sums), folding ranks in rank
+ * order so every rank gets bit-identical statistics. */
+int lk_flce_vp_combine_stats(const float* gathered, int64_t world, int64_t rows, float* row_stats, void* stream);
 
 /* ---- RMSNorm ----------------------------------------------------------- */
 /* rowfuse/ops.py:190-241 and LK/ops/rms_norm.py (forward 58-112, backward 115-210).

@@ -81,6 +81,7 @@ SIGNATURES: dict[str, tuple] = {
     "lk_profile_enable": (None, [c_int]),
     "lk_profile_collect": (c_int, [C.POINTER(C.c_double), c_i64p]),
     "lk_launch_count": (c_i64, []),
+    "lk_test_select_path": (c_int, [c_int, c_int]),
     "lk_cross_entropy_workspace_bytes": (c_size, [c_i64]),
     "lk_cross_entropy_fwd_ex": (c_int, [c_void, c_i64, c_void, c_i64, c_i64, c_int, c_i64, c_float, c_float, c_float,
                                         c_int, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_void, c_void,
@@ -113,6 +114,13 @@ SIGNATURES: dict[str, tuple] = {
         [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_float, c_float,
          c_float, c_int, c_void, c_void, c_void, c_void, c_void, c_void, c_int, c_int, c_void, c_size, c_void],
     ),
+    "lk_flce_vp_backward2": (
+        c_int,
+        [c_void, c_void, c_void, c_i64, c_i64, c_i64, c_i64, c_i64, c_int, c_i64, c_float, c_float,
+         c_float, c_int, c_void, c_void, c_void, c_void, c_void, c_int, c_void, c_int, c_int, c_void, c_size,
+         c_void],
+    ),
+    "lk_flce_vp_combine_stats": (c_int, [c_void, c_i64, c_i64, c_void, c_void]),
     "lk_rmsnorm_fwd": (
         c_int, [c_void, c_void, c_void, c_void, c_i64, c_i64, c_float, c_float, c_int, c_int, c_void]
     ),
@@ -186,3 +194,23 @@ def check(rc: int) -> None:
         return
     msg = load().lk_last_error().decode(errors="replace")
     raise errors.STATUS.get(rc, RuntimeError)(msg)
+
+
+# Test-only path knobs (include/liger_b200.h lk_test_select_path): 0 = the product path.
+PATH_CTA_GROUP, PATH_FLCE_FINALIZE, PATH_FLCE_SEPARATE_CAST, PATH_CE_IMPL, PATH_NORM_IMPL = range(5)
+
+
+class select_path:
+    """Context manager for the parity tests: run a block on an alternative kernel path."""
+
+    def __init__(self, knob: int, value: int):
+        self.knob, self.value = knob, value
+
+    def __enter__(self):
+        self.prev = load().lk_test_select_path(self.knob, self.value)
+        if self.prev < 0:
+            raise ValueError(f"unknown path knob {self.knob} / value {self.value}")
+        return self
+
+    def __exit__(self, *exc):
+        load().lk_test_select_path(self.knob, self.prev)

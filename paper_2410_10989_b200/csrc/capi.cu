@@ -25,6 +25,12 @@ int check_launch(const char* what) {
   return LK_OK;
 }
 
+// ------------------------------------------------ test-only path knobs ----
+static std::atomic<int> g_knobs[5];
+static const int kKnobMax[5] = {1, 1, 1, 1, 3};
+
+int path_knob(int knob) { return (knob >= 0 && knob < 5) ? g_knobs[knob].load(std::memory_order_relaxed) : 0; }
+
 // ---------------------------------------------------------- profiling ----
 struct ProfRec {
   int stage;
@@ -112,4 +118,9 @@ extern "C" int lk_has_tcgen05(void) {
 #else
   return 0;
 #endif
+}
+
+extern "C" int lk_test_select_path(int knob, int value) {
+  if (knob < 0 || knob >= 5 || value < 0 || value > lk::kKnobMax[knob]) return -1;
+  return lk::g_knobs[knob].exchange(value);
 }

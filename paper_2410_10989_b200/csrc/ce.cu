@@ -30,7 +30,7 @@ __global__ void weight_sum_kernel(const int64_t* __restrict__ t, int64_t rows, i
   double acc = 0.0, tot = 0.0;
   for (int64_t i = threadIdx.x; i < rows; i += blockDim.x) {
     const int64_t y = t[i];
-    if (y != ignore_index) acc += (double)w[y];
+    if (y != ignore_index && y >= 0 && y < vocab) acc += (double)w[y];  // invalid targets: flagged, weight 0
   }
   if (total)
     for (int64_t c = threadIdx.x; c < vocab; c += blockDim.x) tot += (double)w[c];
@@ -234,12 +234,9 @@ extern "C" int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* 
   a.correct_rows = correct_rows; a.pred_rows = pred_rows;
   a.class_weight = class_weight; a.sum_valid_weight = class_weight ? wsum : nullptr;
   a.weight_total = wls ? wtot : nullptr;
-  // LK_CE_IMPL = ring (default) | cluster | block (one CTA per row, ce_rows_kernel)
-  const char* impl_env = getenv("LK_CE_IMPL");  // read per call so tests can switch paths
-  const char impl = impl_env ? impl_env[0] : 'r';
-  rc = LK_UNSUPPORTED;
-  if (impl == 'r') rc = launch_ce_ring(a, dtype, st);
-  if (rc == LK_UNSUPPORTED && impl == 'c') rc = launch_ce_cluster(a, dtype, st);
+  // persistent TMA ring; one CTA per row (ce_rows_kernel) for shapes the ring does not take
+  // (and under the LK_PATH_CE_IMPL test knob)
+  rc = path_knob(LK_PATH_CE_IMPL) == 0 ? launch_ce_ring(a, dtype, st) : LK_UNSUPPORTED;
   if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(a, dtype, st);
   if (rc) return rc;
   if (loss_sum) { rc = launch_reduce_sum(loss_rows, rows, loss_sum, st); if (rc) return rc; }
@@ -344,7 +341,37 @@ int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols,
   return check_launch("vp_row_stats_kernel");
 }
 
+// Vocab-parallel statistics combine: gathered[r][row] = rank r's (max, sumexp, sum_logits,
+// target_logit) -> global (M, sum_r s_r exp(m_r - M), sum_r sz_r, sum_r zt_r).  Ranks are
+// folded in rank order, so every rank computes bit-identical statistics from the one
+// all_gather (replaces a MAX and a SUM all-reduce plus the eager rescale between them).
+__global__ void __launch_bounds__(256) vp_combine_stats_kernel(const float4* __restrict__ g, int64_t world,
+                                                              int64_t rows, float4* __restrict__ out) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  float m = -INFINITY;
+  for (int64_t r = 0; r < world; ++r) m = fmaxf(m, g[r * rows + row].x);
+  float s = 0.f, sz = 0.f, zt = 0.f;
+  for (int64_t r = 0; r < world; ++r) {
+    const float4 q = g[r * rows + row];
+    s += q.y * __expf(q.x - m);
+    sz += q.z;
+    zt += q.w;
+  }
+  out[row] = make_float4(m, s, sz, zt);
+}
+
 }  // namespace lk
+
+extern "C" int lk_flce_vp_combine_stats(const float* gathered, int64_t world, int64_t rows, float* row_stats,
+                                        void* stream) {
+  LK_REQUIRE(world >= 1 && rows >= 0, LK_SIZE_MISMATCH, "world >= 1, rows >= 0 required");
+  LK_REQUIRE(rows == 0 || (gathered && row_stats), LK_INVALID_ARGUMENT, "null pointer");
+  if (rows == 0) return LK_OK;
+  lk::vp_combine_stats_kernel<<<(unsigned)((rows + 255) / 256), 256, 0, lk::as_stream(stream)>>>(
+      reinterpret_cast<const float4*>(gathered), world, rows, reinterpret_cast<float4*>(row_stats));
+  return lk::check_launch("vp_combine_stats_kernel");
+}
 
 namespace lk {
 

@@ -77,7 +77,8 @@ __device__ __forceinline__ RowCoef ce_row_coefs(const CeRowArgs& a, float lse, f
   const float ts = a.token_scaling ? round_to<T>(__expf(zy - lse)) : 1.f;
   RowCoef c;
   if (a.class_weight) {
-    const float wy = a.class_weight[y];
+    // out-of-range targets (flagged by the count kernel, raised by the host) weigh 0: no OOB read
+    const float wy = (y >= 0 && y < a.vocab_total) ? a.class_weight[y] : 0.f;
     float s1 = ts;
     if (mean) {
       const float swn = *a.sum_valid_weight;
@@ -317,8 +318,6 @@ __global__ void count_targets_kernel(const int64_t* __restrict__ t, int64_t rows
 int launch_ce_rows(const CeRowArgs& a, int dtype, cudaStream_t st);
 // Persistent TMA-ring standalone CE (ce_ring.cu, default); LK_UNSUPPORTED if not applicable.
 int launch_ce_ring(const CeRowArgs& a, int dtype, cudaStream_t st);
-// Single-read cluster variant for standalone CE (ce_cluster.cu); LK_UNSUPPORTED if not applicable.
-int launch_ce_cluster(const CeRowArgs& a, int dtype, cudaStream_t st);
 int launch_count_targets(const int64_t* t, int64_t rows, int64_t vocab, int64_t ignore_index,
                          int64_t* out, cudaStream_t st);
 int launch_reduce_sum(const float* v, int64_t n, float* out, cudaStream_t st);

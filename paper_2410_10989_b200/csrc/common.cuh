@@ -50,10 +50,8 @@ class ProfScope {
   int64_t mark_ = 0;
 };
 
-inline int env_int(const char* name, int dflt) {  // tuning knobs read per call
-  const char* e = getenv(name);
-  return e ? atoi(e) : dflt;
-}
+// Test-only path knobs (lk_test_select_path, capi.cu); 0 = the product path.
+int path_knob(int knob);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 inline int sm_count() {  // of the current device; cached per device, thread-safe

@@ -105,14 +105,8 @@ static int encode_out(CUtensorMap* map, const EpiArgs& e, int dtype) {
   return r == CUDA_SUCCESS ? 1 : 0;
 }
 
-// CTA-pair (cta_group::2) kernel by default; LK_CTA_GROUP=1 selects the single-CTA kernel.
-int default_cta_group() {
-  static int cg = [] {
-    const char* e = getenv("LK_CTA_GROUP");
-    return (e && e[0] == '1') ? 1 : 2;
-  }();
-  return cg;
-}
+// CTA-pair (cta_group::2) kernel; the single-CTA kernel only through the test knob.
+int default_cta_group() { return path_knob(LK_PATH_CTA_GROUP) == 1 ? 1 : 2; }
 
 int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int n_problems, int dtype,
                    int* counter, cudaStream_t st, int cta_group, bool register_epilogue) {
@@ -183,7 +177,7 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
 }  // namespace tc
 
 // ------------------------------------------------------------- planning ----
-static bool separate_cast() { return getenv("LK_FLCE_SEPARATE_CAST") != nullptr; }
+static bool separate_cast() { return path_knob(LK_PATH_FLCE_SEPARATE_CAST) == 1; }
 
 static int64_t next_pow2(int64_t n) {
   int64_t p = 1;
@@ -333,12 +327,23 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (rc) return rc;
   }
   if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
+  // grad_w slice events: the caller all-reduces slice s once event s fires, so EVERY event is
+  // recorded on `st` after the work that finalises its rows on every path (sliced tcgen05 last
+  // chunk: after each slice; otherwise -- SIMT, BT == 0, unsupported slice counts -- after all
+  // of grad_w is written).  Slicing itself needs 2..LK_MAX_GRAD_W_SLICES slices.
+  const int n_events = a->grad_w_slice_events ? std::max(0, a->grad_w_slices) : 0;
+  int recorded = 0;
+  auto record_rest = [&]() -> int {
+    for (; recorded < n_events; ++recorded)
+      LK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->grad_w_slice_events[recorded]), st));
+    return LK_OK;
+  };
   if (BT == 0) {
     if (a->loss_sum) LK_CUDA(cudaMemsetAsync(a->loss_sum, 0, sizeof(float), st));
     if (a->z_loss_sum) LK_CUDA(cudaMemsetAsync(a->z_loss_sum, 0, sizeof(float), st));
     if (a->grad_w) LK_CUDA(cudaMemsetAsync(a->grad_w, 0, (size_t)V * H * es, st));
     if (a->grad_bias) LK_CUDA(cudaMemsetAsync(a->grad_bias, 0, (size_t)V * es, st));
-    return LK_OK;
+    return record_rest();
   }
 
   for (int64_t ci = 0; ci < L.nchunks; ++ci) {
@@ -388,7 +393,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {
       ProfScope ps(1, st);
-      rc = tc && !getenv("LK_FLCE_FINALIZE_BLOCK") ? launch_ce_ring(ce, dt, st) : LK_UNSUPPORTED;
+      rc = tc && path_knob(LK_PATH_FLCE_FINALIZE) == 0 ? launch_ce_ring(ce, dt, st) : LK_UNSUPPORTED;
       if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dt, st);
     }
     if (rc) return rc;
@@ -420,7 +425,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     } else {
       // last chunk: grad_w = dtype(acc + tile) straight from the epilogue (register path),
       // instead of a TMA reduce-add into acc and a separate cast pass: -3.15 GB of HBM
-      // traffic at cfg2 (LK_FLCE_SEPARATE_CAST=1 restores the old order for comparison)
+      // traffic at cfg2 (the LK_PATH_FLCE_SEPARATE_CAST test knob restores the old order)
       const bool fold = last && !separate_cast();
       we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = fold ? 1 : 0;
     }
@@ -436,7 +441,8 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
         ++np;
       }
-      const int slices = (last && a->grad_w && a->grad_w_slice_events) ? std::min(a->grad_w_slices, 16) : 1;
+      const int slices =
+          (last && a->grad_w && n_events >= 2 && n_events <= LK_MAX_GRAD_W_SLICES) ? n_events : 1;
       if (a->grad_w && slices <= 1) {
         As[np] = {zbuf, V, r, L.ldz, 1};
         Bs[np] = {xc, H, r, H, 1};
@@ -461,7 +467,10 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
           P1.M = v1 - v0; P1.N = H; P1.K = r; P1.n_fast = 1; P1.epi = ws;
           rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, dt, sched + 2 * L.nchunks + 2 + sl, st);
         }
-        if (!rc) LK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->grad_w_slice_events[sl]), st));
+        if (!rc) {
+          LK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->grad_w_slice_events[sl]), st));
+          recorded = sl + 1;
+        }
       }
     } else {
       if (a->grad_x) {
@@ -490,7 +499,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     rc = launch_reduce_sum(a->z_loss_rows, BT, a->z_loss_sum, st);
     if (rc) return rc;
   }
-  return LK_OK;
+  return record_rest();
 }
 
 // ------------------------------------------------------ vocab-parallel ----
@@ -542,14 +551,16 @@ extern "C" int lk_flce_vp_logits(const void* x, const void* weight_shard, const 
                              tc ? parts : nullptr, nparts, tgt, reinterpret_cast<float4*>(row_stats), st);
 }
 
-extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
-                                   int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
-                                   int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
-                                   float softcap, int reduction, const int64_t* n_non_ignore,
-                                   const float* row_stats_global, void* logits_buf, float* loss_rows,
-                                   void* grad_x_partial_f32, void* grad_w_accum, int grad_w_dtype, int accumulate, void* workspace,
-                                   size_t workspace_bytes, void* stream) {
+extern "C" int lk_flce_vp_backward2(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                                    int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
+                                    int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
+                                    float softcap, int reduction, const int64_t* n_non_ignore,
+                                    const float* row_stats_global, void* logits_buf, float* loss_rows,
+                                    void* grad_x_partial, int grad_x_dtype, void* grad_w_accum, int grad_w_dtype,
+                                    int accumulate, void* workspace, size_t workspace_bytes, void* stream) {
   LK_REQUIRE(rows >= 0 && hidden >= 1 && vocab_local >= 1, LK_SIZE_MISMATCH, "bad sizes");
+  LK_REQUIRE(grad_x_dtype == LK_F32 || grad_x_dtype == dtype, LK_INVALID_ARGUMENT,
+             "grad_x partial must be fp32 or the input dtype");
   if (rows == 0) return LK_OK;
   cudaStream_t st = as_stream(stream);
   const int64_t ldz = ld_logits(vocab_local);
@@ -562,9 +573,10 @@ extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, c
   int rc = launch_ce_ring(ce, dtype, st);  // persistent TMA ring; the block kernel for other shapes
   if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dtype, st);
   if (rc) return rc;
-  // dX partial (fp32, all-reduced by the caller) and local dW shard (fp32 accumulator)
+  // dX partial (fp32 or the input dtype, all-reduced by the caller) and the local dW shard
+  void* grad_x_partial_f32 = grad_x_partial;
   EpiArgs xe{};
-  xe.kind = EPI_STORE; xe.out_dtype = LK_F32; xe.out = grad_x_partial_f32; xe.ldo = hidden; xe.alpha = 1.f;
+  xe.kind = EPI_STORE; xe.out_dtype = grad_x_dtype; xe.out = grad_x_partial; xe.ldo = hidden; xe.alpha = 1.f;
   xe.M = rows; xe.N = hidden;
   EpiArgs we{};
   LK_REQUIRE(grad_w_dtype == LK_F32 || grad_w_dtype == dtype, LK_INVALID_ARGUMENT,
@@ -584,7 +596,7 @@ extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, c
     tc::Problem Ps[2];
     int np = 0;
     if (grad_x_partial_f32) {
-      xe.kind = EPI_F32;
+      if (grad_x_dtype == LK_F32) xe.kind = EPI_F32;  // else EPI_STORE in the input dtype (TMA store)
       As[np] = {logits_buf, vocab_local, rows, ldz, 0};
       Bs[np] = {weight_shard, hidden, vocab_local, hidden, 1};
       Ps[np] = tc::Problem{};
@@ -613,6 +625,19 @@ extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, c
     rc = launch_simt_gemm(A, B, vocab_local, hidden, rows, dtype, we, st);
   }
   return rc;
+}
+
+extern "C" int lk_flce_vp_backward_ex(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,
+                                      int64_t hidden, int64_t vocab_local, int64_t vocab_offset, int64_t vocab_total,
+                                      int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
+                                      float softcap, int reduction, const int64_t* n_non_ignore,
+                                      const float* row_stats_global, void* logits_buf, float* loss_rows,
+                                      void* grad_x_partial_f32, void* grad_w_accum, int grad_w_dtype, int accumulate,
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+  return lk_flce_vp_backward2(x, weight_shard, target, rows, hidden, vocab_local, vocab_offset, vocab_total, dtype,
+                              ignore_index, label_smoothing, lse_square_scale, softcap, reduction, n_non_ignore,
+                              row_stats_global, logits_buf, loss_rows, grad_x_partial_f32, LK_F32, grad_w_accum,
+                              grad_w_dtype, accumulate, workspace, workspace_bytes, stream);
 }
 
 extern "C" int lk_flce_vp_backward(const void* x, const void* weight_shard, const int64_t* target, int64_t rows,

@@ -308,19 +308,10 @@ static bool aligned16_all(std::initializer_list<const void*> ptrs) {
   return true;
 }
 
-// Implementation choice: LK_NORM_IMPL = cta (default) | ring | warp | generic; read per call so
-// the parity tests can run every path against the others.
+// Implementation choice: CTA per row (product path); warp-per-row, generic and TMA-ring kernels
+// only through the LK_PATH_NORM_IMPL test knob, so the parity tests run every path against the others.
 enum { IMPL_CTA = 0, IMPL_WARP = 1, IMPL_GENERIC = 2, IMPL_RING = 3 };
-static int norm_impl() {
-  const char* e = getenv("LK_NORM_IMPL");
-  if (!e) return IMPL_CTA;
-  switch (e[0]) {
-    case 'w': return IMPL_WARP;
-    case 'g': return IMPL_GENERIC;
-    case 'r': return IMPL_RING;
-    default: return IMPL_CTA;
-  }
-}
+static int norm_impl() { return path_knob(LK_PATH_NORM_IMPL); }
 
 #define LK_VPT8_DISPATCH(vpt, VPT, ...)                     \
   switch (vpt) {                                            \

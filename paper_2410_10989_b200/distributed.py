@@ -28,7 +28,17 @@ import torch
 import torch.distributed as dist
 
 from . import _capi
-from ._utils import as_targets, check, device_guard, dtype_code, lib, ptr, stream_of, workspace
+from ._utils import (
+    as_targets,
+    check,
+    device_guard,
+    dtype_code,
+    lib,
+    ptr,
+    raise_if_out_of_range,
+    stream_of,
+    workspace,
+)
 
 
 # ------------------------------------------------------------- token sharded
@@ -46,18 +56,26 @@ def _count_cuda(t: torch.Tensor, vocab: int, ignore_index: int) -> torch.Tensor:
     return out
 
 
-def _local_flce_cuda(x, w, t, mean_count, **kw):
+MAX_DW_SLICES = 16  # LK_MAX_GRAD_W_SLICES (include/liger_b200.h)
+
+
+def _local_flce_cuda(x, w, t, mean_count, reduction="mean", **kw):
     from .fused_linear_cross_entropy import fused_linear_cross_entropy_forward
 
+    # no host read of the out-of-range count here: token_sharded_flce checks the GLOBAL count
+    # after every collective is enqueued, so the dW all-reduce can overlap the dW GEMMs
     loss, _, _, _, gx, gw, _ = fused_linear_cross_entropy_forward(
-        x, w, t, compute_grad_input=True, compute_grad_weight=True, mean_count=mean_count[:1], **kw)
+        x, w, t, compute_grad_input=True, compute_grad_weight=True, reduction=reduction,
+        mean_count=mean_count[:1] if reduction == "mean" else None, check_targets=False, **kw)
     return loss, gx, gw
 
 
 def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw):
     """Local FLCE whose last-chunk grad_w GEMM is split into `dw_slices` vocab-row slices;
     slice s is all-reduced on a side stream as soon as its event fires, so all but the last
-    slice's all-reduce hide under the remaining dW GEMM launches."""
+    slice's all-reduce hide under the remaining dW GEMM launches.  The library records every
+    event on every path (include/liger_b200.h, grad_w_slice_events), so a slice is never
+    all-reduced before it is final -- also on the SIMT path or for a rank with no rows."""
     events = [torch.cuda.Event() for _ in range(dw_slices)]
     loss, gx, gw = local_fn(x, w, t, counts, grad_w_slice_events=events, **kw)
     v = gw.shape[0]
@@ -86,20 +104,30 @@ def token_sharded_flce(
     local_fn: Optional[Callable] = None,
     reduce_grad_weight: bool = True,
     dw_slices: int = 4,
+    check_targets: bool = True,
     **kw,
 ):
-    """Returns (global loss, local grad_x, all-reduced grad_w).
+    """Returns (loss, local grad_x, all-reduced grad_w).
 
-    With the CUDA kernels (default `local_fn`) and `dw_slices` > 1, the grad_w all-reduce
-    overlaps the last chunk's grad_w GEMM (`_allreduce_grad_w_overlapped`).
+    `loss` is the global scalar for reduction 'mean'/'sum'; for 'none' it is this rank's
+    per-row loss vector (rows of different ranks are not summed element-wise).
+    With the CUDA kernels (default `local_fn`) and 2 <= `dw_slices` <= 16, the grad_w
+    all-reduce overlaps the last chunk's grad_w GEMM (`_allreduce_grad_w_overlapped`): the
+    call enqueues every kernel and collective without a host sync, and only then (with
+    `check_targets`) reads the globally all-reduced out-of-range target count, so every rank
+    raises TargetOutOfRange together instead of one rank leaving the others in a collective.
     """
+    if reduction not in ("mean", "sum", "none"):
+        raise ValueError(f"reduction must be 'mean' or 'sum' or 'none'. Got: {reduction}")
     t = as_targets(target_local) if target_local.is_cuda else target_local.reshape(-1).to(torch.int64)
     count_fn = count_fn or (lambda tt: _count_cuda(tt, weight.shape[0], ignore_index))
+    dw_slices = max(1, min(int(dw_slices), MAX_DW_SLICES))
     overlap = local_fn is None and reduce_grad_weight and dw_slices > 1 and x_local.is_cuda
+    cuda_local = local_fn is None
     local_fn = local_fn or _local_flce_cuda
     counts = count_fn(t)
-    if reduction == "mean":
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    # (n_valid, n_out_of_range) summed over ranks: the MEAN denominator and the global range check
+    dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     kw = dict(kw, ignore_index=ignore_index, reduction=reduction)
     cw = kw.get("ce_weight")
     if cw is not None and reduction == "mean" and local_fn is _local_flce_cuda:
@@ -115,8 +143,11 @@ def token_sharded_flce(
         loss, gx, gw = local_fn(x_local, weight, t, counts, **kw)
         if reduce_grad_weight and gw is not None:
             dist.all_reduce(gw, op=dist.ReduceOp.SUM, group=group)
-    loss = loss.clone()
-    dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+    if reduction != "none":
+        loss = loss.clone()
+        dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
+    if check_targets and cuda_local:
+        raise_if_out_of_range(counts, weight.shape[0])
     return loss, gx, gw
 
 
@@ -133,19 +164,15 @@ def vocab_shard(vocab: int, rank: int, world: int) -> VocabShard:
     return VocabShard(lo, hi - lo, vocab)
 
 
-def combine_row_stats(stats: torch.Tensor, group=None) -> torch.Tensor:
-    """All-reduce per-row (max, sumexp, sum_logits, target_logit) across vocab shards."""
-    m = stats[:, 0].clone()
-    dist.all_reduce(m, op=dist.ReduceOp.MAX, group=group)
-    out = torch.empty_like(stats)
-    out[:, 0] = m
-    out[:, 1] = stats[:, 1] * torch.exp(stats[:, 0] - m)
-    out[:, 2] = stats[:, 2]
-    out[:, 3] = stats[:, 3]
-    rest = out[:, 1:].contiguous()
-    dist.all_reduce(rest, op=dist.ReduceOp.SUM, group=group)
-    out[:, 1:] = rest
-    return out
+def combine_row_stats(stats: torch.Tensor, ops, group=None) -> torch.Tensor:
+    """Global per-row (max, sumexp, sum_logits, target_logit) across vocab shards: ONE
+    all_gather of the [rows, 4] local statistics, then `ops.combine_stats` folds the ranks in
+    rank order (lk_flce_vp_combine_stats), so every rank holds bit-identical statistics."""
+    world = dist.get_world_size(group)
+    rows = stats.shape[0]
+    gathered = torch.empty(world * rows, stats.shape[1], dtype=stats.dtype, device=stats.device)
+    dist.all_gather_into_tensor(gathered, stats.contiguous(), group=group)
+    return ops.combine_stats(gathered.view(world, rows, stats.shape[1]))
 
 
 class CudaVocabOps:
@@ -167,17 +194,24 @@ class CudaVocabOps:
                                   stream_of(x)))
         return stats, buf
 
+    def combine_stats(self, gathered):
+        world, rows = gathered.shape[0], gathered.shape[1]
+        out = torch.empty(rows, 4, dtype=torch.float32, device=gathered.device)
+        check(lib().lk_flce_vp_combine_stats(ptr(gathered), world, rows, ptr(out), stream_of(gathered)))
+        return out
+
     def backward(self, x, w_shard, t, shard, stats_g, buf, n_valid, gw_acc, accumulate, *, ignore_index,
-                 label_smoothing, lse_square_scale, softcap, reduction):
+                 label_smoothing, lse_square_scale, softcap, reduction, gx_out=None):
+        """dX partial into `gx_out` (the x dtype or fp32) when given, else a new fp32 tensor."""
         rows, h = x.shape
         loss_rows = torch.empty(rows, dtype=torch.float32, device=x.device)
-        gx = torch.empty(rows, h, dtype=torch.float32, device=x.device)
+        gx = gx_out if gx_out is not None else torch.empty(rows, h, dtype=torch.float32, device=x.device)
         ws = workspace(256, x.device)
-        check(lib().lk_flce_vp_backward_ex(
+        check(lib().lk_flce_vp_backward2(
             ptr(x), ptr(w_shard), ptr(t), rows, h, shard.size, shard.offset, shard.total, self.dt, ignore_index,
             float(label_smoothing), float(lse_square_scale), float(softcap or 0.0), _capi.REDUCTIONS[reduction],
-            ptr(n_valid), ptr(stats_g), ptr(buf), ptr(loss_rows), ptr(gx), ptr(gw_acc), dtype_code(gw_acc),
-            int(accumulate), ptr(ws), ws.numel(), stream_of(x)))
+            ptr(n_valid), ptr(stats_g), ptr(buf), ptr(loss_rows), ptr(gx), dtype_code(gx), ptr(gw_acc),
+            dtype_code(gw_acc), int(accumulate), ptr(ws), ws.numel(), stream_of(x)))
         return loss_rows, gx
 
     def count(self, t, vocab, ignore_index):
@@ -199,12 +233,18 @@ def vocab_parallel_flce(
     chunk_rows: int = 2048,
     ops=None,
     accum_dtype: Optional[torch.dtype] = None,
+    dx_reduce_dtype: Optional[torch.dtype] = None,
+    check_targets: bool = True,
 ):
     """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
 
     Every rank holds all rows of x and the targets; only W is sharded by vocab rows.
     `accum_dtype` follows Liger's FLCE option: None accumulates the dW shard across chunks
     in the weight dtype (16-bit weights), torch.float32 in an fp32 buffer.
+    The dX partial of chunk k is all-reduced asynchronously (`async_op=True`) while chunk k+1
+    computes; by default it is written by the backward GEMM straight into grad_x in the x
+    dtype and reduced there in place (`dx_reduce_dtype=torch.float32` reduces fp32 partials
+    and casts after the last wait).  The only wait is on the outstanding reductions at the end.
     """
     ops = ops or CudaVocabOps(x.dtype, x.device)
     t = target.reshape(-1).to(torch.int64).contiguous()
@@ -221,14 +261,22 @@ def vocab_parallel_flce(
     loss_rows = torch.empty(bt, dtype=torch.float32, device=x.device)
     kw = dict(ignore_index=ignore_index, label_smoothing=label_smoothing, lse_square_scale=lse_square_scale,
               softcap=softcap, reduction=reduction)
+    dx_dt = dx_reduce_dtype or x.dtype
+    pending = []  # (work, lo, hi, partial) of in-flight dX reductions
     for ci, lo in enumerate(range(0, bt, chunk_rows)):
         hi = min(lo + chunk_rows, bt)
         xc, tc = x[lo:hi].contiguous(), t[lo:hi]
         stats, buf = ops.logits_stats(xc, w_shard, tc, shard, softcap, ignore_index)
-        stats_g = combine_row_stats(stats, group)
-        lr, gxp = ops.backward(xc, w_shard, tc, shard, stats_g, buf, n_valid, gw_acc, ci > 0, **kw)
-        dist.all_reduce(gxp, op=dist.ReduceOp.SUM, group=group)
-        gx[lo:hi] = gxp.to(x.dtype)
+        stats_g = combine_row_stats(stats, ops, group)
+        gx_out = gx[lo:hi] if dx_dt == x.dtype else torch.empty(hi - lo, h, dtype=dx_dt, device=x.device)
+        lr, gxp = ops.backward(xc, w_shard, tc, shard, stats_g, buf, n_valid, gw_acc, ci > 0, gx_out=gx_out, **kw)
+        pending.append((dist.all_reduce(gxp, op=dist.ReduceOp.SUM, group=group, async_op=True), lo, hi, gxp))
         loss_rows[lo:hi] = lr
+    for work, lo, hi, gxp in pending:
+        work.wait()
+        if gxp.data_ptr() != gx[lo:hi].data_ptr():
+            gx[lo:hi] = gxp.to(x.dtype)
     loss = loss_rows if reduction == "none" else loss_rows.sum()
+    if check_targets and isinstance(ops, CudaVocabOps):
+        raise_if_out_of_range(n_valid, shard.total)
     return loss, gx, gw_acc.to(w_shard.dtype)

@@ -72,6 +72,7 @@ def fused_linear_cross_entropy_forward(
     mean_count: Optional[torch.Tensor] = None,
     grad_w_slice_events=None,
     mean_weight_sum: Optional[torch.Tensor] = None,
+    check_targets: bool = True,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -85,6 +86,9 @@ def fused_linear_cross_entropy_forward(
     non-ignored count (token-sharded mode).  `grad_w_slice_events` (list of torch.cuda.Event)
     splits the last chunk's grad_w GEMM into that many vocab-row slices and records event s
     when slice s of grad_w is final (overlap of the token-sharded dW all-reduce).
+    `check_targets=False` skips the host read of the device-side out-of-range count (the one
+    host sync of the call); the caller then owns the check (token_sharded_flce does it on the
+    all-reduced count after enqueueing its collectives).
     """
     if not (0.0 <= label_smoothing <= 1.0):
         raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
@@ -169,7 +173,8 @@ def fused_linear_cross_entropy_forward(
         raise errors.ShapeMismatch("mean_weight_sum must be a CUDA float32 tensor")
     check(L.lk_flce_forward_backward(_capi.C.byref(args)))
     del ws
-    raise_if_out_of_range(stats, v)
+    if check_targets:
+        raise_if_out_of_range(stats, v)
     if reduction == "none":
         loss = loss_rows
         z_loss = z_rows.to(x.dtype) if return_z_loss else None

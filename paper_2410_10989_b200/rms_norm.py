@@ -24,7 +24,9 @@ def rms_norm_forward(X, W, eps, offset=0.0, casting_mode="llama"):
     rows, cols = X2.shape
     if W is not None and (W.shape != (cols,)):
         raise ValueError("Incompatible hidden size dimension between input tensor and weight")
-    Wc = W.contiguous() if W is not None else None
+    # The kernels read the weight in the activation dtype: a weight of another dtype (e.g. fp32
+    # weight with bf16 activations, which Liger accepts) is cast first, as layer_norm.py does.
+    Wc = W.to(X2.dtype).contiguous() if W is not None else None
     Y = torch.empty_like(X2)
     rstd = torch.empty(rows, dtype=torch.float32 if mode in (0, 1) else X2.dtype, device=X2.device)
     check(lib().lk_rmsnorm_fwd(ptr(X2), ptr(Wc), ptr(Y), ptr(rstd), rows, cols, float(eps), float(offset), mode,
@@ -38,11 +40,16 @@ def rms_norm_backward(dY, X2, W, rstd, offset, mode, in_place):
     dY2 = dY.reshape(-1, shape[-1]).contiguous()
     rows, cols = dY2.shape
     dX = dY2 if in_place else torch.empty_like(dY2)
+    w_dtype = W.dtype if W is not None else None
+    if W is not None and W.dtype != dY2.dtype:
+        W = W.to(dY2.dtype)
     dW = torch.empty_like(W) if W is not None else None
     L = lib()
     ws = workspace(L.lk_rmsnorm_bwd_workspace_bytes(rows, cols), dY2.device) if W is not None else None
     check(L.lk_rmsnorm_bwd(ptr(dY2), ptr(X2), ptr(W), ptr(rstd), ptr(dX), ptr(dW), rows, cols, float(offset), mode,
                            dtype_code(dY2), ptr(ws), ws.numel() if ws is not None else 0, stream_of(dY2)))
+    if dW is not None and dW.dtype != w_dtype:
+        dW = dW.to(w_dtype)  # Liger returns dW in the weight's dtype
     return dX.view(shape), dW
 
 

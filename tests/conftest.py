@@ -46,3 +46,21 @@ def rel_close(actual, ref, rtol, atol_frac=None):
     err = np.abs(a - b)
     ok = err <= atol + rtol * np.abs(b)
     return bool(ok.all()), float(err.max() / (scale if scale else 1.0)) if b.size else 0.0
+
+
+@pytest.fixture
+def path_knob():
+    """Select a test-only alternative kernel path for the rest of the test (lk_test_select_path);
+    restored to the product path afterwards."""
+    from paper_2410_10989_b200 import _capi
+
+    ctxs = []
+
+    def select(knob, value):
+        c = _capi.select_path(knob, value)
+        c.__enter__()
+        ctxs.append(c)
+
+    yield select
+    for c in reversed(ctxs):
+        c.__exit__(None, None, None)

@@ -57,7 +57,8 @@ def oracle_local_flce(x, w, t, counts, ignore_index=-100, reduction="mean", **kw
                                     reduction="sum", **kw)
     scale = 1.0 / max(n, 1) if reduction == "mean" else 1.0
     g = g * scale
-    return (torch.tensor(loss * scale, dtype=torch.float64), torch.tensor(g @ w.numpy()), torch.tensor(g.T @ x.numpy()))
+    lv = torch.tensor(rows) if reduction == "none" else torch.tensor(loss * scale, dtype=torch.float64)
+    return lv, torch.tensor(g @ w.numpy()), torch.tensor(g.T @ x.numpy())
 
 
 class OracleVocabOps:
@@ -76,8 +77,14 @@ class OracleVocabOps:
         zt = np.where(inr, z[np.arange(len(tl)), np.clip(tl, 0, shard.size - 1)], 0.0)
         return torch.tensor(np.stack([m, s, sz, zt], axis=1)), torch.tensor(z)
 
+    def combine_stats(self, gathered):
+        g = gathered.numpy()
+        m = g[:, :, 0].max(axis=0)
+        s = (g[:, :, 1] * np.exp(g[:, :, 0] - m[None, :])).sum(axis=0)
+        return torch.tensor(np.stack([m, s, g[:, :, 2].sum(axis=0), g[:, :, 3].sum(axis=0)], axis=1))
+
     def backward(self, x, w_shard, t, shard, stats_g, buf, n_valid, gw_acc, accumulate, *, ignore_index,
-                 label_smoothing, lse_square_scale, softcap, reduction):
+                 label_smoothing, lse_square_scale, softcap, reduction, gx_out=None):
         z = buf.numpy()
         st = stats_g.numpy()
         m, s, sz, zt = st[:, 0], st[:, 1], st[:, 2], st[:, 3]
@@ -119,7 +126,12 @@ def _worker(rank, port, mode, kw, out, world=WORLD, prob=None):
             lo, hi = shard_rows(len(t), rank, world)
             loss, gx, gw = token_sharded_flce(torch.tensor(x[lo:hi]), torch.tensor(w), torch.tensor(t[lo:hi]),
                                               count_fn=oracle_count, local_fn=oracle_local_flce, **kw)
-            np.testing.assert_allclose(loss.item(), ref_loss, rtol=1e-12)
+            if kw.get("reduction") == "none":  # this rank's own per-row losses, never summed across ranks
+                ref_rows = liger_ref.flce(x[lo:hi], w, t[lo:hi], **kw)[1]
+                assert loss.shape == (hi - lo,)
+                np.testing.assert_allclose(loss.numpy(), ref_rows, rtol=1e-12, atol=1e-14)
+            else:
+                np.testing.assert_allclose(loss.item(), ref_loss, rtol=1e-12)
             np.testing.assert_allclose(gx.numpy(), rgx[lo:hi], rtol=1e-10, atol=1e-14)
             np.testing.assert_allclose(gw.numpy(), rgw, rtol=1e-10, atol=1e-14)
         else:
@@ -161,6 +173,12 @@ def test_token_sharded_world2_matches_single_process(kw):
 @pytest.mark.parametrize("kw", [dict(), dict(softcap=3.0, label_smoothing=0.1), dict(lse_square_scale=1e-3)])
 def test_vocab_parallel_world2_matches_single_process(kw):
     run_world("vocab", kw)
+
+
+def test_token_sharded_reduction_none_ragged_world3():
+    """reduction='none' returns each rank's own per-row losses (ragged 9/8/8 shards): the
+    per-row vectors are not all-reduced element-wise across ranks."""
+    run_world("token", dict(reduction="none"), world=3, prob=dict(bt=25))
 
 
 @pytest.mark.parametrize("mode", ["token", "vocab"])

@@ -11,7 +11,7 @@ import torch
 
 import paper_2410_10989_b200 as lk
 from oracle import liger_ref, rowfuse_port as rp
-from paper_2410_10989_b200 import errors
+from paper_2410_10989_b200 import _capi, errors
 from tests.conftest import rel_close
 
 pytestmark = pytest.mark.gpu
@@ -89,9 +89,8 @@ def test_ce_large_vocab_bf16_rows_sum_to_zero():
 @pytest.mark.parametrize("v,dtype", [(32000, torch.bfloat16), (128256, torch.bfloat16), (256000, torch.bfloat16),
                                      (128256, torch.float32), (40000, torch.float16), (5003, torch.bfloat16),
                                      (1000, torch.float32), (8192, torch.bfloat16)])
-@pytest.mark.parametrize("impl", ["cluster", "block"])
-def test_ce_ring_path_matches_other_paths(v, dtype, impl, monkeypatch):
-    """Default persistent TMA-ring kernel vs the cluster (DSMEM) and one-CTA-per-row kernels, and the oracle."""
+def test_ce_ring_path_matches_other_paths(v, dtype):
+    """Default persistent TMA-ring kernel vs the one-CTA-per-row kernel, and the oracle."""
     rows = 300  # > SM count: several rows per persistent CTA
     g = torch.Generator(device="cuda").manual_seed(v)
     z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(dtype)
@@ -107,9 +106,8 @@ def test_ce_ring_path_matches_other_paths(v, dtype, impl, monkeypatch):
         return loss.detach().float(), x.grad.float()
 
     l1, g1 = run()
-    monkeypatch.setenv("LK_CE_IMPL", impl)
-    l2, g2 = run()
-    monkeypatch.delenv("LK_CE_IMPL")
+    with _capi.select_path(_capi.PATH_CE_IMPL, 1):
+        l2, g2 = run()
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     ok, err = rel_close(l1.cpu().numpy(), l2.cpu().numpy(), tol)
     assert ok, err
@@ -194,9 +192,9 @@ def test_rowfuse_inplace_contract_port_vs_gpu(golden):
 @pytest.mark.parametrize("impl", ["ring", "block"])
 @pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
 @pytest.mark.parametrize("cap", [None, 20.0])
-def test_ce_token_accuracy_and_predicted_tokens(impl, reduction, cap, monkeypatch):
+def test_ce_token_accuracy_and_predicted_tokens(impl, reduction, cap, path_knob):
     """Liger return_token_accuracy / return_predicted_tokens (LK/ops/cross_entropy.py:131-163, 294-299, 415-420)."""
-    monkeypatch.setenv("LK_CE_IMPL", impl)
+    path_knob(_capi.PATH_CE_IMPL, {"ring": 0, "block": 1}[impl])
     rows, v = 300, 32000
     g = torch.Generator(device="cuda").manual_seed(7)
     z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(torch.bfloat16)
@@ -255,11 +253,11 @@ def test_ce_int64_offsets_beyond_2_31_elements():
 @pytest.mark.parametrize("reduction", ["mean", "sum", "none"])
 @pytest.mark.parametrize("kw", [dict(), dict(softcap=20.0, lse_square_scale=1e-4), dict(label_smoothing=0.1),
                                 dict(label_smoothing=0.2, softcap=20.0, lse_square_scale=1e-4)])
-def test_ce_class_weights(impl, reduction, kw, monkeypatch):
+def test_ce_class_weights(impl, reduction, kw, path_knob):
     """Liger `weight` (class weights, LK/ops/cross_entropy.py:122-124, 165-171, 220-239, 278-288),
     with and without label smoothing, vs the float64 oracle (itself pinned to torch
     F.cross_entropy(weight=, label_smoothing=))."""
-    monkeypatch.setenv("LK_CE_IMPL", impl)
+    path_knob(_capi.PATH_CE_IMPL, {"ring": 0, "block": 1}[impl])
     rows, v = 300, 4096
     g = torch.Generator(device="cuda").manual_seed(13)
     z = (torch.randn(rows, v, device="cuda", generator=g) * 3).to(torch.bfloat16)

@@ -17,7 +17,7 @@ import torch
 
 import paper_2410_10989_b200 as lk
 from oracle import liger_ref
-from paper_2410_10989_b200 import errors
+from paper_2410_10989_b200 import _capi, errors
 from paper_2410_10989_b200.fused_linear_cross_entropy import fused_linear_cross_entropy_forward as flce_fwd
 from tests.conftest import rel_close
 from tests.torch_ref import close, flce_ref, rel_err
@@ -123,17 +123,17 @@ def test_bf16_ragged_shapes_and_bias():
 
 @pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(softcap=5.0),
                                 dict(lse_square_scale=1e-4, reduction="sum")])
-@pytest.mark.parametrize("env", ["LK_FLCE_FINALIZE_BLOCK", "LK_FLCE_SEPARATE_CAST"])
-def test_ring_finalize_and_folded_dw_cast_match_reference_paths(kw, env, monkeypatch):
+@pytest.mark.parametrize("env", ["finalize_block", "separate_cast"])
+def test_ring_finalize_and_folded_dw_cast_match_reference_paths(kw, env):
     """Default path (TMA-ring finalize, dW cast folded into the last chunk's epilogue) vs the
     one-CTA-per-row finalize / separate cast kernel, and the oracle."""
     xb, wb, tb, x, w, t = bf16_problem(1000, 256, 4096, seed=11)
-    if env == "LK_FLCE_SEPARATE_CAST":
+    if env == "separate_cast":
         kw = dict(kw, accum_dtype=torch.float32)  # the fold only exists on the fp32-accumulator path
     a = flce(xb, wb, tb, chunk_rows=256, **kw)
-    monkeypatch.setenv(env, "1")
-    b = flce(xb, wb, tb, chunk_rows=256, **kw)
-    monkeypatch.delenv(env)
+    knob = _capi.PATH_FLCE_FINALIZE if env == "finalize_block" else _capi.PATH_FLCE_SEPARATE_CAST
+    with _capi.select_path(knob, 1):
+        b = flce(xb, wb, tb, chunk_rows=256, **kw)
     assert rel_err(a[0], b[0]) < 1e-5
     assert close(a[2], b[2], 1e-2) and close(a[3], b[3], 1e-2)
     ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t, **{k: v for k, v in kw.items() if k != "accum_dtype"})
@@ -214,6 +214,25 @@ def test_target_out_of_range_raises():
         flce_fwd(xb, wb, tb)
 
 
+@pytest.mark.parametrize("bad", [128, 100000, -5])
+def test_target_out_of_range_with_class_weights_raises(bad):
+    """Class weights are indexed by target: an out-of-range target must raise the typed error,
+    not read past the weight vector."""
+    xb, wb, tb, *_ = bf16_problem(64, 64, 128, seed=6, ignore_frac=0.0)
+    tb[3] = bad
+    cw = torch.rand(128, device="cuda") + 0.5
+    with pytest.raises(errors.TargetOutOfRange):
+        flce_fwd(xb, wb, tb, ce_weight=cw)
+    with pytest.raises(errors.TargetOutOfRange):
+        flce_fwd(xb, wb, tb, ce_weight=cw, label_smoothing=0.1)
+    x = torch.randn(8, 128, device="cuda")
+    t = torch.randint(0, 128, (8,), device="cuda")
+    t[2] = bad
+    with pytest.raises(errors.TargetOutOfRange):
+        lk.LigerCrossEntropyLoss(weight=cw)(x, t)
+    torch.cuda.synchronize()  # no illegal-address fault left behind
+
+
 def test_no_grad_forward_matches():
     xb, wb, tb, x, w, t = bf16_problem(300, 64, 700, seed=8)
     loss = flce_fwd(xb, wb, tb, compute_grad_input=False)[0]
@@ -263,13 +282,19 @@ def test_cfg2_llama3_head_vs_torch_fp32_and_properties():
 
 def test_cfg4_gemma2_head_softcap_smoothing():
     # Gemma-2-9B head: H=3584, V=256000, softcap 30, label smoothing 0.1 (stress scale: logit sigma ~ 10)
-    x, w, t = big_problem(2048, 3584, 256000, seed=1, wscale=30.0)
+    # BT = 8192: 8192 x 256000 logits = 2.1e9 elements, above 2^31 - 1 bytes in
+    # bf16, in 4 chunks; flce_ref is pinned to oracle.liger_ref (tests/test_oracle.py)
+    x, w, t = big_problem(8192, 3584, 256000, seed=1, wscale=30.0)
     kw = dict(softcap=30.0, label_smoothing=0.1)
     loss, _, gx, gw, _ = flce(x, w, t, **kw)
     rloss, _, rgx, rgw, _ = flce_ref(x, w, t, **kw)
     assert abs(loss.item() - rloss.item()) <= 2e-2 * abs(rloss.item())
     assert close(gx, rgx, 2e-2), rel_err(gx, rgx)
     assert close(gw, rgw, 2e-2), rel_err(gw, rgw)
+    assert torch.all(gx[t == -100] == 0)
+    del rgx, rgw
+    loss2, _, gx2, gw2, _ = flce(x, w, t, **kw)  # bitwise deterministic
+    assert loss.item() == loss2.item() and torch.equal(gx, gx2) and torch.equal(gw, gw2)
 
 
 @pytest.mark.parametrize("simt", [False, True])

@@ -1,0 +1,148 @@
+"""Oracle parity at the BASELINE headline configurations (GPU).
+
+north_star: results "must match the CPU reference in pkg/src on identical inputs" -- loss
+and gradients within rtol 1e-4 in fp32, 2e-2 in bf16, exact ignore masking and counts.
+
+* cfg1 (BT=1024, H=512, V=4096, fp32): FULL dX and dW against the pinned port of
+  rowfuse.flce_forward_backward run in float64 (oracle/rowfuse_port.py, itself pinned to the
+  reference's goldens), plus the 10%-ignored variant against the float64 Liger oracle.
+* cfg2 (H=4096, V=128256) and cfg4 (H=3584, V=256000, softcap 30, smoothing 0.1): row
+  slices of the full-size synthetic batch with the FULL weight, against oracle.liger_ref in
+  float64 on the bf16-rounded inputs -- loss, per-row losses, full dX and full dW -- with the
+  ignored rows' losses and gradients exactly 0 and the non-ignored count exact.  The slices
+  are run both as one chunk and chunked (weight-dtype dW accumulation across chunks).
+The full-BT runs (tests/test_gpu_flce.py) compare against tests/torch_ref.flce_ref, which
+tests/test_oracle.py pins to oracle.liger_ref.
+"""
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import liger_ref
+from oracle import rowfuse_port as rp
+from paper_2410_10989_b200.fused_linear_cross_entropy import fused_linear_cross_entropy_forward as flce_fwd
+from tests.conftest import rel_close
+
+pytestmark = pytest.mark.gpu
+
+
+def run(x, w, t, **kw):
+    loss, _, _, _, gx, gw, _ = flce_fwd(x, w, t, compute_grad_input=True, compute_grad_weight=True, **kw)
+    torch.cuda.synchronize()
+    return loss, gx, gw
+
+
+def headline_batch(bt, h, v, seed, wscale=1.0, ignore_frac=0.1):
+    """The bench's synthetic cfg2/cfg4 batch: X ~ U(-1,1), W ~ U(-1,1)*wscale/64, 10% ignored."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = (torch.rand(bt, h, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+    w = ((torch.rand(v, h, device="cuda", generator=g) * 2 - 1) * (wscale / 64.0)).to(torch.bfloat16)
+    t = torch.randint(0, v, (bt,), device="cuda", generator=g)
+    t[torch.rand(bt, device="cuda", generator=g) < ignore_frac] = -100
+    return x, w, t
+
+
+# ------------------------------------------------------------------- cfg1 fp32
+def cfg1_inputs(ignore_frac=0.0):
+    """SURVEY §8(d) cfg1 generator (rowfuse/bench.py:295-297): X ~ U(-1,1), W_hv ~ U(-1,1)/sqrt(H)."""
+    rng = np.random.default_rng(0)
+    x = rng.uniform(-1, 1, (1024, 512))
+    w_hv = rng.uniform(-1, 1, (512, 4096)) / math.sqrt(512)
+    t = rng.integers(0, 4096, 1024)
+    if ignore_frac:
+        t[np.random.default_rng(1).random(1024) < ignore_frac] = -100
+    return x, w_hv, t
+
+
+@pytest.mark.parametrize("chunk", [None, 128, 1024])
+def test_cfg1_fp32_full_tensors_vs_rowfuse_port_f64(chunk):
+    x, w_hv, t = cfg1_inputs()
+    xf = x.astype(np.float32).astype(np.float64)  # the fp32-rounded inputs both sides see
+    wf = w_hv.astype(np.float32).astype(np.float64)
+    ref_loss, ref_dx, ref_dw_hv = rp.flce_forward_backward(xf, wf, t, mean=True)
+    xd = torch.tensor(x, dtype=torch.float32, device="cuda")
+    wd = torch.tensor(np.ascontiguousarray(w_hv.T), dtype=torch.float32, device="cuda")
+    loss, gx, gw = run(xd, wd, torch.tensor(t, device="cuda"), chunk_rows=chunk)
+    assert loss.item() == pytest.approx(ref_loss, rel=1e-4)
+    ok, err = rel_close(gx.double().cpu().numpy(), ref_dx, 1e-4)
+    assert ok, ("dx", err)
+    ok, err = rel_close(gw.double().cpu().numpy(), ref_dw_hv.T, 1e-4)
+    assert ok, ("dw", err)
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(reduction="sum")])
+def test_cfg1_fp32_ignore_index_full_tensors_vs_liger_oracle(opts):
+    x, w_hv, t = cfg1_inputs(ignore_frac=0.1)
+    w_vh = np.ascontiguousarray(w_hv.T)
+    xf = x.astype(np.float32).astype(np.float64)
+    wf = w_vh.astype(np.float32).astype(np.float64)
+    ref_loss, ref_rows, _, rgx, rgw, _ = liger_ref.flce(xf, wf, t, **opts)
+    tt = torch.tensor(t, device="cuda")
+    xd = torch.tensor(x, dtype=torch.float32, device="cuda")
+    wd = torch.tensor(w_vh, dtype=torch.float32, device="cuda")
+    loss, gx, gw = run(xd, wd, tt, **opts)
+    assert loss.item() == pytest.approx(ref_loss, rel=1e-4)
+    assert rel_close(gx.double().cpu().numpy(), rgx, 1e-4)[0]
+    assert rel_close(gw.double().cpu().numpy(), rgw, 1e-4)[0]
+    rows = run(xd, wd, tt, **dict(opts, reduction="none"))[0]
+    ign = t == -100
+    assert torch.all(rows[torch.tensor(ign, device="cuda")] == 0)
+    assert torch.all(gx[tt == -100] == 0)
+    scale = 1.0 if opts.get("reduction") == "sum" else 1.0 / int((~ign).sum())
+    assert rel_close(rows.double().cpu().numpy(), ref_rows / scale, 1e-4)[0]
+
+
+# --------------------------------------------------- cfg2 / cfg4 row slices
+def _slice_parity(x, w, t, lo, rows, chunk, **opts):
+    xs, ts = x[lo:lo + rows].contiguous(), t[lo:lo + rows].contiguous()
+    xn, wn, tn = xs.double().cpu().numpy(), w.double().cpu().numpy(), ts.cpu().numpy()
+    ref_loss, ref_rows, _, rgx, rgw, _ = liger_ref.flce(xn, wn, tn, **opts)
+    loss, gx, gw = run(xs, w, ts, chunk_rows=chunk, **opts)
+    assert rel_close(loss.item(), ref_loss, 2e-2)[0], (loss.item(), ref_loss)
+    ok, err = rel_close(gx.float().cpu().numpy(), rgx, 2e-2)
+    assert ok, ("dx", err)
+    gwn = gw.float().cpu().numpy()
+    ok, err = rel_close(gwn, rgw, 2e-2)
+    assert ok, ("dw", err)
+    del gwn, rgw
+    # exact ignore masking and counts
+    ign = tn == -100
+    assert torch.all(gx[ts == -100] == 0)
+    out = flce_fwd(xs, w, ts, reduction="none", chunk_rows=chunk, **opts)
+    loss_rows = out[0]
+    assert torch.all(loss_rows[ts == -100] == 0)
+    n_valid = int((~ign).sum())
+    scale = 1.0 / n_valid
+    ok, err = rel_close(loss_rows.double().cpu().numpy(), ref_rows / scale, 2e-2)
+    assert ok, ("loss rows", err)
+    # MEAN = SUM / the exact integer count of non-ignored targets
+    lsum = run(xs, w, ts, chunk_rows=chunk, reduction="sum", **opts)[0]
+    assert loss.item() == pytest.approx(lsum.item() / n_valid, rel=1e-6)
+
+
+@pytest.fixture(scope="module")
+def cfg2_batch():
+    x, w, t = headline_batch(8192, 4096, 128256, seed=0)
+    yield x, w, t
+    del x, w, t
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("lo,rows,chunk", [(0, 256, None), (4096, 384, 128), (8192 - 200, 200, 64)])
+def test_cfg2_row_slice_full_vocab_vs_oracle(cfg2_batch, lo, rows, chunk):
+    x, w, t = cfg2_batch
+    _slice_parity(x, w, t, lo, rows, chunk)
+
+
+@pytest.mark.parametrize("wscale", [64 / math.sqrt(3584), 30.0])
+@pytest.mark.parametrize("lo,rows,chunk", [(0, 256, None), (5000, 320, 128)])
+def test_cfg4_row_slice_full_vocab_vs_oracle(wscale, lo, rows, chunk):
+    """Gemma-2-9B head: softcap 30, label smoothing 0.1; typical weights (W ~ U(-1,1)/sqrt(H)) and
+    the stress scale (logit sigma ~ 10) so the tanh cap saturates."""
+    x, w, t = headline_batch(8192, 3584, 256000, seed=1, wscale=wscale)
+    _slice_parity(x, w, t, lo, rows, chunk, softcap=30.0, label_smoothing=0.1)
+    del x, w, t
+    torch.cuda.empty_cache()

@@ -5,6 +5,7 @@ import pytest
 import torch
 
 import paper_2410_10989_b200 as lk
+from paper_2410_10989_b200 import _capi
 from oracle import liger_ref, rowfuse_port as rp
 from tests.conftest import rel_close
 from tests.torch_ref import close
@@ -62,7 +63,7 @@ def test_rmsnorm_bf16_vs_oracle(mode, shape):
                                          ((37, 1000), torch.bfloat16), ((1000, 2048), torch.float32),
                                          ((513, 256), torch.float16), ((3, 64), torch.bfloat16)])
 @pytest.mark.parametrize("mode", ["llama", "gemma", "none"])
-def test_rmsnorm_default_matches_other_paths(impl, shape, dtype, mode, monkeypatch):
+def test_rmsnorm_default_matches_other_paths(impl, shape, dtype, mode):
     """Default (CTA register) kernels vs the TMA-ring, register-warp and generic kernels."""
     rows, cols = shape
     g = torch.Generator(device="cuda").manual_seed(rows * 7 + cols)
@@ -79,9 +80,8 @@ def test_rmsnorm_default_matches_other_paths(impl, shape, dtype, mode, monkeypat
         return y.detach().float(), xr.grad.float(), wr.grad.float()
 
     a = run(True)
-    monkeypatch.setenv("LK_NORM_IMPL", impl)
-    b = run(False)
-    monkeypatch.delenv("LK_NORM_IMPL")
+    with _capi.select_path(_capi.PATH_NORM_IMPL, {"warp": 1, "generic": 2, "ring": 3}[impl]):
+        b = run(False)
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     for name, u, v in zip(("y", "dx", "dw"), a, b):
         ok, err = rel_close(u.cpu().numpy(), v.cpu().numpy(), tol)
@@ -513,3 +513,29 @@ def test_rmsnorm_unaligned_views_vs_torch(mode):
     yf = xf * torch.rsqrt((xf * xf).mean(-1, keepdim=True) + 1e-6) * (off + wf)
     yf.backward(dy.float())
     assert close(y, yf, 2e-2) and close(xr.grad, xf.grad, 2e-2) and close(wr.grad, wf.grad, 2e-2)
+
+
+@pytest.mark.parametrize("xdt,wdt", [(torch.bfloat16, torch.float32), (torch.float32, torch.bfloat16),
+                                     (torch.float16, torch.float32)])
+@pytest.mark.parametrize("mode", ["llama", "gemma"])
+def test_rmsnorm_weight_dtype_differs_from_input(xdt, wdt, mode):
+    """A weight whose dtype differs from X (Liger accepts an fp32 weight with bf16 activations):
+    the weight is read in X's dtype and dW comes back in the weight's dtype."""
+    rows, cols = 300, 1000
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(xdt)
+    w = (torch.rand(cols, device="cuda", generator=g) + 0.5).to(wdt)
+    dy = (torch.rand(rows, cols, device="cuda", generator=g) * 2 - 1).to(xdt)
+    offset = 1.0 if mode == "gemma" else 0.0
+    xr, wr = x.clone().requires_grad_(True), w.clone().requires_grad_(True)
+    y = lk.liger_rms_norm(xr, wr, 1e-6, offset, mode, False)
+    y.backward(dy)
+    assert y.dtype == xdt and xr.grad.dtype == xdt and wr.grad.dtype == wdt
+    wq = w.to(xdt).double().cpu().numpy()  # the weight as the kernels read it
+    ry, _ = liger_ref.rmsnorm_fwd(x.double().cpu().numpy(), wq, 1e-6, offset)
+    rdx, _ = liger_ref.rmsnorm_bwd(dy.double().cpu().numpy(), x.double().cpu().numpy(), wq, 1e-6, offset)
+    assert rel_close(y.float().detach().cpu().numpy(), ry, 2e-2)[0]
+    assert rel_close(xr.grad.float().cpu().numpy(), rdx, 2e-2)[0]
+    xf, dyf = x.double(), dy.double()
+    rdw = (dyf * xf * torch.rsqrt((xf * xf).mean(1, keepdim=True) + 1e-6)).sum(0)
+    assert close(wr.grad.double(), rdw, 2e-2)

@@ -284,3 +284,35 @@ def test_liger_ref_class_weights_match_torch(reduction, ls):
     ref.sum().backward()
     np.testing.assert_allclose(loss, ref.detach().numpy(), rtol=1e-12)
     np.testing.assert_allclose(g, zt.grad.numpy(), rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(reduction="sum"), dict(reduction="none"), dict(label_smoothing=0.1),
+                                  dict(softcap=3.0), dict(softcap=5.0, label_smoothing=0.1, lse_square_scale=1e-3),
+                                  dict(bias=True)])
+def test_torch_ref_pinned_to_liger_oracle(opts):
+    """tests/torch_ref.flce_ref (the checker at full BASELINE sizes, run in fp32 on the GPU) is the
+    same math as the pinned float64 oracle: in float64 on CPU it matches liger_ref.flce to
+    round-off, chunked and unchunked, so the full-size GPU checks inherit the oracle's pin."""
+    import torch
+
+    from tests.torch_ref import flce_ref
+
+    rng = np.random.default_rng(11)
+    bt, h, v = 37, 16, 53
+    x = rng.uniform(-1, 1, (bt, h))
+    w = rng.uniform(-1, 1, (v, h)) * 1.5
+    t = rng.integers(0, v, bt)
+    t[rng.random(bt) < 0.2] = -100
+    kw = dict(opts)
+    b = rng.normal(size=v) if kw.pop("bias", False) else None
+    ref_loss, ref_rows, _, rgx, rgw, rgb = liger_ref.flce(x, w, t, bias=b, **kw)
+    for chunk in (5, 2048):
+        loss, rows, gx, gw, gb = flce_ref(torch.tensor(x), torch.tensor(w), torch.tensor(t),
+                                          bias=None if b is None else torch.tensor(b), chunk=chunk,
+                                          compute_dtype=torch.float64, **kw)
+        np.testing.assert_allclose(loss.numpy(), ref_loss, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(rows.numpy(), ref_rows, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(gx.numpy(), rgx, rtol=1e-10, atol=1e-14)
+        np.testing.assert_allclose(gw.numpy(), rgw, rtol=1e-10, atol=1e-14)
+        if b is not None:
+            np.testing.assert_allclose(gb.numpy(), rgb, rtol=1e-10, atol=1e-14)

@@ -28,7 +28,8 @@ def ce_grad(z, t, ignore_index=-100, label_smoothing=0.0, lse_square_scale=0.0, 
     loss = (loss + zl) * scale
     p = torch.softmax(zc, dim=1)
     g = p * (1 + 2 * lse_square_scale * lse[:, None]) - eps
-    g.scatter_add_(1, tsafe[:, None], torch.where(valid, -(1 - label_smoothing), 0.0)[:, None].to(g.dtype))
+    hit = torch.full_like(lse, -(1 - label_smoothing)).masked_fill(~valid, 0.0)  # in z's dtype
+    g.scatter_add_(1, tsafe[:, None], hit[:, None])
     g = g * scale
     if th is not None:
         g = g * (1 - th * th)
@@ -38,21 +39,23 @@ def ce_grad(z, t, ignore_index=-100, label_smoothing=0.0, lse_square_scale=0.0, 
 
 
 def flce_ref(x, w, t, bias=None, ignore_index=-100, label_smoothing=0.0, lse_square_scale=0.0, softcap=None,
-             reduction="mean", chunk=2048):
-    """fp32 (loss, loss_rows, grad_x, grad_w, grad_bias) from (possibly bf16) inputs."""
-    xf, wf = x.float(), w.float()
+             reduction="mean", chunk=2048, compute_dtype=torch.float32):
+    """(loss, loss_rows, grad_x, grad_w, grad_bias) in `compute_dtype` (fp32 on the GPU for the
+    full-size checks) from (possibly bf16) inputs.  Pinned to oracle.liger_ref by
+    tests/test_oracle.py::test_torch_ref_pinned_to_liger_oracle (float64 on CPU)."""
+    xf, wf = x.to(compute_dtype), w.to(compute_dtype)
     bt = x.shape[0]
     n = int((t != ignore_index).sum())
     scale = 1.0 / max(n, 1) if reduction == "mean" else 1.0
     gx = torch.empty_like(xf)
     gw = torch.zeros_like(wf)
-    gb = torch.zeros(w.shape[0], device=x.device) if bias is not None else None
-    rows = torch.empty(bt, device=x.device)
+    gb = torch.zeros(w.shape[0], device=x.device, dtype=compute_dtype) if bias is not None else None
+    rows = torch.empty(bt, device=x.device, dtype=compute_dtype)
     for lo in range(0, bt, chunk):
         hi = min(lo + chunk, bt)
         z = xf[lo:hi] @ wf.t()
         if bias is not None:
-            z += bias.float()
+            z += bias.to(compute_dtype)
         l, g = ce_grad(z, t[lo:hi], ignore_index, label_smoothing, lse_square_scale, softcap, scale)
         rows[lo:hi] = l
         gx[lo:hi] = g @ wf
