@@ -182,7 +182,7 @@ typedef struct {
   void* workspace;
   size_t workspace_bytes;
   void* stream;
-  int force_simt;         /* 1: use the SIMT GEMM path (debug/fp32)            */
+  int force_simt;         /* 1: the SIMT FFMA GEMMs (test reference for fp32)   */
   /* Token-sharded mode: device int64 holding the GLOBAL non-ignored count used as
    * the MEAN denominator (all-reduced by the caller); NULL = local count. */
   const int64_t* mean_count;
@@ -217,7 +217,18 @@ typedef struct {
    * targets' weights (the weighted MEAN denominator, all-reduced by the caller); NULL =
    * local sum. */
   const float* mean_weight_sum;
+  /* fp32 inputs (dtype LK_F32): the GEMMs run on the bf16 tensor cores on operands split
+   * into this many bf16 pieces (csrc/split.cu): 2 (default when 0) = 3 piece products per
+   * product (relative error ~2^-16 per product, below fp32's own accumulation bound at
+   * K >= 256), 3 = 6 products (fp32-exact products).  Ignored for 16-bit dtypes and with
+   * force_simt. */
+  int fp32_pieces;
 } lk_flce_args;
+
+/* Workspace bytes for exactly this call (every field that sizes the workspace is read:
+ * bt, hidden, vocab, dtype, chunk_rows, grad_w, grad_bias, grad_w_accum, force_simt,
+ * fp32_pieces; pointers may be NULL). */
+size_t lk_flce_workspace_bytes_for(const lk_flce_args* args);
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };
 #define LK_ACCUM_AUTO_MAX_CHUNKS 8

@@ -70,6 +70,7 @@ class FlceArgs(C.Structure):
         ("use_token_scaling", c_int),
         ("ce_weight", c_void),
         ("mean_weight_sum", c_void),
+        ("fp32_pieces", c_int),
     ]
 
 
@@ -98,6 +99,7 @@ SIGNATURES: dict[str, tuple] = {
     "lk_flce_plan": (c_int, [c_i64, c_i64, c_i64, c_int, c_i64p, c_i64p]),
     "lk_flce_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_int, c_i64, c_int]),
     "lk_flce_forward_backward": (c_int, [C.POINTER(FlceArgs)]),
+    "lk_flce_workspace_bytes_for": (c_size, [C.POINTER(FlceArgs)]),
     "lk_flce_vp_workspace_bytes": (c_size, [c_i64, c_i64, c_i64, c_int]),
     "lk_flce_vp_logits": (
         c_int,

@@ -331,6 +331,10 @@ int launch_vp_row_stats(const void* x, int64_t ld, int64_t rows, int64_t n_cols,
                         float4* out, cudaStream_t st);
 // dst[i] = dtype(src[i]) for n fp32 values (the multi-chunk dW accumulator -> grad_w).
 int launch_cast_f32(const float* src, void* dst, int64_t n, int dtype, cudaStream_t st);
+// fp32 -> n_terms bf16 piece copies (split.cu): dst + row*row_stride + t*term_stride + col
+int launch_split_bf16(const float* src, int64_t rows, int64_t cols, int64_t ld_src, int64_t rows_pad,
+                      int64_t cols_pad, void* dst, int64_t row_stride, int64_t term_stride, int n_terms,
+                      const int* order, cudaStream_t st);
 int launch_colsum_rows(const void* x, int64_t rows, int64_t cols, int64_t ld, int dtype,
                        void* out, int out_dtype, int accumulate, cudaStream_t st);
 

@@ -205,8 +205,28 @@ static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dt
 struct FlceLayout {
   int64_t C, nchunks, ldz, nparts;
   bool tc, need_acc, need_bias_acc;
-  size_t off_counts, off_sched, off_z, off_parts, off_tgt, off_acc, off_bias, total;
+  // fp32 inputs on the bf16 tensor cores (split operands, csrc/split.cu)
+  bool tc32;
+  int pieces, nT;
+  size_t off_counts, off_sched, off_z, off_parts, off_tgt, off_acc, off_bias;
+  size_t off_wk, off_wmn, off_xs, off_dzs;  // W' [V][nT][H], W'' [nT][ldz][H], X'_c [C][nT][H], dZ' [C][nT][ldz]
+  size_t total;
 };
+
+// Term orders of the split GEMMs: term t pairs piece A_ORD[t] of X (and of W in the dX GEMM)
+// with piece C_ORD[t] of W in the logits GEMM (and of dZ in both backward GEMMs); the pairs
+// enumerate i + j <= pieces - 1.
+static const int kOrdA2[3] = {0, 0, 1}, kOrdC2[3] = {0, 1, 0};
+static const int kOrdA3[6] = {0, 0, 1, 0, 1, 2}, kOrdC3[6] = {0, 1, 0, 2, 1, 0};
+
+static bool use_tc32_path(int dtype, int64_t hidden, int force_simt) {
+#ifdef LK_HAS_TCGEN05
+  return dtype == LK_F32 && !force_simt && hidden % 8 == 0;
+#else
+  (void)dtype; (void)hidden; (void)force_simt;
+  return false;
+#endif
+}
 
 static bool use_tc_path(int dtype, int64_t hidden, const void* x, const void* w, int force_simt) {
 #ifdef LK_HAS_TCGEN05
@@ -230,8 +250,12 @@ static bool wdtype_accum(int mode, int dtype, int64_t nchunks, bool tc) {
 }
 
 static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t chunk_rows,
-                              bool has_grad_w, bool has_bias_grad, bool tc, int accum_mode) {
+                              bool has_grad_w, bool has_bias_grad, bool tc, int accum_mode, bool tc32 = false,
+                              int pieces = 2, bool has_grad_x = true) {
   FlceLayout L{};
+  L.tc32 = tc32;
+  L.pieces = pieces == 3 ? 3 : 2;
+  L.nT = L.pieces == 3 ? 6 : 3;
   L.C = chunk_rows > 0 ? chunk_rows : b200_chunk_rows(bt, hidden, vocab, dtype);
   L.C = std::max<int64_t>(1, std::min<int64_t>(L.C, std::max<int64_t>(bt, 1)));
   L.nchunks = bt > 0 ? (bt + L.C - 1) / L.C : 0;
@@ -245,10 +269,15 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   L.off_counts = take(4 * sizeof(int64_t));  // n_valid, n_out_of_range, class-weight sum
   L.off_sched = take((size_t)(2 * L.nchunks + 2 + 16) * sizeof(int));  // + per-slice counters
   L.off_z = take((size_t)L.C * L.ldz * elt_size(dtype));
-  L.off_parts = take(tc ? (size_t)L.C * L.nparts * sizeof(float4) : 0);
-  L.off_tgt = take(tc ? (size_t)L.C * sizeof(float) : 0);
+  L.off_parts = take((tc || tc32) ? (size_t)L.C * L.nparts * sizeof(float4) : 0);
+  L.off_tgt = take((tc || tc32) ? (size_t)L.C * sizeof(float) : 0);
   L.off_acc = take(L.need_acc ? (size_t)vocab * hidden * sizeof(float) : 0);
   L.off_bias = take(L.need_bias_acc ? (size_t)vocab * sizeof(float) : 0);
+  const size_t nT = (size_t)L.nT;
+  L.off_wk = take(tc32 ? (size_t)vocab * nT * hidden * 2 : 0);
+  L.off_wmn = take(tc32 && has_grad_x ? nT * (size_t)L.ldz * hidden * 2 : 0);
+  L.off_xs = take(tc32 ? (size_t)L.C * nT * hidden * 2 : 0);
+  L.off_dzs = take(tc32 ? (size_t)L.C * nT * L.ldz * 2 : 0);
   L.total = align_up(off, 1024);
   return L;
 }
@@ -270,13 +299,27 @@ extern "C" int lk_flce_plan(int64_t bt, int64_t hidden, int64_t vocab, int dtype
 extern "C" size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
                                           int64_t chunk_rows, int has_grad_w) {
   bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
-  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, LK_ACCUM_AUTO).total;
+  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, LK_ACCUM_AUTO,
+                     use_tc32_path(dtype, hidden, 0), 2, true).total;
 }
 
 extern "C" size_t lk_flce_workspace_bytes_ex(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
                                              int64_t chunk_rows, int has_grad_w, int grad_w_accum) {
   bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
-  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, grad_w_accum).total;
+  return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, grad_w_accum,
+                     use_tc32_path(dtype, hidden, 0), 2, true).total;
+}
+
+static FlceLayout layout_for(const lk_flce_args* a) {
+  const bool tc = use_tc_path(a->dtype, a->hidden, a->x, a->weight, a->force_simt);
+  const bool tc32 = use_tc32_path(a->dtype, a->hidden, a->force_simt);
+  return flce_layout(a->bt, a->hidden, a->vocab, a->dtype, a->chunk_rows, a->grad_w != nullptr,
+                     a->grad_bias != nullptr, tc, a->grad_w_accum, tc32, a->fp32_pieces, a->grad_x != nullptr);
+}
+
+extern "C" size_t lk_flce_workspace_bytes_for(const lk_flce_args* a) {
+  if (!a) return 0;
+  return layout_for(a).total;
 }
 
 extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
@@ -295,12 +338,21 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   const bool want_grad = a->grad_x || a->grad_w || a->grad_bias;
   LK_REQUIRE(a->grad_w_accum >= LK_ACCUM_AUTO && a->grad_w_accum <= LK_ACCUM_WEIGHT_DTYPE, LK_INVALID_ARGUMENT,
              "bad grad_w_accum");
-  FlceLayout L = flce_layout(BT, H, V, dt, a->chunk_rows, a->grad_w != nullptr, a->grad_bias != nullptr, tc,
-                             a->grad_w_accum);
+  LK_REQUIRE(a->fp32_pieces == 0 || a->fp32_pieces == 2 || a->fp32_pieces == 3, LK_INVALID_ARGUMENT,
+             "fp32_pieces must be 0 (default), 2 or 3");
+  FlceLayout L = layout_for(a);
+  const bool tc32 = L.tc32;
   const bool wacc = a->grad_w && wdtype_accum(a->grad_w_accum, dt, L.nchunks, tc);
   LK_REQUIRE(a->workspace && a->workspace_bytes >= L.total, LK_INVALID_ARGUMENT,
              "workspace too small: need " + std::to_string(L.total) + " bytes");
   char* ws = static_cast<char*>(a->workspace);
+  const int* ordA = L.pieces == 3 ? kOrdA3 : kOrdA2;
+  const int* ordC = L.pieces == 3 ? kOrdC3 : kOrdC2;
+  const int64_t nT = L.nT;
+  void* wk = ws + L.off_wk;    // W'  [V][nT][H]       logits B (K-major), pieces in C order
+  void* wmn = ws + L.off_wmn;  // W'' [nT][ldz][H]     dX B (MN-major, K' = t*ldz + v), A order
+  void* xs = ws + L.off_xs;    // X'_c [r][nT][H]      logits A (K-major) / dW B (MN-major, K' = row*nT + t), A order
+  void* dzs = ws + L.off_dzs;  // dZ' [r][nT][ldz]     dX A (K-major) / dW A (MN-major), C order
   int64_t* counts = reinterpret_cast<int64_t*>(ws + L.off_counts);
   int* sched = reinterpret_cast<int*>(ws + L.off_sched);
   void* zbuf = ws + L.off_z;
@@ -326,7 +378,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
                            V, wls ? reinterpret_cast<float*>(counts + 3) : nullptr);
     if (rc) return rc;
   }
-  if (tc) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
+  if (tc || tc32) LK_CUDA(cudaMemsetAsync(sched, 0, (size_t)(2 * L.nchunks + 2 + 16) * sizeof(int), st));
   // grad_w slice events: the caller all-reduces slice s once event s fires, so EVERY event is
   // recorded on `st` after the work that finalises its rows on every path (sliced tcgen05 last
   // chunk: after each slice; otherwise -- SIMT, BT == 0, unsupported slice counts -- after all
@@ -346,11 +398,25 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     return record_rest();
   }
 
+  if (tc32) {  // split W once per call: W' for the logits GEMM, W'' (zero-padded to ldz rows) for dX
+    ProfScope ps(3, st);
+    rc = launch_split_bf16(static_cast<const float*>(a->weight), V, H, H, V, H, wk, nT * H, H, (int)nT, ordC, st);
+    if (!rc && a->grad_x)
+      rc = launch_split_bf16(static_cast<const float*>(a->weight), V, H, H, L.ldz, H, wmn, H, L.ldz * H, (int)nT,
+                             ordA, st);
+    if (rc) return rc;
+  }
+
   for (int64_t ci = 0; ci < L.nchunks; ++ci) {
     const int64_t lo = ci * L.C;
     const int64_t r = std::min(L.C, BT - lo);
     const char* xc = static_cast<const char*>(a->x) + lo * H * es;
     const bool first = ci == 0, last = ci == L.nchunks - 1;
+    if (tc32) {
+      ProfScope ps(3, st);
+      rc = launch_split_bf16(reinterpret_cast<const float*>(xc), r, H, H, r, H, xs, nT * H, H, (int)nT, ordA, st);
+      if (rc) return rc;
+    }
 
     // ---- 1. logits ----
     EpiArgs le{};
@@ -368,6 +434,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         // n-fastest measured 15% slower, profiles/README.md)
         P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
+      } else if (tc32) {  // fp32 logits = sum of the piece products, K' = nT * H
+        tc::TmaOperand A{xs, nT * H, r, nT * H, 0}, B{wk, nT * H, V, nT * H, 0};
+        tc::Problem P{};
+        P.M = r; P.N = V; P.K = nT * H; P.n_fast = 0; P.epi = le;
+        rc = tc::launch_tc_gemm(&A, &B, &P, 1, LK_BF16, sched + 2 * ci, st);
       } else {
         Operand A{xc, H, 1}, B{a->weight, H, 1};
         rc = launch_simt_gemm(A, B, r, V, H, dt, le, st);
@@ -390,10 +461,10 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
                           : a->mean_weight_sum ? a->mean_weight_sum : reinterpret_cast<const float*>(counts + 2);
     ce.weight_total = wls ? reinterpret_cast<const float*>(counts + 3) : nullptr;
     ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
-    if (tc) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
+    if (tc || tc32) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {
       ProfScope ps(1, st);
-      rc = tc && path_knob(LK_PATH_FLCE_FINALIZE) == 0 ? launch_ce_ring(ce, dt, st) : LK_UNSUPPORTED;
+      rc = (tc || tc32) && path_knob(LK_PATH_FLCE_FINALIZE) == 0 ? launch_ce_ring(ce, dt, st) : LK_UNSUPPORTED;
       if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dt, st);
     }
     if (rc) return rc;
@@ -429,28 +500,46 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
       const bool fold = last && !separate_cast();
       we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = fold ? 1 : 0;
     }
+    if (tc32) {  // dZ (fp32, in the chunk buffer) -> dZ' pieces, zero-padded to ldz columns
+      ProfScope ps(3, st);
+      rc = launch_split_bf16(static_cast<const float*>(zbuf), r, V, L.ldz, r, L.ldz, dzs, nT * L.ldz, L.ldz,
+                             (int)nT, ordC, st);
+      if (rc) return rc;
+      xe.kind = EPI_F32;  // dX in fp32 straight from the accumulator
+    }
     ProfScope ps_bwd(2, st);
-    if (tc) {
+    if (tc || tc32) {
+      const int gdt = tc32 ? LK_BF16 : dt;
+      // operands of the two backward problems: bf16 chunk / X for 16-bit inputs, the split
+      // pieces (K' = nT * V for dX, K' = nT * r for dW) for fp32 inputs
+      const tc::TmaOperand dxA = tc32 ? tc::TmaOperand{dzs, nT * L.ldz, r, nT * L.ldz, 0}
+                                      : tc::TmaOperand{zbuf, V, r, L.ldz, 0};
+      const tc::TmaOperand dxB = tc32 ? tc::TmaOperand{wmn, H, nT * L.ldz, H, 1} : tc::TmaOperand{a->weight, H, V, H, 1};
+      const int64_t dxK = tc32 ? nT * L.ldz : V;
+      const int64_t dwK = tc32 ? nT * r : r;
+      const void* dwA_base = tc32 ? dzs : zbuf;
+      const int64_t dwA_ld = tc32 ? L.ldz : L.ldz;
+      const void* dwB_base = tc32 ? xs : xc;
       tc::TmaOperand As[2], Bs[2];
       tc::Problem Ps[2];
       int np = 0;
       if (a->grad_x) {
-        As[np] = {zbuf, V, r, L.ldz, 0};
-        Bs[np] = {a->weight, H, V, H, 1};
+        As[np] = dxA;
+        Bs[np] = dxB;
         Ps[np] = tc::Problem{};
-        Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
+        Ps[np].M = r; Ps[np].N = H; Ps[np].K = dxK; Ps[np].n_fast = 0; Ps[np].epi = xe;
         ++np;
       }
       const int slices =
           (last && a->grad_w && n_events >= 2 && n_events <= LK_MAX_GRAD_W_SLICES) ? n_events : 1;
       if (a->grad_w && slices <= 1) {
-        As[np] = {zbuf, V, r, L.ldz, 1};
-        Bs[np] = {xc, H, r, H, 1};
+        As[np] = {dwA_base, V, dwK, dwA_ld, 1};
+        Bs[np] = {dwB_base, H, dwK, H, 1};
         Ps[np] = tc::Problem{};
-        Ps[np].M = V; Ps[np].N = H; Ps[np].K = r; Ps[np].n_fast = 1; Ps[np].epi = we;
+        Ps[np].M = V; Ps[np].N = H; Ps[np].K = dwK; Ps[np].n_fast = 1; Ps[np].epi = we;
         ++np;
       }
-      if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, dt, sched + 2 * ci + 1, st);
+      if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, gdt, sched + 2 * ci + 1, st);
       // token-sharded overlap: the last chunk's dW in vocab-row slices, one event per slice
       const int64_t step = (V + slices - 1) / slices;
       const int64_t sl_rows = (step + 255) / 256 * 256;
@@ -461,11 +550,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
           ws.out = static_cast<char*>(a->grad_w) + v0 * H * es;
           if (ws.acc) ws.acc = ws.acc + v0 * H;
           ws.M = v1 - v0;
-          tc::TmaOperand As1{static_cast<const char*>(zbuf) + v0 * es, v1 - v0, r, L.ldz, 1};
-          tc::TmaOperand Bs1{xc, H, r, H, 1};
+          tc::TmaOperand As1{static_cast<const char*>(dwA_base) + v0 * (tc32 ? 2 : es), v1 - v0, dwK, dwA_ld, 1};
+          tc::TmaOperand Bs1{dwB_base, H, dwK, H, 1};
           tc::Problem P1{};
-          P1.M = v1 - v0; P1.N = H; P1.K = r; P1.n_fast = 1; P1.epi = ws;
-          rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, dt, sched + 2 * L.nchunks + 2 + sl, st);
+          P1.M = v1 - v0; P1.N = H; P1.K = dwK; P1.n_fast = 1; P1.epi = ws;
+          rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, gdt, sched + 2 * L.nchunks + 2 + sl, st);
         }
         if (!rc) {
           LK_CUDA(cudaEventRecord(static_cast<cudaEvent_t>(a->grad_w_slice_events[sl]), st));

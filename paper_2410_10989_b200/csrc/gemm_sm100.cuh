@@ -224,7 +224,9 @@ __device__ __forceinline__ void store32(T* dst, const float (&v)[32]) {
   }
 }
 
-template <typename T>
+// OutT = the chunk buffer's type: T (16-bit logits) or float (fp32 FLCE on split operands,
+// where the partials come from the unrounded fp32 logits).
+template <typename T, typename OutT = T>
 __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64_t n0, int n_blk,
                                            uint32_t taddr) {
   const bool row_ok = grow < e.M;
@@ -239,8 +241,8 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
   bool have_t = false;
   float best_v = -INFINITY;
   int best_i = 0;
-  T* orow = static_cast<T*>(e.out) + grow * e.ldo;
-  const bool vec_ok = (e.ldo % 8) == 0;
+  OutT* orow = static_cast<OutT*>(e.out) + grow * e.ldo;
+  const bool vec_ok = (e.ldo % (16 / sizeof(OutT))) == 0;
 #pragma unroll 1
   for (int c = 0; c < BN / 32; ++c) {
     uint32_t r[32];
@@ -255,8 +257,8 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
     for (int j = 0; j < 32; ++j) {
       float z = __uint_as_float(r[j]);
       if (e.bias && j < nvalid) z += load_any(e.bias, col0 + j, e.out_dtype);
-      if (cap) z = e.softcap * tanh_fast(z * inv_cap);
-      v[j] = round_to<T>(z);
+      if (cap) z = sizeof(OutT) == 4 ? e.softcap * tanhf(z * inv_cap) : e.softcap * tanh_fast(z * inv_cap);
+      v[j] = round_to<OutT>(z);
     }
     float cm = -INFINITY;
 #pragma unroll
@@ -285,9 +287,9 @@ __device__ __forceinline__ void epi_logits(const EpiArgs& e, int64_t grow, int64
       have_t = true;
     }
     if (nvalid == 32 && vec_ok) {
-      store32<T>(orow + col0, v);
+      store32<OutT>(orow + col0, v);
     } else {
-      for (int j = 0; j < nvalid; ++j) orow[col0 + j] = from_f<T>(v[j]);
+      for (int j = 0; j < nvalid; ++j) orow[col0 + j] = from_f<OutT>(v[j]);
     }
   }
   if (row_ok) {
@@ -688,7 +690,10 @@ __device__ __forceinline__ void run_epilogue(const Problem& P, uint64_t omap, St
     return;
   }
   switch (e.kind) {
-    case EPI_LOGITS: epi_logits<T>(e, grow, n0, n_blk, taddr); break;
+    case EPI_LOGITS:
+      if (e.out_dtype == LK_F32) epi_logits<T, float>(e, grow, n0, n_blk, taddr);
+      else epi_logits<T>(e, grow, n0, n_blk, taddr);
+      break;
     case EPI_STORE: epi_store<T>(e, grow, n0, taddr); break;
     case EPI_ACCUM: epi_accum<T>(e, grow, n0, taddr); break;
     default: epi_f32<T>(e, grow, n0, taddr); break;

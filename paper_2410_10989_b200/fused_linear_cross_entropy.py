@@ -73,6 +73,7 @@ def fused_linear_cross_entropy_forward(
     grad_w_slice_events=None,
     mean_weight_sum: Optional[torch.Tensor] = None,
     check_targets: bool = True,
+    fp32_pieces: int = 0,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -86,6 +87,9 @@ def fused_linear_cross_entropy_forward(
     non-ignored count (token-sharded mode).  `grad_w_slice_events` (list of torch.cuda.Event)
     splits the last chunk's grad_w GEMM into that many vocab-row slices and records event s
     when slice s of grad_w is final (overlap of the token-sharded dW all-reduce).
+    fp32 inputs run on the bf16 tensor cores on split operands (`fp32_pieces` bf16 pieces
+    per value: 0/2 = 3 piece products, 3 = 6; include/liger_b200.h); `force_simt=True` runs
+    the SIMT FFMA GEMMs instead (the test reference).
     `check_targets=False` skips the host read of the device-side out-of-range count (the one
     host sync of the call); the caller then owns the check (token_sharded_flce does it on the
     all-reduced count after enqueueing its collectives).
@@ -135,6 +139,8 @@ def fused_linear_cross_entropy_forward(
     L = lib()
     dt = dtype_code(x)
     cr = int(chunk_rows or 0)
+    if fp32_pieces not in (0, 2, 3):
+        raise ValueError(f"fp32_pieces must be 0 (default), 2 or 3. Got: {fp32_pieces}")
     if force_simt:
         accum = _capi.LK_ACCUM_FP32  # the SIMT (fp32 parity) GEMM accumulates dW in an fp32 workspace
     elif accum_dtype is None:
@@ -145,20 +151,21 @@ def fused_linear_cross_entropy_forward(
         accum = _capi.LK_ACCUM_WEIGHT_DTYPE
     else:
         raise errors.UnsupportedOption(f"accum_dtype {accum_dtype}: use None, torch.float32 or the weight dtype")
-    ws = workspace(L.lk_flce_workspace_bytes_ex(bt, h, v, dt, cr, int(grad_w is not None), accum), dev)
     args = _capi.FlceArgs(
         x=ptr(x), weight=ptr(w), target=ptr(t), bias=ptr(b), bt=bt, hidden=h, vocab=v, dtype=dt,
         ignore_index=int(ignore_index), label_smoothing=float(label_smoothing),
         lse_square_scale=float(lse_square_scale), softcap=float(softcap) if softcap is not None else 0.0,
         reduction=_capi.REDUCTIONS[reduction], chunk_rows=cr, loss_rows=ptr(loss_rows), loss_sum=ptr(loss_sum),
         z_loss_rows=ptr(z_rows), z_loss_sum=ptr(z_sum), grad_x=ptr(grad_x), grad_w=ptr(grad_w),
-        grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=ptr(ws), workspace_bytes=ws.numel(),
-        stream=stream_of(x), force_simt=int(bool(force_simt)),
+        grad_bias=ptr(grad_b), target_stats=ptr(stats), workspace=None, workspace_bytes=0,
+        stream=stream_of(x), force_simt=int(bool(force_simt)), fp32_pieces=int(fp32_pieces or 0),
         mean_count=ptr(mean_count) if mean_count is not None else None, grad_w_accum=accum,
         token_correct_rows=ptr(correct), predicted_tokens=ptr(pred), use_token_scaling=int(bool(use_token_scaling)),
         ce_weight=ptr(cw),
         mean_weight_sum=ptr(mean_weight_sum) if mean_weight_sum is not None else None,
     )
+    ws = workspace(L.lk_flce_workspace_bytes_for(_capi.C.byref(args)), dev)  # sized for exactly this call
+    args.workspace, args.workspace_bytes = ptr(ws), ws.numel()
     ev_arr = None
     if grad_w_slice_events:
         for ev in grad_w_slice_events:  # torch creates the CUDA event lazily on first record

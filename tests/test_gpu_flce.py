@@ -297,13 +297,14 @@ def test_cfg4_gemma2_head_softcap_smoothing():
     assert loss.item() == loss2.item() and torch.equal(gx, gx2) and torch.equal(gw, gw2)
 
 
-@pytest.mark.parametrize("simt", [False, True])
+@pytest.mark.parametrize("path", ["bf16", "fp32_simt", "fp32_tc"])
 @pytest.mark.parametrize("kw", [dict(), dict(softcap=30.0, label_smoothing=0.1)])
-def test_flce_token_accuracy_and_predicted_tokens(simt, kw):
+def test_flce_token_accuracy_and_predicted_tokens(path, kw):
     """Liger return_token_accuracy / return_predicted_tokens on the FLCE head (argmax of the rounded,
-    softcapped logits; the tcgen05 path tracks it in the logits epilogue, no extra pass)."""
+    softcapped logits; the tcgen05 paths track it in the logits epilogue, no extra pass)."""
     xb, wb, tb, x, w, t = bf16_problem(700, 256, 5000, seed=21)
-    if simt:
+    simt = path == "fp32_simt"
+    if path != "bf16":
         xb, wb = xb.float(), wb.float()
     logits = xb.float() @ wb.float().T
     if "softcap" in kw:

@@ -146,3 +146,52 @@ def test_cfg4_row_slice_full_vocab_vs_oracle(wscale, lo, rows, chunk):
     _slice_parity(x, w, t, lo, rows, chunk, softcap=30.0, label_smoothing=0.1)
     del x, w, t
     torch.cuda.empty_cache()
+
+
+# ------------------------------------------- fp32 on the bf16 tensor cores (split operands)
+@pytest.mark.parametrize("pieces", [0, 3])
+@pytest.mark.parametrize("opts", [dict(), dict(label_smoothing=0.1, softcap=30.0, lse_square_scale=1e-4),
+                                  dict(reduction="sum", chunk_rows=300), dict(bias=True)])
+def test_fp32_split_tensor_core_path_vs_oracle_and_simt(pieces, opts):
+    """fp32 FLCE runs its GEMMs on the bf16 tensor cores over split operands (csrc/split.cu);
+    it matches the float64 oracle at the fp32 tolerance (rtol 1e-4) and the SIMT FFMA path."""
+    rng = np.random.default_rng(3)
+    bt, h, v = 700, 264, 5003  # ragged: H % 64 != 0, V % 64 != 0, BT not a chunk multiple
+    x = rng.uniform(-1, 1, (bt, h)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (v, h)) / math.sqrt(h) * 4).astype(np.float32)
+    t = rng.integers(0, v, bt)
+    t[rng.random(bt) < 0.1] = -100
+    kw = dict(opts)
+    b = rng.normal(size=v).astype(np.float32) if kw.pop("bias", False) else None
+    ref_kw = {k: val for k, val in kw.items() if k != "chunk_rows"}
+    ref_loss, _, _, rgx, rgw, rgb = liger_ref.flce(x.astype(np.float64), w.astype(np.float64), t,
+                                                   bias=None if b is None else b.astype(np.float64), **ref_kw)
+    xd, wd, td = (torch.tensor(x, device="cuda"), torch.tensor(w, device="cuda"), torch.tensor(t, device="cuda"))
+    bd = None if b is None else torch.tensor(b, device="cuda")
+    outs = {}
+    for name, extra in (("tc", dict(fp32_pieces=pieces)), ("simt", dict(force_simt=True))):
+        loss, _, _, _, gx, gw, gb = flce_fwd(xd, wd, td, bias=bd, compute_grad_input=True, compute_grad_weight=True,
+                                             **kw, **extra)
+        torch.cuda.synchronize()
+        outs[name] = (loss, gx, gw, gb)
+        assert loss.item() == pytest.approx(ref_loss, rel=1e-4), name
+        assert rel_close(gx.double().cpu().numpy(), rgx, 1e-4)[0], (name, "dx")
+        assert rel_close(gw.double().cpu().numpy(), rgw, 1e-4)[0], (name, "dw")
+        if b is not None:
+            assert rel_close(gb.double().cpu().numpy(), rgb, 1e-4)[0], (name, "db")
+        assert torch.all(gx[td == -100] == 0)
+    assert rel_close(outs["tc"][1].cpu().numpy(), outs["simt"][1].cpu().numpy(), 1e-4)[0]
+
+
+def test_fp32_cfg2_row_slice_full_vocab_vs_oracle():
+    """fp32 at the Llama-3-8B head's full H and V (split-operand tensor-core path), 256 rows."""
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.rand(256, 4096, device="cuda", generator=g) * 2 - 1
+    w = (torch.rand(128256, 4096, device="cuda", generator=g) * 2 - 1) / 64.0
+    t = torch.randint(0, 128256, (256,), device="cuda", generator=g)
+    t[torch.rand(256, device="cuda", generator=g) < 0.1] = -100
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x.double().cpu().numpy(), w.double().cpu().numpy(), t.cpu().numpy())
+    loss, gx, gw = run(x, w, t)
+    assert loss.item() == pytest.approx(ref_loss, rel=1e-4)
+    assert rel_close(gx.double().cpu().numpy(), rgx, 1e-4)[0]
+    assert rel_close(gw.double().cpu().numpy(), rgw, 1e-4)[0]
