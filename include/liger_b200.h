@@ -218,10 +218,11 @@ typedef struct {
    * local sum. */
   const float* mean_weight_sum;
   /* fp32 inputs (dtype LK_F32): the GEMMs run on the bf16 tensor cores on operands split
-   * into this many bf16 pieces (csrc/split.cu): 2 (default when 0) = 3 piece products per
-   * product (relative error ~2^-16 per product, below fp32's own accumulation bound at
-   * K >= 256), 3 = 6 products (fp32-exact products).  Ignored for 16-bit dtypes and with
-   * force_simt. */
+   * into this many bf16 pieces (csrc/split.cu): 3 (default when 0) = 6 piece products per
+   * product (products exact to fp32's 2^-24), 2 = 3 products (~2^-16 per product: faster,
+   * below the fp32 tolerance on long training runs).  The long-K dX GEMM accumulates in
+   * segments added in fp32 (the tensor core's own accumulator truncates).  Ignored for
+   * 16-bit dtypes and with force_simt. */
   int fp32_pieces;
 } lk_flce_args;
 

@@ -130,6 +130,8 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     rc = encode_operand(&maps[2 * p + 1], b[p], dtype, b_rows_in_box, &P.b_mode);
     if (rc) return rc;
     P.tma_out = register_epilogue ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
+    // segmented accumulation needs the fp32 TMA store / reduce-add epilogue
+    if (P.seg_kb > 0 && (!P.tma_out || P.epi.kind != EPI_F32 || P.seg_kb >= P.k_blocks)) P.seg_kb = 0;
     args.prob[p] = P;
     args.idesc[p] = cta_group == 2 ? tc2::make_idesc2(dtype, a[p].mn_major, b[p].mn_major)
                                    : make_idesc(dtype, a[p].mn_major, b[p].mn_major);
@@ -217,6 +219,9 @@ struct FlceLayout {
 // with piece C_ORD[t] of W in the logits GEMM (and of dZ in both backward GEMMs); the pairs
 // enumerate i + j <= pieces - 1.
 static const int kOrdA2[3] = {0, 0, 1}, kOrdC2[3] = {0, 1, 0};
+// k-blocks (of 64) per accumulation segment of the fp32 dX GEMM: 128 truncating K=16 MMA
+// steps per segment (scripts/probe_tc_accum.py, profiles/r02_tc_accum.md)
+static const int kFp32SegKb = 32;
 static const int kOrdA3[6] = {0, 0, 1, 0, 1, 2}, kOrdC3[6] = {0, 1, 0, 2, 1, 0};
 
 static bool use_tc32_path(int dtype, int64_t hidden, int force_simt) {
@@ -254,7 +259,7 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
                               int pieces = 2, bool has_grad_x = true) {
   FlceLayout L{};
   L.tc32 = tc32;
-  L.pieces = pieces == 3 ? 3 : 2;
+  L.pieces = pieces == 2 ? 2 : 3;  // default 3: products exact to fp32's 2^-24
   L.nT = L.pieces == 3 ? 6 : 3;
   L.C = chunk_rows > 0 ? chunk_rows : b200_chunk_rows(bt, hidden, vocab, dtype);
   L.C = std::max<int64_t>(1, std::min<int64_t>(L.C, std::max<int64_t>(bt, 1)));
@@ -528,6 +533,9 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Bs[np] = dxB;
         Ps[np] = tc::Problem{};
         Ps[np].M = r; Ps[np].N = H; Ps[np].K = dxK; Ps[np].n_fast = 0; Ps[np].epi = xe;
+        // fp32 dX (K' = nT * V): restart the truncating tensor-core accumulation every
+        // kFp32SegKb k-blocks and add the segments in fp32 (Problem::seg_kb)
+        if (tc32) Ps[np].seg_kb = kFp32SegKb;
         ++np;
       }
       const int slices =

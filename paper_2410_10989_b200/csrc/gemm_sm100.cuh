@@ -45,6 +45,14 @@ struct Problem {
   int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
   int tma_out;          // 1: epilogue writes through smem staging + TMA store (map mc<p>)
+  // Segmented accumulation (fp32 TMA output only): the K loop restarts the TMEM accumulator
+  // every seg_kb k-blocks, alternating the two TMEM buffers like separate tiles, and the
+  // epilogue stores the first segment and TMA-reduce-adds (fp32, round-to-nearest, in L2) the
+  // later ones, each after the previous segment's bulk ops of the same rows have completed
+  // (same issuing lane, in order: deterministic).  The tensor core's own fp32 accumulation
+  // truncates at every MMA (scripts/probe_tc_accum.py: the error grows with the number of
+  // K=16 steps), so long-K fp32 problems keep each truncated run short.  0 = off.
+  int seg_kb;
   EpiArgs epi;
 };
 
@@ -672,6 +680,20 @@ __device__ __forceinline__ void epi_tma32(uint64_t omap, Stager& sg, int lane, i
   }
 }
 
+// Segmented accumulation helpers (Problem::seg_kb).
+__device__ __forceinline__ int seg_len(const Problem& P) { return P.seg_kb > 0 ? P.seg_kb : P.k_blocks; }
+__device__ __forceinline__ int seg_count(const Problem& P) {
+  return P.seg_kb > 0 ? (P.k_blocks + P.seg_kb - 1) / P.seg_kb : 1;
+}
+// One segment's fp32 partial: the first stores, later ones reduce-add after this lane's
+// earlier bulk ops (which cover exactly these rows) have been performed.
+__device__ __forceinline__ void epi_segment(uint64_t omap, Stager& sg, int lane, int row0, int64_t n0, int seg,
+                                            uint32_t taddr) {
+  if (seg > 0 && lane == 0) bulk_wait_all();
+  __syncwarp();
+  epi_tma32(omap, sg, lane, row0, n0, seg > 0, taddr);
+}
+
 // Dispatch one tile's epilogue for this warp.
 template <typename T>
 __device__ __forceinline__ void run_epilogue(const Problem& P, uint64_t omap, Stager& sg, int lane, int64_t grow,
@@ -803,7 +825,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
   } else if (warp == 1) {
     // ===================== MMA issuer (warp-converged, one elected issuer) =====================
     int stage = 0;
-    uint32_t phase = 0;
+    uint32_t phase = 0, use = 0;  // use: accumulations issued so far (TMEM buffer = use & 1)
     const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB), full0 = smem_u32(full), empty0 = smem_u32(empty);
     for (int it = 0;; ++it) {
       const int slot = it % SCHED;
@@ -817,17 +839,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       const int a_mn = (p ? args.prob[1].a_mode : args.prob[0].a_mode) != 0;
       const int b_mn = (p ? args.prob[1].b_mode : args.prob[0].b_mode) != 0;
       const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
+      const int seg_kb = seg_len(args.prob[p]);
       const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];
-      const int buf = it & 1;
-      mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
-      tc_fence_after();
-      const uint32_t d_tmem = tmem_base + buf * BN;
       // descriptors of stage 0 / k 0; stage and K advances only touch the start-address field
       const uint64_t a_desc0 = make_desc(sA0, a_mn ? 8192u : 16u, 1024u);
       const uint64_t b_desc0 = make_desc(sB0, b_mn ? 8192u : 16u, 1024u);
       const uint32_t a_k16 = a_mn ? (2048u >> 4) : (32u >> 4);   // per UMMA_K=16 step
       const uint32_t b_k16 = b_mn ? (2048u >> 4) : (32u >> 4);
+      int buf = 0, ks = 0;
+      uint32_t d_tmem = 0;
       for (int kb = 0; kb < kblocks; ++kb) {
+        if (ks == 0) {  // a new accumulation (tile, or segment of a segmented tile): next TMEM buffer
+          buf = (int)(use & 1);
+          mbar_wait(&tempty[buf], ((use >> 1) & 1) ^ 1);
+          tc_fence_after();
+          d_tmem = tmem_base + buf * BN;
+        }
         mbar_wait_addr(full0 + stage * 8, phase);
         tc_fence_after();
         if (elect_one()) {
@@ -835,19 +862,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
           const uint64_t bd = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
-            umma_f16(d_tmem, ad + k * a_k16, bd + k * b_k16, idesc, (kb | k) != 0 ? 1u : 0u);
+            umma_f16(d_tmem, ad + k * a_k16, bd + k * b_k16, idesc, (ks | k) != 0 ? 1u : 0u);
           umma_commit_addr(empty0 + stage * 8);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++ks == seg_kb || kb == kblocks - 1) {
+          if (elect_one()) umma_commit(&tfull[buf]);
+          __syncwarp();
+          ks = 0;
+          ++use;
+        }
       }
-      if (elect_one()) umma_commit(&tfull[buf]);
-      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int q = warp & 3;
     Stager sg{smem_u32(sStg) + (uint32_t)(q * 2 * STG_BYTES), 0};
+    uint32_t use = 0;
     for (int it = 0;; ++it) {
       const int slot = it % SCHED;
       mbar_wait(&sfull[slot], (it / SCHED) & 1);
@@ -858,17 +890,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       const TileCoord tcd = decode_tile(args, tile);
       const Problem& P = args.prob[tcd.p];
       const uint64_t omap = reinterpret_cast<uint64_t>(tcd.p ? &mc1 : &mc0);
-      const int buf = it & 1;
-      mbar_wait(&tfull[buf], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(q * 32) << 16);
       const int row0 = tcd.m_blk * BM + q * 32;
       const int64_t grow = (int64_t)row0 + lane;
       const int64_t n0 = (int64_t)tcd.n_blk * BN;
-      run_epilogue<T>(P, omap, sg, lane, grow, row0, n0, tcd.n_blk, taddr);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
+      const int nseg = seg_count(P);
+      for (int sgi = 0; sgi < nseg; ++sgi, ++use) {
+        const int buf = (int)(use & 1);
+        mbar_wait(&tfull[buf], (use >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + buf * BN + ((uint32_t)(q * 32) << 16);
+        if (nseg > 1) epi_segment(omap, sg, lane, row0, n0, sgi, taddr);
+        else run_epilogue<T>(P, omap, sg, lane, grow, row0, n0, tcd.n_blk, taddr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
     }
     if (lane == 0) bulk_wait_all();
   }

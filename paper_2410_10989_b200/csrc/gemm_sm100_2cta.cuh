@@ -238,7 +238,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
     if (leader) {
       // ===================== MMA issuer (leader CTA only) =====================
       int stage = 0;
-      uint32_t phase = 0;
+      uint32_t phase = 0, use = 0;  // use: accumulations issued so far (TMEM buffer = use & 1)
       const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
       for (int it = 0;; ++it) {
         const int slot = it % SCHED;
@@ -251,16 +251,21 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
         const int a_mn = (p ? args.prob[1].a_mode : args.prob[0].a_mode) != 0;
         const int b_mn = (p ? args.prob[1].b_mode : args.prob[0].b_mode) != 0;
         const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
+        const int seg_kb = tc::seg_len(args.prob[p]);
         const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];
-        const int buf = it & 1;
-        mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + buf * PBN;
         const uint64_t a_desc0 = tc::make_desc(sA0, a_mn ? 8192u : 16u, 1024u);
         const uint64_t b_desc0 = tc::make_desc(sB0, b_mn ? 8192u : 16u, 1024u);
         const uint32_t a_k16 = a_mn ? (2048u >> 4) : (32u >> 4);
         const uint32_t b_k16 = b_mn ? (2048u >> 4) : (32u >> 4);
+        int buf = 0, ks = 0;
+        uint32_t d_tmem = 0;
         for (int kb = 0; kb < kblocks; ++kb) {
+          if (ks == 0) {  // a new accumulation (tile, or segment of a segmented tile): next TMEM buffer
+            buf = (int)(use & 1);
+            mbar_wait(&tempty[buf], ((use >> 1) & 1) ^ 1);
+            tc_fence_after();
+            d_tmem = tmem_base + buf * PBN;
+          }
           mbar_wait_addr(full0 + stage * 8, phase);
           tc_fence_after();
           if (elect_one()) {
@@ -268,20 +273,25 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
             const uint64_t bd = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              umma2_f16(d_tmem, ad + k * a_k16, bd + k * b_k16, idesc, (kb | k) != 0 ? 1u : 0u);
+              umma2_f16(d_tmem, ad + k * a_k16, bd + k * b_k16, idesc, (ks | k) != 0 ? 1u : 0u);
             umma2_commit_mc(empty0 + stage * 8, (uint16_t)0x3);
           }
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++ks == seg_kb || kb == kblocks - 1) {
+            if (elect_one()) umma2_commit_mc(smem_u32(&tfull[buf]), (uint16_t)0x3);
+            __syncwarp();
+            ks = 0;
+            ++use;
+          }
         }
-        if (elect_one()) umma2_commit_mc(smem_u32(&tfull[buf]), (uint16_t)0x3);
-        __syncwarp();
       }
     }
   } else if (warp >= 4) {
     // ===================== epilogue (both CTAs) =====================
     const int q = warp & 3;
     tc::Stager sg{smem_u32(sStg) + (uint32_t)(q * 2 * tc::STG_BYTES), 0};
+    uint32_t use = 0;
     for (int it = 0;; ++it) {
       const int slot = it % SCHED;
       const uint32_t sp = (it / SCHED) & 1;
@@ -297,19 +307,23 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
       const PairTile pt = decode_pair(args, tile);
       const Problem& P = args.prob[pt.p];
       const uint64_t omap = reinterpret_cast<uint64_t>(pt.p ? &mc1 : &mc0);
-      const int buf = it & 1;
-      mbar_wait(&tfull[buf], (it >> 1) & 1);
-      tc_fence_after();
-      const uint32_t taddr = tmem_base + buf * PBN + ((uint32_t)(q * 32) << 16);
       const int row0 = pt.m_blk * PBM + (int)rank * HALF + q * 32;
       const int64_t grow = (int64_t)row0 + lane;
       const int64_t n0 = (int64_t)pt.n_blk * PBN;
-      tc::run_epilogue<T>(P, omap, sg, lane, grow, row0, n0, pt.n_blk, taddr);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (leader) mbar_arrive(&tempty[buf]);
-        else mbar_arrive_cluster(leader_tempty0 + 8 * buf);
+      const int nseg = tc::seg_count(P);
+      for (int sgi = 0; sgi < nseg; ++sgi, ++use) {
+        const int buf = (int)(use & 1);
+        mbar_wait(&tfull[buf], (use >> 1) & 1);
+        tc_fence_after();
+        const uint32_t taddr = tmem_base + buf * PBN + ((uint32_t)(q * 32) << 16);
+        if (nseg > 1) tc::epi_segment(omap, sg, lane, row0, n0, sgi, taddr);
+        else tc::run_epilogue<T>(P, omap, sg, lane, grow, row0, n0, pt.n_blk, taddr);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (leader) mbar_arrive(&tempty[buf]);
+          else mbar_arrive_cluster(leader_tempty0 + 8 * buf);
+        }
       }
     }
     if (lane == 0) tc::bulk_wait_all();

@@ -88,8 +88,8 @@ def fused_linear_cross_entropy_forward(
     splits the last chunk's grad_w GEMM into that many vocab-row slices and records event s
     when slice s of grad_w is final (overlap of the token-sharded dW all-reduce).
     fp32 inputs run on the bf16 tensor cores on split operands (`fp32_pieces` bf16 pieces
-    per value: 0/2 = 3 piece products, 3 = 6; include/liger_b200.h); `force_simt=True` runs
-    the SIMT FFMA GEMMs instead (the test reference).
+    per value: 0/3 = 6 piece products (fp32-exact products), 2 = 3; include/liger_b200.h);
+    `force_simt=True` runs the SIMT FFMA GEMMs instead (the test reference).
     `check_targets=False` skips the host read of the device-side out-of-range count (the one
     host sync of the call); the caller then owns the check (token_sharded_flce does it on the
     all-reduced count after enqueueing its collectives).

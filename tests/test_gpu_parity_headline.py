@@ -149,7 +149,7 @@ def test_cfg4_row_slice_full_vocab_vs_oracle(wscale, lo, rows, chunk):
 
 
 # ------------------------------------------- fp32 on the bf16 tensor cores (split operands)
-@pytest.mark.parametrize("pieces", [0, 3])
+@pytest.mark.parametrize("pieces", [0, 2])
 @pytest.mark.parametrize("opts", [dict(), dict(label_smoothing=0.1, softcap=30.0, lse_square_scale=1e-4),
                                   dict(reduction="sum", chunk_rows=300), dict(bias=True)])
 def test_fp32_split_tensor_core_path_vs_oracle_and_simt(pieces, opts):
@@ -184,7 +184,11 @@ def test_fp32_split_tensor_core_path_vs_oracle_and_simt(pieces, opts):
 
 
 def test_fp32_cfg2_row_slice_full_vocab_vs_oracle():
-    """fp32 at the Llama-3-8B head's full H and V (split-operand tensor-core path), 256 rows."""
+    """fp32 at the Llama-3-8B head's full H and V (split-operand tensor-core path), 256 rows.
+    The dX GEMM's K' = 6 x 128256: without segmented accumulation the tensor core's truncating
+    fp32 accumulator drifts to ~5e-4 of max|dX| (scripts/probe_tc_accum.py); with it the error
+    is at the SIMT FFMA path's level.  Run twice: the segment reduce-adds are ordered, so the
+    result is bitwise repeatable."""
     g = torch.Generator(device="cuda").manual_seed(5)
     x = torch.rand(256, 4096, device="cuda", generator=g) * 2 - 1
     w = (torch.rand(128256, 4096, device="cuda", generator=g) * 2 - 1) / 64.0
@@ -193,5 +197,8 @@ def test_fp32_cfg2_row_slice_full_vocab_vs_oracle():
     ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x.double().cpu().numpy(), w.double().cpu().numpy(), t.cpu().numpy())
     loss, gx, gw = run(x, w, t)
     assert loss.item() == pytest.approx(ref_loss, rel=1e-4)
-    assert rel_close(gx.double().cpu().numpy(), rgx, 1e-4)[0]
+    ok, err = rel_close(gx.double().cpu().numpy(), rgx, 1e-4)
+    assert ok and err < 1e-4, err
     assert rel_close(gw.double().cpu().numpy(), rgw, 1e-4)[0]
+    loss2, gx2, gw2 = run(x, w, t)
+    assert torch.equal(gx, gx2) and torch.equal(gw, gw2) and loss.item() == loss2.item()
