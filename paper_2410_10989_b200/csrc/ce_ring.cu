@@ -179,8 +179,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       uint4 raw[KPL];
 #pragma unroll
       for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + 512u * k) : make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      if (lane == 0) ring::arrive(empty_a + 8u * (uint32_t)s);
+      ring::release_after_loads(empty_a + 8u * (uint32_t)s, raw, lane);
       float2 z[KPL][NP];
       float lmax = -INFINITY;
       if (nvec == (int)(PIECE / 16)) {  // whole piece (all but a ragged row tail): no masking
@@ -313,8 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
       uint4 raw[KPL];
 #pragma unroll
       for (int k = 0; k < KPL; ++k) raw[k] = v0 + 32 * k < nvec ? ring::lds128(st + 512u * k) : make_uint4(0, 0, 0, 0);
-      __syncwarp();
-      if (lane == 0) ring::arrive(empty_a + 8u * (uint32_t)s);
+      ring::release_after_loads(empty_a + 8u * (uint32_t)s, raw, lane);
       const int64_t col0 = (int64_t)j * (PIECE / sizeof(T));
       T* xp = xr + col0 + (int64_t)v0 * NV;  // this lane's first vector of the piece
       const float* wp = W ? wcol + col0 + (int64_t)v0 * NV : nullptr;

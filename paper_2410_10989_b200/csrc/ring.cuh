@@ -53,6 +53,29 @@ __device__ __forceinline__ void wait(uint32_t b, uint32_t parity) {
         : "memory");
   } while (!done);
 }
+// Release a ring stage right after loading from it (before the loaded registers are used).
+// A plain `mbarrier.arrive` after the ld.shared is NOT enough in practice: the SYNCS arrive
+// can take effect while the warp's LDS are still queued behind its global stores, the
+// producer then refills the stage, and the late LDS read the NEXT piece (measured on B200: a
+// few 256-column stretches per ~20k FLCE finalize rows differed run to run;
+// scripts/determinism_stage.py, profiles/r02/ring_release_race.md).  The arrive here
+// consumes `dep`, an OR of one register of every loaded vector (an LDS.128 completes for the
+// whole warp at once, so one register per load instruction carries the scoreboard wait), so
+// the warp cannot issue it before all of its loads have returned.  `min(dep, 0) + bar` keeps
+// the address equal to `bar` (checked in the SASS: VIMNMX.U32 feeding SYNCS.ARRIVE).
+// Called by every lane; lane 0 arrives.
+template <int K>
+__device__ __forceinline__ void release_after_loads(uint32_t bar, const uint4 (&raw)[K], int lane) {
+  uint32_t dep = 0;
+#pragma unroll
+  for (int k = 0; k < K; ++k) dep |= raw[k].x;
+  __syncwarp();
+  if (lane == 0)
+    asm volatile(
+        "{\n\t.reg .b32 t;\n\tmin.u32 t, %1, 0;\n\tadd.u32 t, t, %0;\n\t"
+        "mbarrier.arrive.shared::cta.b64 _, [t];\n\t}" ::"r"(bar), "r"(dep)
+        : "memory");
+}
 // global -> shared 1D bulk copy, completion counted on `bar` (bytes multiple of 16).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

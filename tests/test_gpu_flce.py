@@ -249,6 +249,22 @@ def big_problem(bt, h, v, seed, wscale=1.0, ignore_frac=0.1):
     return x, w, t
 
 
+def test_finalize_ring_bitwise_repeatable():
+    """The FLCE finalize (CE ring, one HBM pass) releases each ring stage only after its shared-
+    memory loads have returned (ring::release_after_loads).  With a plain arrive, ~1 in 5 calls
+    of this shape differed in one 256-column stretch of one row (the producer's refill overwrote
+    the stage under late loads; profiles/r02/ring_release_race.md).  Gemma-2 head width, one
+    2048-row chunk, softcap + smoothing, 12 calls: all bitwise equal."""
+    x, w, t = big_problem(2048, 3584, 256000, seed=1, wscale=30.0)
+    kw = dict(softcap=30.0, label_smoothing=0.1, chunk_rows=2048)
+    loss0, _, _, _, gx0, _, _ = flce_fwd(x, w, t, compute_grad_input=True, compute_grad_weight=False,
+                                         reduction="none", **kw)
+    for _ in range(11):
+        loss, _, _, _, gx, _, _ = flce_fwd(x, w, t, compute_grad_input=True, compute_grad_weight=False,
+                                           reduction="none", **kw)
+        assert torch.equal(loss, loss0) and torch.equal(gx, gx0)
+
+
 def test_cfg2_llama3_head_vs_torch_fp32_and_properties():
     x, w, t = big_problem(8192, 4096, 128256, seed=0)
     loss, _, gx, gw, _ = flce(x, w, t)
