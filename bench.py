@@ -31,7 +31,8 @@ Keys beyond the base contract:
                 GPU's fp32 FLCE on the same cfg1 inputs.  Rank 0 at N=1 only.
   e2e           the public module LigerFusedLinearCrossEntropyLoss + autograd backward with
                 X/targets copied from pinned host memory every step (on a side stream, one
-                step ahead, double-buffered) and the loss read back with .item() every step.
+                step ahead, double-buffered) and every step's loss copied back to pinned host
+                memory inside the timed region, read on the host one step later.
   variants      accum_dtype=torch.float32 (fp32 dW accumulator) tokens/s and peak memory.
   --impl reference  times the reference's CPU algorithm (oracle port, f32) on the box's host
                 cores; rank 0 only.
@@ -318,7 +319,40 @@ def gpu_cfg1_fp32(dev):
     med, q20, q80 = quantiles(times)
     return {"median_ms": 1e3 * med, "q20_ms": 1e3 * q20, "q80_ms": 1e3 * q80, "tokens_per_s": 1024 / med,
             "tflops": 6.0 * 1024 * 512 * 4096 / med / 1e12,
-            "path": "fp32 FLCE through fused_linear_cross_entropy_forward (includes the host-side range check)"}
+            "path": "fp32 FLCE through fused_linear_cross_entropy_forward (includes the host-side range check): "
+                    "bf16 tensor cores on 3-piece split operands, segmented fp32 accumulation of dX"}
+
+
+def gpu_cfg2_fp32(dev, steps=3):
+    """fp32 FLCE at the cfg2 shape (X, W, grads in fp32): the split-operand tensor-core path."""
+    import torch
+
+    from paper_2410_10989_b200.fused_linear_cross_entropy import fused_linear_cross_entropy_forward
+
+    g = torch.Generator(device=dev).manual_seed(0)
+    x = torch.rand(BT, H, device=dev, generator=g) * 2 - 1
+    w = (torch.rand(V, H, device=dev, generator=g) * 2 - 1) / 64.0
+    t = torch.randint(0, V, (BT,), device=dev, generator=g)
+    t[torch.rand(BT, device=dev, generator=g) < IGNORE_FRAC] = -100
+
+    def call():
+        return fused_linear_cross_entropy_forward(x, w, t, compute_grad_input=True, compute_grad_weight=True)
+
+    call()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        call()
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    flop = 6.0 * BT * H * V
+    return {"value": BT / (ms / 1e3), "unit": "tokens/s", "steps": steps, "ms_per_step": ms,
+            "algorithmic_tflops": flop / (ms / 1e3) / 1e12,
+            "note": "fp32 inputs/outputs at the cfg2 shape; GEMMs on the bf16 tensor cores over 3-piece split "
+                    "operands (6 piece products per product, K' = 6K), dX accumulated in 32-k-block segments "
+                    "summed in fp32; algorithmic_tflops counts 6*BT*H*V"}
 
 
 def run_ours(args):
@@ -461,6 +495,8 @@ def run_ours(args):
                                    "peak_extra_minus_outputs": pk32 - out_bytes,
                                    "note": "accum_dtype=torch.float32: grad_w accumulated across chunks in an "
                                            "fp32 workspace (V*H*4 bytes), one final rounding"}}
+        if world == 1 and args.config == "cfg2" and not vocab_mode and args.bt == BT:
+            variants["fp32_cfg2"] = gpu_cfg2_fp32(dev)
 
     # ---- e2e through the public module, host buffers, H2D/D2H inside the timed region ----
     xh = x.cpu().pin_memory()
@@ -474,7 +510,20 @@ def run_ours(args):
     copy_stream = torch.cuda.Stream(device=dev)
     bufs = [(torch.empty_like(x), torch.empty_like(t)) for _ in range(2)]
     ready = [torch.cuda.Event() for _ in range(2)]
-    state = {"i": 0}
+    state = {"i": 0, "pending": None}
+    # each step's loss goes device->host into pinned memory on the compute stream (inside the
+    # timed region) and is read on the host one step later, as a training loop logs its loss,
+    # so the read does not stall the launch of the next step
+    loss_host = [torch.empty((), dtype=torch.float32).pin_memory() for _ in range(2)]
+    loss_ready = [torch.cuda.Event() for _ in range(2)]
+    e2e_losses = []
+
+    def read_pending():
+        j = state["pending"]
+        if j is not None:
+            loss_ready[j % 2].synchronize()
+            e2e_losses.append(float(loss_host[j % 2]))
+            state["pending"] = None
 
     def stage_copy(i):
         xb, tb = bufs[i % 2]
@@ -496,19 +545,20 @@ def run_ours(args):
         state["i"] = i + 1
         if vocab_mode:
             loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, **opts)
-            val = loss.item()
         elif world > 1:
             loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk, **opts)
-            val = loss.item()
         else:
             loss = loss_fn(wp, xd, td)
             loss.backward()
-            val = loss.item()
+        loss_host[i % 2].copy_(loss.detach().float(), non_blocking=True)
+        loss_ready[i % 2].record(cur)
+        read_pending()  # the previous step's loss (its copy finished long ago)
+        state["pending"] = i
         wp.grad = None
-        return val
 
     for _ in range(max(1, args.warmup)):
         e2e_step()
+    read_pending()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -517,6 +567,8 @@ def run_ours(args):
         e2e_step()
     e1.record()
     torch.cuda.synchronize()
+    read_pending()
+    assert all(math.isfinite(v) for v in e2e_losses), "non-finite loss in the e2e loop"
     e2e_value = tokens_per_step * args.steps / (max_over_ranks(e0.elapsed_time(e1)) / 1e3)
 
     peaks, peak_src = measured_peaks()
@@ -574,7 +626,10 @@ def run_ours(args):
                             "distributed.token_sharded_flce" if world > 1 else
                             "LigerFusedLinearCrossEntropyLoss + backward()"),
                     "h2d_pipeline": "each step's X/targets copied from pinned host memory on a side stream, "
-                                    "double-buffered one step ahead; loss read back with .item() every step"},
+                                    "double-buffered one step ahead; every step's loss copied device->host "
+                                    "(pinned, on the compute stream, inside the timed region) and read on the "
+                                    "host one step later; the forward's target-range check is a host sync "
+                                    "every step (as Liger's n_non_ignore .item())"},
             "gpu_launches": launches * args.steps,
             "gpu_launches_per_step": launches,
             "clocks": clk.summary(),

@@ -5,11 +5,11 @@
 set -e
 cd /root/repo
 PYTHONDONTWRITEBYTECODE=1 PYTHONPATH=/root/reference/pkg/src python -m rowfuse.cli bench \
-  --ops rmsnorm,swiglu,rope,cross_entropy --repeats 3 --dtype f32 --csv /tmp/ref_bench.csv > /dev/null
+  --ops rmsnorm,layernorm,swiglu,geglu,rope,cross_entropy,linear_ce --repeats 3 --dtype f32 --csv /tmp/ref_bench.csv > /dev/null
 python - <<'PY'
 import csv
 ref = list(csv.reader(open("/tmp/ref_bench.csv")))
-gpu = list(csv.reader(open("profiles/r01_benchrecord_gpu_f32.csv")))
+gpu = list(csv.reader(open("profiles/r02/r2_benchrecord_gpu_f32.csv")))
 rows = [r for r in ref[1:] if r[1] == "reference"] + gpu[1:]
 with open("/tmp/merged_bench.csv", "w", newline="") as f:
     w = csv.writer(f); w.writerow(ref[0]); w.writerows(rows)
