@@ -55,9 +55,11 @@ def plan_chunks(total_rows: int, vocab_size: int, hidden_size: int) -> ChunkPlan
 
 def b200_plan(total_rows: int, vocab_size: int, hidden_size: int, elem_bytes: int = 2) -> ChunkPlan:
     """Host restatement of the library's default (flce.cu b200_chunk_rows): at least
-    min(next_pow2(BT), 2048) rows, at most a 1 GiB chunk buffer."""
+    min(next_pow2(BT), 2048) rows -- 4096 when BT > 16384 (more than 8 chunks of 2048) --
+    at most a 1 GiB chunk buffer."""
     ref = plan_chunks(total_rows, vocab_size, hidden_size).chunk_rows
-    c = max(ref, min(next_pow2(total_rows), 2048))
+    c_min = 4096 if total_rows > 2048 * 8 else 2048
+    c = max(ref, min(next_pow2(total_rows), c_min))
     ldz = -(-vocab_size // 64) * 64
     while c > 128 and c * ldz * elem_bytes > (1 << 30):
         c >>= 1

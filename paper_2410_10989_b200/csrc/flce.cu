@@ -192,13 +192,17 @@ static int64_t ld_logits(int64_t vocab) { return (vocab + 63) / 64 * 64; }
 // Reference rule (rowfuse/flce.py:69-78):
 //   C_ref = 2^ceil(log2(ceil(BT / ceil(V/H)))).
 // B200 rule: at least 2048 rows per chunk when the batch has them, because every
-// chunk costs one fp32 read-modify-write of dW (V x H x 8 bytes); at C = 2048 the
-// dW GEMM's MMA time per tile covers its RMW traffic (SURVEY §7 "hard parts").
-// The chunk buffer is capped at 1 GiB.
+// chunk re-streams W (V x H) through two GEMMs and costs one read-modify-write of dW;
+// at C = 2048 the dW GEMM's MMA time per tile covers its RMW traffic (SURVEY §7 "hard
+// parts").  Batches that would need more than LK_ACCUM_AUTO_MAX_CHUNKS 2048-row chunks
+// (BT > 16384) take 4096-row chunks: half the W re-streams and dW RMWs, +3.2% at
+// BT = 65536 (cfg5 at N = 1) and +0.8% at BT = 8192, for which the smaller buffer is kept
+// (profiles/r02/chunk_sweep.log).  The chunk buffer is capped at 1 GiB.
 static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dtype) {
   int64_t ratio = (vocab + hidden - 1) / hidden;
   int64_t c_ref = next_pow2((bt + ratio - 1) / ratio);
-  int64_t c = std::max<int64_t>(c_ref, std::min<int64_t>(next_pow2(bt), 2048));
+  const int64_t c_min = bt > 2048 * LK_ACCUM_AUTO_MAX_CHUNKS ? 4096 : 2048;
+  int64_t c = std::max<int64_t>(c_ref, std::min<int64_t>(next_pow2(bt), c_min));
   const int64_t cap_bytes = (int64_t)1 << 30;
   while (c > 128 && c * ld_logits(vocab) * elt_size(dtype) > cap_bytes) c >>= 1;
   return std::max<int64_t>(1, c);

@@ -11,6 +11,7 @@ import pytest
 import torch
 
 import paper_2410_10989_b200 as lk
+from paper_2410_10989_b200.chunking import b200_plan
 from paper_2410_10989_b200 import _capi, errors
 
 HEADER = Path(__file__).resolve().parents[1] / "include" / "liger_b200.h"
@@ -64,6 +65,10 @@ def test_plan_and_workspace_queries():
     # more than 8 chunks: auto falls back to the fp32 accumulator
     assert lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 512, 1) > dw_acc
     assert lk.flce_plan(8192, 4096, 128256) == (2048, 4)
+    for bt in (16384, 65536, 32768 + 5):  # the host restatement agrees with the library
+        for h, v in ((4096, 128256), (3584, 256000), (512, 4096)):
+            p = b200_plan(bt, v, h)
+            assert lk.flce_plan(bt, h, v) == (p.chunk_rows, p.num_chunks), (bt, h, v)
 
 
 def test_status_codes_map_to_reference_exceptions():

@@ -220,6 +220,9 @@ def test_chunk_plan_validation():
     p = b200_plan(8192, 128256, 4096)
     assert p.chunk_rows == 2048 and p.num_chunks == 4
     assert b200_plan(1024, 4096, 512).num_chunks == 1
+    assert b200_plan(16384, 128256, 4096).chunk_rows == 2048  # 8 chunks: weight-dtype dW accumulation
+    assert b200_plan(65536, 128256, 4096).chunk_rows == 4096  # cfg5 at N = 1: 16 chunks
+    assert b200_plan(65536, 256000, 3584).chunk_rows == 2048  # 1 GiB buffer cap at V = 256000
 
 
 def test_flce_properties_f64():
