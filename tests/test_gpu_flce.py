@@ -249,6 +249,28 @@ def big_problem(bt, h, v, seed, wscale=1.0, ignore_frac=0.1):
     return x, w, t
 
 
+def test_cfg5_one_gpu_default_plan():
+    """BASELINE configs[4] on one GPU: 65536 tokens of the Llama-3-8B head.  The default plan
+    takes 4096-row chunks above 16384 tokens (16 chunks, so grad_w accumulates in the fp32
+    workspace); checked against the chunked fp32 restatement (pinned to the oracle), the
+    2048-row plan, and a second run (bitwise)."""
+    x, w, t = big_problem(65536, 4096, 128256, seed=2)
+    assert lk.flce_plan(65536, 4096, 128256) == (4096, 16)
+    loss, _, gx, gw, _ = flce(x, w, t)
+    rloss, _, rgx, rgw, _ = flce_ref(x, w, t, chunk=4096)
+    assert abs(loss.item() - rloss.item()) <= 2e-2 * abs(rloss.item())
+    assert close(gx, rgx, 2e-2), rel_err(gx, rgx)
+    assert close(gw, rgw, 2e-2), rel_err(gw, rgw)
+    assert torch.all(gx[t == -100] == 0)
+    del rgx, rgw
+    loss2, _, gx2, gw2, _ = flce(x, w, t)
+    assert loss.item() == loss2.item() and torch.equal(gx, gx2) and torch.equal(gw, gw2)
+    del gx2, gw2
+    loss3, _, gx3, gw3, _ = flce(x, w, t, chunk_rows=2048)
+    assert abs(loss3.item() - loss.item()) <= 1e-4 * abs(loss.item())
+    assert close(gx3, gx, 1e-2) and close(gw3, gw, 2e-2)
+
+
 def test_finalize_ring_bitwise_repeatable():
     """The FLCE finalize (CE ring, one HBM pass) releases each ring stage only after its shared-
     memory loads have returned (ring::release_after_loads).  With a plain arrive, ~1 in 5 calls
