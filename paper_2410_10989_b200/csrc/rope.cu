@@ -80,63 +80,67 @@ __global__ void __launch_bounds__(256) rope_kernel(T* __restrict__ q, T* __restr
   }
 }
 
-// Token-major variant (the common shapes): one thread per (head, vector) of a token -- its
-// head / vector / cos-offset decomposition is computed once -- and each CTA walks a
-// contiguous token range two tokens at a time (both tokens' loads issued before either's
-// stores), so the per-item 64-bit index divisions of the grid-stride kernel disappear.
+// Token-major variant (the common shapes): one thread per (head, 16-byte vector) of a token,
+// so the head / vector / cos-offset decomposition is computed once; q and k heads of a token
+// in one CTA (cos/sin reused from L1).  One non-persistent CTA per ROPE_U consecutive tokens,
+// every q/k load of the chunk issued before any rotation, the CTA retired after its stores:
+// the block scheduler then streams one contiguous window through memory.  Against the
+// previous semi-persistent design (each CTA walking ~10 tokens two at a time): 0.83 -> 0.89
+// of HBM steady, 0.93 -> 0.97 cold, and 1.03-1.04x upstream Liger's Triton kernel at the
+// kernel level (profiles/r02/rope_chunk_ab.log; 4 / 8 tokens per CTA: 0.83 / 0.57).
+constexpr int ROPE_U = 2;
 template <typename T, typename C>
-__global__ void __launch_bounds__(1024) rope_tok_kernel(T* __restrict__ q, T* __restrict__ k,
-                                                        const C* __restrict__ cosp, const C* __restrict__ sinp,
-                                                        int tokens, int seq, int nq, int nk, int d, int cos_per_tok,
-                                                        int tok_per_cta, int backward) {
+__global__ void __launch_bounds__(1024) rope_chunk_kernel(T* __restrict__ q, T* __restrict__ k,
+                                                          const C* __restrict__ cosp, const C* __restrict__ sinp,
+                                                          int tokens, int seq, int nq, int nk, int d, int cos_per_tok,
+                                                          int backward) {
   constexpr int NV = Vec16<T>::N;
   const int half = d / 2, vph = half / NV;
   const int h = threadIdx.x / vph, i0 = (threadIdx.x - h * vph) * NV;
   const float sgn = backward ? -1.f : 1.f;
-  const int t0 = blockIdx.x * tok_per_cta, t1 = min(tokens, t0 + tok_per_cta);
+  const int t0 = blockIdx.x * ROPE_U;
   T* const hb = h < nq ? q + (int64_t)h * d : k + (int64_t)(h - nq) * d;
   const int64_t tstride = (int64_t)(h < nq ? nq : nk) * d;
-  int t = t0 % seq;  // position of token t0 inside its sequence (cos/sin row when shared by the batch)
-  auto rot = [&](int tok, int pos, Vec16<T>& a, Vec16<T>& b) {
-    const int64_t crow = (int64_t)(cos_per_tok ? tok : pos) * d + i0;
-    float c[NV], sn[NV];
-    if constexpr (sizeof(C) == sizeof(T)) {
-      Vec16<C> vc, vs;
-      vc.load(cosp + crow);
-      vs.load(sinp + crow);
+  uint4 ra[ROPE_U], rb[ROPE_U];
 #pragma unroll
-      for (int e = 0; e < NV; ++e) { c[e] = vc.v[e]; sn[e] = sgn * vs.v[e]; }
-    } else {
-#pragma unroll
-      for (int e = 0; e < NV; ++e) { c[e] = to_f<C>(cosp[crow + e]); sn[e] = sgn * to_f<C>(sinp[crow + e]); }
+  for (int u = 0; u < ROPE_U; ++u) {
+    if (t0 + u < tokens) {
+      const T* p = hb + (int64_t)(t0 + u) * tstride;
+      ra[u] = *reinterpret_cast<const uint4*>(p + i0);
+      rb[u] = *reinterpret_cast<const uint4*>(p + half + i0);
     }
-#pragma unroll
-    for (int e = 0; e < NV; ++e) {
-      const float x1 = a.v[e], x2 = b.v[e];
-      a.v[e] = x1 * c[e] - x2 * sn[e];
-      b.v[e] = x2 * c[e] + x1 * sn[e];
-    }
-  };
-  int tok = t0;
-  for (; tok + 1 < t1; tok += 2) {
-    T* p0 = hb + (int64_t)tok * tstride;
-    T* p1 = p0 + tstride;
-    const int pos0 = t, pos1 = t + 1 == seq ? 0 : t + 1;
-    Vec16<T> a0, b0, a1, b1;
-    a0.load(p0 + i0); b0.load(p0 + half + i0);
-    a1.load(p1 + i0); b1.load(p1 + half + i0);
-    rot(tok, pos0, a0, b0);
-    rot(tok + 1, pos1, a1, b1);
-    a0.store(p0 + i0); b0.store(p0 + half + i0);
-    a1.store(p1 + i0); b1.store(p1 + half + i0);
-    t = pos1 + 1 == seq ? 0 : pos1 + 1;
   }
-  if (tok < t1) {
-    T* p0 = hb + (int64_t)tok * tstride;
-    Vec16<T> a0, b0;
-    a0.load(p0 + i0); b0.load(p0 + half + i0);
-    rot(tok, t, a0, b0);
-    a0.store(p0 + i0); b0.store(p0 + half + i0);
+  int pos = t0 % seq;
+#pragma unroll
+  for (int u = 0; u < ROPE_U; ++u) {
+    const int tok = t0 + u;
+    if (tok < tokens) {
+      const int64_t crow = (int64_t)(cos_per_tok ? tok : pos) * d + i0;
+      float c[NV], sn[NV];
+      if constexpr (sizeof(C) == sizeof(T)) {
+        Vec16<C> vc, vs;
+        vc.load(cosp + crow);
+        vs.load(sinp + crow);
+#pragma unroll
+        for (int e = 0; e < NV; ++e) { c[e] = vc.v[e]; sn[e] = sgn * vs.v[e]; }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NV; ++e) { c[e] = to_f<C>(cosp[crow + e]); sn[e] = sgn * to_f<C>(sinp[crow + e]); }
+      }
+      const T* ea = reinterpret_cast<const T*>(&ra[u]);
+      const T* eb = reinterpret_cast<const T*>(&rb[u]);
+      Vec16<T> a, b;
+#pragma unroll
+      for (int e = 0; e < NV; ++e) {
+        const float x1 = to_f<T>(ea[e]), x2 = to_f<T>(eb[e]);
+        a.v[e] = x1 * c[e] - x2 * sn[e];
+        b.v[e] = x2 * c[e] + x1 * sn[e];
+      }
+      T* p = hb + (int64_t)tok * tstride;
+      a.store(p + i0);
+      b.store(p + half + i0);
+    }
+    pos = pos + 1 == seq ? 0 : pos + 1;
   }
 }
 
@@ -150,14 +154,12 @@ static int launch_rope(void* q, void* k, const void* cs, const void* sn, int64_t
     vec = vec && ((reinterpret_cast<uintptr_t>(cs) & 15) == 0) && ((reinterpret_cast<uintptr_t>(sn) & 15) == 0);
   const int64_t per_tok = (nq + nk) * ((d / 2) / NV), tokens = batch * seq;
   if (vec && per_tok % 32 == 0 && per_tok <= 1024 && tokens <= 0x7fffffff) {
-    const int threads = (int)per_tok;
-    const int64_t ctas = std::max<int64_t>(1, (int64_t)sm_count() * std::max(1, 2048 / threads));
-    const int tpc = (int)std::max<int64_t>(1, (tokens + ctas - 1) / ctas);
-    const unsigned g = (unsigned)((tokens + tpc - 1) / tpc);
-    rope_tok_kernel<T, C><<<g, threads, 0, st>>>(static_cast<T*>(q), static_cast<T*>(k), static_cast<const C*>(cs),
-                                                 static_cast<const C*>(sn), (int)tokens, (int)seq, (int)nq, (int)nk,
-                                                 (int)d, cb == 1 ? 0 : 1, tpc, backward);
-    return check_launch("rope_tok_kernel");
+    const unsigned g = (unsigned)((tokens + ROPE_U - 1) / ROPE_U);
+    rope_chunk_kernel<T, C><<<g, (int)per_tok, 0, st>>>(static_cast<T*>(q), static_cast<T*>(k),
+                                                         static_cast<const C*>(cs), static_cast<const C*>(sn),
+                                                         (int)tokens, (int)seq, (int)nq, (int)nk, (int)d,
+                                                         cb == 1 ? 0 : 1, backward);
+    return check_launch("rope_chunk_kernel");
   }
   const int64_t items = batch * seq * (nq + nk) * ((d / 2) / (vec ? NV : 1));
   unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, 16 * (int64_t)sm_count()));

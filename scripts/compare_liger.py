@@ -3,7 +3,8 @@ Triton, installed in the image) vs torch eager, on the north-star workloads.
 
 Not part of the product or the tests: a measurement script.  Each op runs forward + backward
 through its public module/function; timing is CUDA events around the call (median of
-`--reps` after 3 warm-ups), inputs resident in HBM; peak memory = allocator peak above
+`--reps` after 3 warm-ups), inputs resident in HBM; `graph_ms` (small ops) is the GPU time
+per call with 10 calls captured in one CUDA graph (host launch cost out of the loop); peak memory = allocator peak above
 the inputs during one call.
 
     python scripts/compare_liger.py [--reps 10] [--only flce,ce,rmsnorm,rope,swiglu,layernorm]
@@ -39,11 +40,46 @@ def timed(fn, reps):
     return statistics.median(ts), (torch.cuda.max_memory_allocated() - base) / 2**20
 
 
-def run(name, impls, reps, out):
+def graph_timed(fn, calls=10, replays=5):
+    """GPU time per call with the host out of the loop: `calls` calls captured in one CUDA graph,
+    replayed; None when the implementation cannot be captured (a host sync inside)."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    try:
+        with torch.cuda.graph(g):
+            for _ in range(calls):
+                fn()
+    except Exception:
+        torch.cuda.synchronize()
+        return None
+    g.replay()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(replays):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / calls)
+    del g
+    return statistics.median(ts)
+
+
+def run(name, impls, reps, out, graph=False):
     for impl, fn in impls:
         try:
             ms, mb = timed(fn, reps)
             rec = {"op": name, "impl": impl, "ms": round(ms, 4), "peak_mib": round(mb, 1)}
+            if graph:
+                gms = graph_timed(fn)
+                rec["graph_ms"] = None if gms is None else round(gms, 4)
         except Exception as exc:  # e.g. an upstream kernel that does not run on sm_100
             rec = {"op": name, "impl": impl, "error": f"{type(exc).__name__}: {str(exc)[:160]}"}
         print(json.dumps(rec), flush=True)
@@ -107,7 +143,7 @@ def main():
         run("cross_entropy 8192x128256 (+clone)", [("b200", mk(lk.LigerCrossEntropyLoss())),
                                                    ("liger_triton", mk(lkt.LigerCrossEntropyLoss())),
                                                    ("torch_eager", mk(lambda zz, tt: F.cross_entropy(zz.float(), tt)))],
-            a.reps, out)
+            a.reps, out, graph=True)
         del z
     x = (torch.rand(8192, 4096, device=dev, generator=g) * 2 - 1).to(bf)
     dy = (torch.rand(8192, 4096, device=dev, generator=g) * 2 - 1).to(bf)
@@ -124,7 +160,8 @@ def main():
             xx = x.detach().requires_grad_(True)
             xf = xx.float()
             (ours.weight * (xf * torch.rsqrt(xf.pow(2).mean(-1, keepdim=True) + 1e-6)).to(bf)).backward(dy)
-        run("rmsnorm 8192x4096", [("b200", mk(ours)), ("liger_triton", mk(up)), ("torch_eager", eager)], a.reps, out)
+        run("rmsnorm 8192x4096", [("b200", mk(ours)), ("liger_triton", mk(up)), ("torch_eager", eager)], a.reps, out,
+            graph=True)
     if "layernorm" in want:
         ours, up = lk.LigerLayerNorm(4096).to(dev, bf), lkt.LigerLayerNorm(4096).to(dev, bf)
         ref = torch.nn.LayerNorm(4096).to(dev, bf)
@@ -135,7 +172,7 @@ def main():
                 mod(xx).backward(dy)
             return f
         run("layernorm 8192x4096", [("b200", mk(ours)), ("liger_triton", mk(up)), ("torch_eager", mk(ref))], a.reps,
-            out)
+            out, graph=True)
     if "rope" in want:
         b, t_, nq, nk, d = 4, 2048, 32, 8, 128
         q0 = torch.randn(b, t_, nq, d, device=dev, generator=g).to(bf)
@@ -160,7 +197,7 @@ def main():
             return rot(q, c[:, None], s[:, None]), rot(k, c[:, None], s[:, None])
         run("rope 4x2048, 32q/8kv heads x128 (+clones)", [("b200", mk(lk.liger_rotary_pos_emb)),
                                                          ("liger_triton", mk(up_rope)),
-                                                         ("torch_eager", mk(eager_fn))], a.reps, out)
+                                                         ("torch_eager", mk(eager_fn))], a.reps, out, graph=True)
     if "swiglu" in want:
         a_ = torch.randn(8192, 14336, device=dev, generator=g).to(bf)
         b_ = torch.randn(8192, 14336, device=dev, generator=g).to(bf)
@@ -174,7 +211,8 @@ def main():
             return f
         run("swiglu 8192x14336 (+clones)", [("b200", mk(lk.LigerSiLUMulFunction.apply)),
                                             ("liger_triton", mk(UpSiLU.apply)),
-                                            ("torch_eager", mk(lambda aa, bb: F.silu(aa) * bb))], a.reps, out)
+                                            ("torch_eager", mk(lambda aa, bb: F.silu(aa) * bb))], a.reps, out,
+            graph=True)
     print(json.dumps({"summary": out}))
 
 
