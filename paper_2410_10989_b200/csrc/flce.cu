@@ -641,6 +641,7 @@ extern "C" int lk_flce_vp_logits(const void* x, const void* weight_shard, const 
     tc::TmaOperand A{x, hidden, rows, hidden, 0}, B{weight_shard, hidden, vocab_local, hidden, 0};
     tc::Problem P{};
     P.M = rows; P.N = vocab_local; P.K = hidden; P.n_fast = 0; P.epi = le;
+    ProfScope ps(0, st);  // stage timing as in the token-local loop (logits GEMM)
     rc = tc::launch_tc_gemm(&A, &B, &P, 1, dtype, sched, st);
   } else {
     Operand A{x, hidden, 1}, B{weight_shard, hidden, 1};
@@ -671,8 +672,12 @@ extern "C" int lk_flce_vp_backward2(const void* x, const void* weight_shard, con
   ce.label_smoothing = label_smoothing; ce.lse_square_scale = lse_square_scale; ce.softcap = softcap;
   ce.input_capped = 1; ce.reduction = reduction; ce.compute_grad = 1; ce.n_valid = n_non_ignore;
   ce.loss_rows = loss_rows; ce.row_stats = reinterpret_cast<const float4*>(row_stats_global);
-  int rc = launch_ce_ring(ce, dtype, st);  // persistent TMA ring; the block kernel for other shapes
-  if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dtype, st);
+  int rc;
+  {
+    ProfScope ps(1, st);  // finalize
+    rc = launch_ce_ring(ce, dtype, st);  // persistent TMA ring; the block kernel for other shapes
+    if (rc == LK_UNSUPPORTED) rc = launch_ce_rows(ce, dtype, st);
+  }
   if (rc) return rc;
   // dX partial (fp32 or the input dtype, all-reduced by the caller) and the local dW shard
   void* grad_x_partial_f32 = grad_x_partial;
@@ -714,6 +719,7 @@ extern "C" int lk_flce_vp_backward2(const void* x, const void* weight_shard, con
     if (!np) return LK_OK;
     int* sched = static_cast<int*>(workspace);
     LK_CUDA(cudaMemsetAsync(sched, 0, 64, st));
+    ProfScope ps(2, st);  // backward GEMM (dX partial + dW shard)
     return tc::launch_tc_gemm(As, Bs, Ps, np, dtype, sched, st);
   }
   if (grad_x_partial_f32) {
