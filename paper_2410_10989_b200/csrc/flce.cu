@@ -309,14 +309,14 @@ extern "C" size_t lk_flce_workspace_bytes(int64_t bt, int64_t hidden, int64_t vo
                                           int64_t chunk_rows, int has_grad_w) {
   bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
   return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, LK_ACCUM_AUTO,
-                     use_tc32_path(dtype, hidden, 0), 2, true).total;
+                     use_tc32_path(dtype, hidden, 0), 0, true).total;
 }
 
 extern "C" size_t lk_flce_workspace_bytes_ex(int64_t bt, int64_t hidden, int64_t vocab, int dtype,
                                              int64_t chunk_rows, int has_grad_w, int grad_w_accum) {
   bool tc = use_tc_path(dtype, hidden, nullptr, nullptr, 0);
   return flce_layout(bt, hidden, vocab, dtype, chunk_rows, has_grad_w != 0, true, tc, grad_w_accum,
-                     use_tc32_path(dtype, hidden, 0), 2, true).total;
+                     use_tc32_path(dtype, hidden, 0), 0, true).total;
 }
 
 static FlceLayout layout_for(const lk_flce_args* a) {

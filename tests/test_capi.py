@@ -65,6 +65,13 @@ def test_plan_and_workspace_queries():
     # more than 8 chunks: auto falls back to the fp32 accumulator
     assert lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 512, 1) > dw_acc
     assert lk.flce_plan(8192, 4096, 128256) == (2048, 4)
+    # the legacy size queries cover the exact-call query for the default options, fp32 included
+    # (fp32 runs on split operands with 3 pieces by default: 6 terms along K)
+    for dt, (bt, h, v) in ((0, (1024, 512, 4096)), (0, (300, 264, 5003)), (1, (8192, 4096, 128256))):
+        a = _capi.FlceArgs(bt=bt, hidden=h, vocab=v, dtype=dt, grad_x=1, grad_w=1)
+        exact = lib.lk_flce_workspace_bytes_for(C.byref(a))
+        assert lib.lk_flce_workspace_bytes(bt, h, v, dt, 0, 1) >= exact
+        assert lib.lk_flce_workspace_bytes_ex(bt, h, v, dt, 0, 1, _capi.LK_ACCUM_AUTO) >= exact
     for bt in (16384, 65536, 32768 + 5):  # the host restatement agrees with the library
         for h, v in ((4096, 128256), (3584, 256000), (512, 4096)):
             p = b200_plan(bt, v, h)
