@@ -45,7 +45,38 @@ int encode_operand(CUtensorMap* map, const TmaOperand& op, int dtype, int rows_i
   LK_REQUIRE(enc != nullptr, LK_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
   const CUtensorMapDataType dt =
       dtype == LK_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
-  cuuint32_t es[3] = {1u, 1u, 1u};
+  cuuint32_t es[4] = {1u, 1u, 1u, 1u};
+  if (op.pieces > 0) {
+    // piece-addressed operand: `pieces` [outer][inner] matrices, piece_elems apart; the piece
+    // is the last map coordinate (box extent 1), so a box lands exactly as modes 0 / 1 / 2 do
+    LK_REQUIRE((op.piece_elems * 2) % 16 == 0, LK_INVALID_ARGUMENT, "piece stride must be 16-byte aligned");
+    const cuuint64_t ps = (cuuint64_t)op.piece_elems * 2;
+    CUresult r;
+    if (!op.mn_major) {
+      cuuint64_t dims[3] = {(cuuint64_t)op.inner, (cuuint64_t)op.outer, (cuuint64_t)op.pieces};
+      cuuint64_t strides[2] = {(cuuint64_t)op.row_elems * 2, ps};
+      cuuint32_t box[3] = {64u, (cuuint32_t)rows_in_box, 1u};
+      r = enc(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      *mode = 3;
+    } else if (op.inner % 64 == 0) {
+      cuuint64_t dims[4] = {64u, (cuuint64_t)op.outer, (cuuint64_t)(op.inner / 64), (cuuint64_t)op.pieces};
+      cuuint64_t strides[3] = {(cuuint64_t)op.row_elems * 2, 128u, ps};
+      cuuint32_t box[4] = {64u, 64u, (cuuint32_t)(rows_in_box / 64), 1u};
+      r = enc(map, dt, 4, const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      *mode = 4;
+    } else {
+      cuuint64_t dims[3] = {(cuuint64_t)op.inner, (cuuint64_t)op.outer, (cuuint64_t)op.pieces};
+      cuuint64_t strides[2] = {(cuuint64_t)op.row_elems * 2, ps};
+      cuuint32_t box[3] = {64u, 64u, 1u};
+      r = enc(map, dt, 3, const_cast<void*>(op.ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      *mode = 5;
+    }
+    LK_REQUIRE(r == CUDA_SUCCESS, LK_CUDA_ERROR, "cuTensorMapEncodeTiled (pieces) failed: " + std::to_string((int)r));
+    return LK_OK;
+  }
   if (op.mn_major && g_allow_3d && op.inner % 64 == 0) {
     // [K rows][MN] viewed as {64 (MN within atom), K, MN/64 atoms}: one box {64, 64, atoms}
     // lands as `atoms` contiguous 8 KB SWIZZLE_128B atoms, the UMMA MN-major canonical layout.
@@ -125,6 +156,8 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     P.tiles_m = (int)((P.M + tile_m - 1) / tile_m);
     P.tiles_n = (int)((P.N + BN - 1) / BN);
     P.k_blocks = (int)((P.K + BK - 1) / BK);
+    LK_REQUIRE((a[p].pieces > 0) == (P.kb_term > 0) && (b[p].pieces > 0) == (P.kb_term > 0), LK_INVALID_ARGUMENT,
+               "piece-addressed operands and Problem::kb_term go together");
     int rc = encode_operand(&maps[2 * p], a[p], dtype, BM, &P.a_mode);
     if (rc) return rc;
     rc = encode_operand(&maps[2 * p + 1], b[p], dtype, b_rows_in_box, &P.b_mode);
@@ -215,7 +248,7 @@ struct FlceLayout {
   bool tc32;
   int pieces, nT;
   size_t off_counts, off_sched, off_z, off_parts, off_tgt, off_acc, off_bias;
-  size_t off_wk, off_wmn, off_xs, off_dzs;  // W' [V][nT][H], W'' [nT][ldz][H], X'_c [C][nT][H], dZ' [C][nT][ldz]
+  size_t off_wp, off_xp, off_dzp;  // bf16 pieces: W [P][V][H], X_c [P][C][H], dZ [P][C][ldz]
   size_t total;
 };
 
@@ -282,11 +315,11 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   L.off_tgt = take((tc || tc32) ? (size_t)L.C * sizeof(float) : 0);
   L.off_acc = take(L.need_acc ? (size_t)vocab * hidden * sizeof(float) : 0);
   L.off_bias = take(L.need_bias_acc ? (size_t)vocab * sizeof(float) : 0);
-  const size_t nT = (size_t)L.nT;
-  L.off_wk = take(tc32 ? (size_t)vocab * nT * hidden * 2 : 0);
-  L.off_wmn = take(tc32 && has_grad_x ? nT * (size_t)L.ldz * hidden * 2 : 0);
-  L.off_xs = take(tc32 ? (size_t)L.C * nT * hidden * 2 : 0);
-  L.off_dzs = take(tc32 ? (size_t)L.C * nT * L.ldz * 2 : 0);
+  (void)has_grad_x;
+  const size_t P = (size_t)L.pieces;
+  L.off_wp = take(tc32 ? P * (size_t)vocab * hidden * 2 : 0);
+  L.off_xp = take(tc32 ? P * (size_t)L.C * hidden * 2 : 0);
+  L.off_dzp = take(tc32 ? P * (size_t)L.C * L.ldz * 2 : 0);
   L.total = align_up(off, 1024);
   return L;
 }
@@ -355,13 +388,21 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
   LK_REQUIRE(a->workspace && a->workspace_bytes >= L.total, LK_INVALID_ARGUMENT,
              "workspace too small: need " + std::to_string(L.total) + " bytes");
   char* ws = static_cast<char*>(a->workspace);
-  const int* ordA = L.pieces == 3 ? kOrdA3 : kOrdA2;
-  const int* ordC = L.pieces == 3 ? kOrdC3 : kOrdC2;
-  const int64_t nT = L.nT;
-  void* wk = ws + L.off_wk;    // W'  [V][nT][H]       logits B (K-major), pieces in C order
-  void* wmn = ws + L.off_wmn;  // W'' [nT][ldz][H]     dX B (MN-major, K' = t*ldz + v), A order
-  void* xs = ws + L.off_xs;    // X'_c [r][nT][H]      logits A (K-major) / dW B (MN-major, K' = row*nT + t), A order
-  void* dzs = ws + L.off_dzs;  // dZ' [r][nT][ldz]     dX A (K-major) / dW A (MN-major), C order
+  // fp32 inputs: each operand is split ONCE into P bf16 pieces, stored piece-major; the GEMMs
+  // address the piece of each K run through a trailing tensor-map coordinate (load modes 3-5),
+  // so the term products i + j <= P - 1 need no duplicated copies
+  const int* ordA = L.pieces == 3 ? kOrdA3 : kOrdA2;  // piece of the left operand per term
+  const int* ordC = L.pieces == 3 ? kOrdC3 : kOrdC2;  // piece of the right operand per term
+  const int64_t nT = L.nT, NP = L.pieces;
+  static const int kIdent[3] = {0, 1, 2};
+  void* wp = ws + L.off_wp;    // W pieces    [P][V][H]:   logits B (K-major), dX B (MN-major, K = v)
+  void* xp = ws + L.off_xp;    // X_c pieces  [P][C][H]:   logits A (K-major), dW B (MN-major, K = row)
+  void* dzp = ws + L.off_dzp;  // dZ pieces   [P][C][ldz]: dX A (K-major, K = v), dW A (MN-major, K = row)
+  auto set_terms = [&](tc::Problem& Pr, int64_t k_run) {  // K = nT runs of ceil(k_run / 64) k-blocks
+    Pr.kb_term = (int)((k_run + tc::BK - 1) / tc::BK);
+    Pr.K = nT * Pr.kb_term * tc::BK;
+    for (int t = 0; t < nT; ++t) { Pr.pa[t] = (unsigned char)ordA[t]; Pr.pb[t] = (unsigned char)ordC[t]; }
+  };
   int64_t* counts = reinterpret_cast<int64_t*>(ws + L.off_counts);
   int* sched = reinterpret_cast<int*>(ws + L.off_sched);
   void* zbuf = ws + L.off_z;
@@ -407,12 +448,9 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     return record_rest();
   }
 
-  if (tc32) {  // split W once per call: W' for the logits GEMM, W'' (zero-padded to ldz rows) for dX
+  if (tc32) {  // split W once per call into its P pieces
     ProfScope ps(3, st);
-    rc = launch_split_bf16(static_cast<const float*>(a->weight), V, H, H, V, H, wk, nT * H, H, (int)nT, ordC, st);
-    if (!rc && a->grad_x)
-      rc = launch_split_bf16(static_cast<const float*>(a->weight), V, H, H, L.ldz, H, wmn, H, L.ldz * H, (int)nT,
-                             ordA, st);
+    rc = launch_split_bf16(static_cast<const float*>(a->weight), V, H, H, V, H, wp, H, V * H, (int)NP, kIdent, st);
     if (rc) return rc;
   }
 
@@ -423,7 +461,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     const bool first = ci == 0, last = ci == L.nchunks - 1;
     if (tc32) {
       ProfScope ps(3, st);
-      rc = launch_split_bf16(reinterpret_cast<const float*>(xc), r, H, H, r, H, xs, nT * H, H, (int)nT, ordA, st);
+      rc = launch_split_bf16(reinterpret_cast<const float*>(xc), r, H, H, r, H, xp, H, L.C * H, (int)NP, kIdent, st);
       if (rc) return rc;
     }
 
@@ -443,10 +481,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         // n-fastest measured 15% slower, profiles/README.md)
         P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
-      } else if (tc32) {  // fp32 logits = sum of the piece products, K' = nT * H
-        tc::TmaOperand A{xs, nT * H, r, nT * H, 0}, B{wk, nT * H, V, nT * H, 0};
+      } else if (tc32) {  // fp32 logits = sum over the terms of X piece ordA[t] . W piece ordC[t]
+        tc::TmaOperand A{xp, H, r, H, 0, (int)NP, L.C * H}, B{wp, H, V, H, 0, (int)NP, V * H};
         tc::Problem P{};
-        P.M = r; P.N = V; P.K = nT * H; P.n_fast = 0; P.epi = le;
+        P.M = r; P.N = V; P.n_fast = 0; P.epi = le;
+        set_terms(P, H);
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, LK_BF16, sched + 2 * ci, st);
       } else {
         Operand A{xc, H, 1}, B{a->weight, H, 1};
@@ -509,26 +548,29 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
       const bool fold = last && !separate_cast();
       we.acc = dwacc; we.ldacc = H; we.beta = first ? 0 : 1; we.final_out = fold ? 1 : 0;
     }
-    if (tc32) {  // dZ (fp32, in the chunk buffer) -> dZ' pieces, zero-padded to ldz columns
+    if (tc32) {  // dZ (fp32, in the chunk buffer) -> its P pieces, zero-padded to ldz columns
       ProfScope ps(3, st);
-      rc = launch_split_bf16(static_cast<const float*>(zbuf), r, V, L.ldz, r, L.ldz, dzs, nT * L.ldz, L.ldz,
-                             (int)nT, ordC, st);
+      rc = launch_split_bf16(static_cast<const float*>(zbuf), r, V, L.ldz, r, L.ldz, dzp, L.ldz, L.C * L.ldz,
+                             (int)NP, kIdent, st);
       if (rc) return rc;
       xe.kind = EPI_F32;  // dX in fp32 straight from the accumulator
     }
     ProfScope ps_bwd(2, st);
     if (tc || tc32) {
       const int gdt = tc32 ? LK_BF16 : dt;
-      // operands of the two backward problems: bf16 chunk / X for 16-bit inputs, the split
-      // pieces (K' = nT * V for dX, K' = nT * r for dW) for fp32 inputs
-      const tc::TmaOperand dxA = tc32 ? tc::TmaOperand{dzs, nT * L.ldz, r, nT * L.ldz, 0}
+      // operands of the two backward problems: the bf16 chunk / X for 16-bit inputs; for fp32
+      // inputs the piece-major dZ / W / X pieces, K = nT runs (dX: ldz per run, dW: r per run)
+      const int npc = tc32 ? (int)NP : 0;
+      const tc::TmaOperand dxA = tc32 ? tc::TmaOperand{dzp, L.ldz, r, L.ldz, 0, npc, L.C * L.ldz}
                                       : tc::TmaOperand{zbuf, V, r, L.ldz, 0};
-      const tc::TmaOperand dxB = tc32 ? tc::TmaOperand{wmn, H, nT * L.ldz, H, 1} : tc::TmaOperand{a->weight, H, V, H, 1};
-      const int64_t dxK = tc32 ? nT * L.ldz : V;
-      const int64_t dwK = tc32 ? nT * r : r;
-      const void* dwA_base = tc32 ? dzs : zbuf;
-      const int64_t dwA_ld = tc32 ? L.ldz : L.ldz;
-      const void* dwB_base = tc32 ? xs : xc;
+      const tc::TmaOperand dxB = tc32 ? tc::TmaOperand{wp, H, V, H, 1, npc, V * H} : tc::TmaOperand{a->weight, H, V, H, 1};
+      const void* dwA_base = tc32 ? dzp : zbuf;
+      const void* dwB_base = tc32 ? xp : xc;
+      auto dw_ops = [&](int64_t v0, int64_t v1, tc::TmaOperand& A, tc::TmaOperand& B) {
+        A = tc::TmaOperand{static_cast<const char*>(dwA_base) + v0 * (tc32 ? 2 : es), v1 - v0, r, L.ldz, 1, npc,
+                           L.C * L.ldz};
+        B = tc::TmaOperand{dwB_base, H, r, H, 1, npc, L.C * H};
+      };
       tc::TmaOperand As[2], Bs[2];
       tc::Problem Ps[2];
       int np = 0;
@@ -536,19 +578,22 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         As[np] = dxA;
         Bs[np] = dxB;
         Ps[np] = tc::Problem{};
-        Ps[np].M = r; Ps[np].N = H; Ps[np].K = dxK; Ps[np].n_fast = 0; Ps[np].epi = xe;
-        // fp32 dX (K' = nT * V): restart the truncating tensor-core accumulation every
-        // kFp32SegKb k-blocks and add the segments in fp32 (Problem::seg_kb)
-        if (tc32) Ps[np].seg_kb = kFp32SegKb;
+        Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
+        if (tc32) {
+          set_terms(Ps[np], L.ldz);
+          // fp32 dX (K = nT x ldz): restart the truncating tensor-core accumulation every
+          // kFp32SegKb k-blocks and add the segments in fp32 (Problem::seg_kb)
+          Ps[np].seg_kb = kFp32SegKb;
+        }
         ++np;
       }
       const int slices =
           (last && a->grad_w && n_events >= 2 && n_events <= LK_MAX_GRAD_W_SLICES) ? n_events : 1;
       if (a->grad_w && slices <= 1) {
-        As[np] = {dwA_base, V, dwK, dwA_ld, 1};
-        Bs[np] = {dwB_base, H, dwK, H, 1};
+        dw_ops(0, V, As[np], Bs[np]);
         Ps[np] = tc::Problem{};
-        Ps[np].M = V; Ps[np].N = H; Ps[np].K = dwK; Ps[np].n_fast = 1; Ps[np].epi = we;
+        Ps[np].M = V; Ps[np].N = H; Ps[np].K = r; Ps[np].n_fast = 1; Ps[np].epi = we;
+        if (tc32) set_terms(Ps[np], r);
         ++np;
       }
       if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, gdt, sched + 2 * ci + 1, st);
@@ -562,10 +607,11 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
           ws.out = static_cast<char*>(a->grad_w) + v0 * H * es;
           if (ws.acc) ws.acc = ws.acc + v0 * H;
           ws.M = v1 - v0;
-          tc::TmaOperand As1{static_cast<const char*>(dwA_base) + v0 * (tc32 ? 2 : es), v1 - v0, dwK, dwA_ld, 1};
-          tc::TmaOperand Bs1{dwB_base, H, dwK, H, 1};
+          tc::TmaOperand As1, Bs1;
+          dw_ops(v0, v1, As1, Bs1);
           tc::Problem P1{};
-          P1.M = v1 - v0; P1.N = H; P1.K = dwK; P1.n_fast = 1; P1.epi = ws;
+          P1.M = v1 - v0; P1.N = H; P1.K = r; P1.n_fast = 1; P1.epi = ws;
+          if (tc32) set_terms(P1, r);
           rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, gdt, sched + 2 * L.nchunks + 2 + sl, st);
         }
         if (!rc) {

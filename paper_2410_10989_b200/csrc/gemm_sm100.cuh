@@ -41,7 +41,8 @@ struct Problem {
   int64_t M, N, K;
   int tiles_m, tiles_n, k_blocks;
   // operand load mode: 0 = K-major (one 2D box), 1 = MN-major via one 3D box
-  // {64, 64 K, atoms}, 2 = MN-major via one 2D box per 64-wide atom
+  // {64, 64 K, atoms}, 2 = MN-major via one 2D box per 64-wide atom; 3 / 4 / 5 = the same
+  // three with a trailing piece coordinate (3D / 4D / 3D maps over [piece][rows][cols])
   int a_mode, b_mode;
   int n_fast;           // tile id -> (m, n): 1 = n varies fastest
   int tma_out;          // 1: epilogue writes through smem staging + TMA store (map mc<p>)
@@ -53,6 +54,11 @@ struct Problem {
   // truncates at every MMA (scripts/probe_tc_accum.py: the error grows with the number of
   // K=16 steps), so long-K fp32 problems keep each truncated run short.  0 = off.
   int seg_kb;
+  // Piece-addressed K (fp32 split operands, a_mode / b_mode 3-5): K is n_terms runs of kb_term
+  // k-blocks; run t reads piece pa[t] of A and pb[t] of B at K offset (kb mod kb_term) * 64 of
+  // that piece (0 = plain K).
+  int kb_term;
+  unsigned char pa[8], pb[8];
   EpiArgs epi;
 };
 
@@ -125,6 +131,31 @@ __device__ __forceinline__ void tma_3d(uint64_t map, uint32_t bar, uint32_t dst,
       "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
       ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
       : "memory");
+}
+__device__ __forceinline__ void tma_4d(uint64_t map, uint32_t bar, uint32_t dst, int x, int y, int z, int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+// Operand load modes 1, 2, 4, 5 land the MN-major canonical layout; 0 and 3 the K-major one.
+__device__ __forceinline__ int mode_mn(int mode) { return (mode != 0 && mode != 3) ? 1 : 0; }
+// One operand box of a k-block (1-CTA kernel): mode as in Problem::a_mode, `atoms` 64-wide MN
+// atoms in the box, k0 the K offset (inside the piece for modes 3-5), pc the piece.
+__device__ __forceinline__ void load_operand(uint64_t map, int mode, uint32_t bar, uint32_t dst, int k0, int mn0,
+                                             int atoms, int pc) {
+  switch (mode) {
+    case 0: tma_2d(map, bar, dst, k0, mn0); break;
+    case 1: tma_3d(map, bar, dst, 0, k0, mn0 >> 6); break;
+    case 2:
+      for (int j = 0; j < atoms; ++j) tma_2d(map, bar, dst + j * 8192, mn0 + 64 * j, k0);
+      break;
+    case 3: tma_3d(map, bar, dst, k0, mn0, pc); break;
+    case 4: tma_4d(map, bar, dst, 0, k0, mn0 >> 6, pc); break;
+    default:
+      for (int j = 0; j < atoms; ++j) tma_3d(map, bar, dst + j * 8192, mn0 + 64 * j, k0, pc);
+      break;
+  }
 }
 __device__ __forceinline__ void tma_prefetch_2d(uint64_t map, int x, int y) {
   asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y)
@@ -793,31 +824,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       const uint64_t ma = reinterpret_cast<uint64_t>(p ? &ma1 : &ma0);
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = tcd.m_blk * BM, n0 = tcd.n_blk * BN;
+      const Problem& PP = args.prob[p];
+      int term = 0, kt = 0;  // piece-addressed K: run index and k-block inside the run
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
         if (elect_one()) {
           const uint32_t fb = full0 + stage * 8;
           mbar_expect_tx_addr(fb, STAGE_BYTES);
           const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
-          const int k0 = kb * BK;
-          // mode 0: K-major 2D {64 K, rows}; 1: MN-major 3D {64, 64 K, atoms}; 2: MN-major 2D per atom
-          if (a_mode == 0) {
-            tma_2d(ma, fb, a_dst, k0, m0);
-          } else if (a_mode == 1) {
-            tma_3d(ma, fb, a_dst, 0, k0, m0 >> 6);
-          } else {
-            tma_2d(ma, fb, a_dst, m0, k0);
-            tma_2d(ma, fb, a_dst + 8192, m0 + 64, k0);
-          }
-          if (b_mode == 0) {
-            tma_2d(mb, fb, b_dst, k0, n0);
-          } else if (b_mode == 1) {
-            tma_3d(mb, fb, b_dst, 0, k0, n0 >> 6);
-          } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) tma_2d(mb, fb, b_dst + j * 8192, n0 + 64 * j, k0);
-          }
+          // mode 0: K-major 2D {64 K, rows}; 1: MN-major 3D {64, 64 K, atoms}; 2: MN-major 2D per atom;
+          // 3-5: the same with a piece coordinate
+          const int k0 = (PP.kb_term ? kt : kb) * BK;
+          load_operand(ma, a_mode, fb, a_dst, k0, m0, BM / 64, PP.pa[term]);
+          load_operand(mb, b_mode, fb, b_dst, k0, n0, BN / 64, PP.pb[term]);
         }
+        if (PP.kb_term && ++kt == PP.kb_term) { kt = 0; ++term; }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -836,8 +857,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       if (tile < 0) break;
       const TileCoord tcd = decode_tile(args, tile);
       const int p = tcd.p;
-      const int a_mn = (p ? args.prob[1].a_mode : args.prob[0].a_mode) != 0;
-      const int b_mn = (p ? args.prob[1].b_mode : args.prob[0].b_mode) != 0;
+      const int a_mn = tc::mode_mn(p ? args.prob[1].a_mode : args.prob[0].a_mode);
+      const int b_mn = tc::mode_mn(p ? args.prob[1].b_mode : args.prob[0].b_mode);
       const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
       const int seg_kb = seg_len(args.prob[p]);
       const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];
@@ -935,6 +956,8 @@ struct TmaOperand {
   int64_t inner, outer;  // elements
   int64_t row_elems;     // row stride in elements
   int mn_major;          // 0: inner dim is K; 1: inner dim is M/N
+  int pieces = 0;        // > 0: `pieces` such matrices, piece_elems apart (load modes 3-5)
+  int64_t piece_elems = 0;
 };
 
 // Encodes the operand's tensor map and returns its load mode (0/1/2, see Problem).

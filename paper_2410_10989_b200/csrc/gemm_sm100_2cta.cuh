@@ -88,6 +88,31 @@ __device__ __forceinline__ void tma_3d_cg2(uint64_t map, uint32_t bar, uint32_t 
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z)
       : "memory");
 }
+__device__ __forceinline__ void tma_4d_cg2(uint64_t map, uint32_t bar, uint32_t dst, int x, int y, int z, int w) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(x), "r"(y), "r"(z), "r"(w)
+      : "memory");
+}
+// One operand half-box of a k-block (CTA pair): 128 rows / columns = 2 atoms; modes as in
+// Problem::a_mode (3-5 carry the piece coordinate `pc`).
+__device__ __forceinline__ void load_operand2(uint64_t map, int mode, uint32_t bar, uint32_t dst, int k0, int mn0,
+                                              int pc) {
+  switch (mode) {
+    case 0: tma_2d_cg2(map, bar, dst, k0, mn0); break;
+    case 1: tma_3d_cg2(map, bar, dst, 0, k0, mn0 >> 6); break;
+    case 2:
+      tma_2d_cg2(map, bar, dst, mn0, k0);
+      tma_2d_cg2(map, bar, dst + 8192, mn0 + 64, k0);
+      break;
+    case 3: tma_3d_cg2(map, bar, dst, k0, mn0, pc); break;
+    case 4: tma_4d_cg2(map, bar, dst, 0, k0, mn0 >> 6, pc); break;
+    default:
+      tma_3d_cg2(map, bar, dst, mn0, k0, pc);
+      tma_3d_cg2(map, bar, dst + 8192, mn0 + 64, k0, pc);
+      break;
+  }
+}
 __device__ __forceinline__ void umma2_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                           uint32_t accum) {
   asm volatile(
@@ -204,32 +229,21 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = pt.m_blk * PBM + (int)rank * HALF;
       const int n0 = pt.n_blk * PBN + (int)rank * HALF;
+      const Problem& PP = args.prob[p];
+      int term = 0, kt = 0;  // piece-addressed K: run index and k-block inside the run
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
         if (elect_one()) {
           const uint32_t fb = leader_full0 + stage * 8;
           if (leader) mbar_expect_tx_addr(full0 + stage * 8, 2 * STAGE_BYTES);
           const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
-          const int k0 = kb * BK;
-          if (a_mode == 0) {
-            tma_2d_cg2(ma, fb, a_dst, k0, m0);
-          } else if (a_mode == 1) {
-            tma_3d_cg2(ma, fb, a_dst, 0, k0, m0 >> 6);
-          } else {
-            tma_2d_cg2(ma, fb, a_dst, m0, k0);
-            tma_2d_cg2(ma, fb, a_dst + 8192, m0 + 64, k0);
-          }
-          if (b_mode == 0) {
-            tma_2d_cg2(mb, fb, b_dst, k0, n0);
-          } else if (b_mode == 1) {
-            tma_3d_cg2(mb, fb, b_dst, 0, k0, n0 >> 6);
-          } else {
-            tma_2d_cg2(mb, fb, b_dst, n0, k0);
-            tma_2d_cg2(mb, fb, b_dst + 8192, n0 + 64, k0);
-          }
+          const int k0 = (PP.kb_term ? kt : kb) * BK;
+          load_operand2(ma, a_mode, fb, a_dst, k0, m0, PP.pa[term]);
+          load_operand2(mb, b_mode, fb, b_dst, k0, n0, PP.pb[term]);
           // (L2 prefetch of the B operand 8/16/32 k-blocks ahead measured 5-7% slower on the
           // logits GEMM: the stall was the epilogue, not operand latency; profiles/README.md)
         }
+        if (PP.kb_term && ++kt == PP.kb_term) { kt = 0; ++term; }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -248,8 +262,8 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
         if (lane == 0) mbar_arrive(&sempty[slot]);
         if (tile < 0) break;
         const int p = tile >= args.tiles0 ? 1 : 0;
-        const int a_mn = (p ? args.prob[1].a_mode : args.prob[0].a_mode) != 0;
-        const int b_mn = (p ? args.prob[1].b_mode : args.prob[0].b_mode) != 0;
+        const int a_mn = tc::mode_mn(p ? args.prob[1].a_mode : args.prob[0].a_mode);
+        const int b_mn = tc::mode_mn(p ? args.prob[1].b_mode : args.prob[0].b_mode);
         const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
         const int seg_kb = tc::seg_len(args.prob[p]);
         const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];

@@ -4,16 +4,18 @@
 // rounding of what the previous ones left (a - a0 is exact in fp32), |r| <= 2^-8P |a|.
 // A product a*b is then the sum of the piece products a_i*b_j with i + j <= P - 1 (3 terms
 // for P = 2, 6 for P = 3; the dropped terms are below 2^-8P relative).  Instead of a new
-// GEMM kernel, the terms are laid out ALONG K: the split operand holds nT = P(P+1)/2
-// copies of the matrix, term t holding piece order[t], so the unchanged bf16 tcgen05 GEMM
-// over K' = nT * K accumulates every term into the same fp32 TMEM accumulator.  The two
-// operands of a GEMM use complementary orders (a_t, c_t) that enumerate the pairs
-// i + j <= P - 1 (flce.cu fp32 section).  With P = 2 the per-product error (~2^-16) is
-// below fp32's own accumulation error bound at K >= 256; P = 3 matches fp32 products.
+// GEMM kernel, the terms are laid out ALONG K: the unchanged bf16 tcgen05 GEMM runs K as
+// nT = P(P+1)/2 runs, run t reading piece pa[t] of A and pb[t] of B through a trailing
+// tensor-map coordinate (gemm_sm100.cuh load modes 3-5), and accumulates every term into the
+// same fp32 TMEM accumulator.  Each operand is therefore split ONCE into P pieces stored
+// piece-major (round 2: the first version wrote nT term copies of every operand -- and a
+// second, MN-major copy of W for dX -- 2-4x the memory and split traffic; fp32 FLCE at the
+// cfg2 shape went 162 -> 134 ms).  P = 3 matches fp32 products; P = 2 (~2^-16 per product)
+// is available.
 //
 // dst(row, t, col) = piece[order[t]] of src(row, col) at dst + row*row_stride +
 // t*term_stride + col, for row < rows_pad, col < cols_pad; rows >= rows or cols >= cols
-// are written as zeros (the padding the concatenated K dimension reads must be finite).
+// are written as zeros (the padding the K runs read must be finite).
 #include "common.cuh"
 
 namespace lk {
