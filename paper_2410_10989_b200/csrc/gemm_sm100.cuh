@@ -824,8 +824,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
       const uint64_t ma = reinterpret_cast<uint64_t>(p ? &ma1 : &ma0);
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = tcd.m_blk * BM, n0 = tcd.n_blk * BN;
+      const int kbt = p ? args.prob[1].kb_term : args.prob[0].kb_term;
       const Problem& PP = args.prob[p];
-      int term = 0, kt = 0;  // piece-addressed K: run index and k-block inside the run
+      int term = 0, kt = 0;  // piece-addressed K (kbt > 0): run index and k-block inside the run
       for (int kb = 0; kb < kblocks; ++kb) {
         mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
         if (elect_one()) {
@@ -834,11 +835,15 @@ gemm_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CUt
           const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
           // mode 0: K-major 2D {64 K, rows}; 1: MN-major 3D {64, 64 K, atoms}; 2: MN-major 2D per atom;
           // 3-5: the same with a piece coordinate
-          const int k0 = (PP.kb_term ? kt : kb) * BK;
-          load_operand(ma, a_mode, fb, a_dst, k0, m0, BM / 64, PP.pa[term]);
-          load_operand(mb, b_mode, fb, b_dst, k0, n0, BN / 64, PP.pb[term]);
+          if (kbt == 0) {
+            load_operand(ma, a_mode, fb, a_dst, kb * BK, m0, BM / 64, 0);
+            load_operand(mb, b_mode, fb, b_dst, kb * BK, n0, BN / 64, 0);
+          } else {
+            load_operand(ma, a_mode, fb, a_dst, kt * BK, m0, BM / 64, PP.pa[term]);
+            load_operand(mb, b_mode, fb, b_dst, kt * BK, n0, BN / 64, PP.pb[term]);
+          }
         }
-        if (PP.kb_term && ++kt == PP.kb_term) { kt = 0; ++term; }
+        if (kbt && ++kt == kbt) { kt = 0; ++term; }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }

@@ -229,23 +229,57 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = pt.m_blk * PBM + (int)rank * HALF;
       const int n0 = pt.n_blk * PBN + (int)rank * HALF;
-      const Problem& PP = args.prob[p];
-      int term = 0, kt = 0;  // piece-addressed K: run index and k-block inside the run
-      for (int kb = 0; kb < kblocks; ++kb) {
-        mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
-        if (elect_one()) {
-          const uint32_t fb = leader_full0 + stage * 8;
-          if (leader) mbar_expect_tx_addr(full0 + stage * 8, 2 * STAGE_BYTES);
-          const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
-          const int k0 = (PP.kb_term ? kt : kb) * BK;
-          load_operand2(ma, a_mode, fb, a_dst, k0, m0, PP.pa[term]);
-          load_operand2(mb, b_mode, fb, b_dst, k0, n0, PP.pb[term]);
-          // (L2 prefetch of the B operand 8/16/32 k-blocks ahead measured 5-7% slower on the
-          // logits GEMM: the stall was the epilogue, not operand latency; profiles/README.md)
+      const int kbt = p ? args.prob[1].kb_term : args.prob[0].kb_term;
+      if (kbt == 0) {
+        // plain K (16-bit inputs): the producer issues 2-4 TMAs per 512-cycle k-block and sits
+        // on the critical path -- per-k-block work here costs the GEMM directly (a generic
+        // mode switch + piece bookkeeping in this loop measured 3% slower)
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
+          if (elect_one()) {
+            const uint32_t fb = leader_full0 + stage * 8;
+            if (leader) mbar_expect_tx_addr(full0 + stage * 8, 2 * STAGE_BYTES);
+            const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
+            const int k0 = kb * BK;
+            if (a_mode == 0) {
+              tma_2d_cg2(ma, fb, a_dst, k0, m0);
+            } else if (a_mode == 1) {
+              tma_3d_cg2(ma, fb, a_dst, 0, k0, m0 >> 6);
+            } else {
+              tma_2d_cg2(ma, fb, a_dst, m0, k0);
+              tma_2d_cg2(ma, fb, a_dst + 8192, m0 + 64, k0);
+            }
+            if (b_mode == 0) {
+              tma_2d_cg2(mb, fb, b_dst, k0, n0);
+            } else if (b_mode == 1) {
+              tma_3d_cg2(mb, fb, b_dst, 0, k0, n0 >> 6);
+            } else {
+              tma_2d_cg2(mb, fb, b_dst, n0, k0);
+              tma_2d_cg2(mb, fb, b_dst + 8192, n0 + 64, k0);
+            }
+            // (L2 prefetch of the B operand 8/16/32 k-blocks ahead measured 5-7% slower on the
+            // logits GEMM: the stall was the epilogue, not operand latency; profiles/README.md)
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        if (PP.kb_term && ++kt == PP.kb_term) { kt = 0; ++term; }
-        __syncwarp();
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      } else {
+        // piece-addressed K (fp32 split operands): run `term` reads pieces pa / pb[term]
+        const Problem& PP = args.prob[p];
+        int term = 0, kt = 0;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait_addr(empty0 + stage * 8, phase ^ 1);
+          if (elect_one()) {
+            const uint32_t fb = leader_full0 + stage * 8;
+            if (leader) mbar_expect_tx_addr(full0 + stage * 8, 2 * STAGE_BYTES);
+            const uint32_t a_dst = sA0 + stage * A_BYTES, b_dst = sB0 + stage * B_BYTES;
+            load_operand2(ma, a_mode, fb, a_dst, kt * BK, m0, PP.pa[term]);
+            load_operand2(mb, b_mode, fb, b_dst, kt * BK, n0, PP.pb[term]);
+          }
+          if (++kt == kbt) { kt = 0; ++term; }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
       }
     }
   } else if (warp == 1) {
