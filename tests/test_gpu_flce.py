@@ -389,6 +389,40 @@ def test_grad_w_slices_with_events_bitwise(slices, accum_dtype):
     assert torch.equal(a[2], b_gx) and torch.equal(a[3], b_gw)
 
 
+@pytest.mark.parametrize("slices", [2, 5])
+def test_fp32_grad_w_slices_with_events_bitwise(slices):
+    """The same hook on the fp32 split-operand path: each slice re-addresses the dZ pieces at a
+    vocab-row offset (piece-major layout, Problem::kb_term runs), bitwise equal to one launch."""
+    g = torch.Generator(device="cuda").manual_seed(32)
+    x = torch.rand(700, 256, device="cuda", generator=g) * 2 - 1
+    w = (torch.rand(3000, 256, device="cuda", generator=g) * 2 - 1) / 16
+    t = torch.randint(0, 3000, (700,), device="cuda", generator=g)
+    a = flce(x, w, t, chunk_rows=300)
+    events = [torch.cuda.Event() for _ in range(slices)]
+    b_loss, _, _, _, b_gx, b_gw, _ = flce_fwd(x, w, t, compute_grad_input=True, compute_grad_weight=True,
+                                              chunk_rows=300, grad_w_slice_events=events)
+    torch.cuda.synchronize()
+    assert a[0].item() == b_loss.item()
+    assert torch.equal(a[2], b_gx) and torch.equal(a[3], b_gw)
+
+
+@pytest.mark.parametrize("shape", [(1, 8, 5), (3, 16, 77), (65, 72, 130), (129, 64, 4096)])
+def test_fp32_split_path_tiny_and_ragged_shapes(shape):
+    """fp32 split-operand path at the edges of its K runs: one row, H = 8 (a run of one partial
+    k-block), V below and across the 64-column padding, chunk rows not a multiple of 64 --
+    against the float64 oracle at the fp32 tolerance."""
+    bt, h, v = shape
+    rng = np.random.default_rng(bt * 7 + h)
+    x = rng.uniform(-1, 1, (bt, h)).astype(np.float32)
+    w = (rng.uniform(-1, 1, (v, h)) / math.sqrt(h)).astype(np.float32)
+    t = rng.integers(0, v, bt)
+    ref_loss, _, _, rgx, rgw, _ = liger_ref.flce(x.astype(np.float64), w.astype(np.float64), t)
+    loss, _, gx, gw, _ = flce(cuda(x), cuda(w), cuda(t, torch.long), chunk_rows=max(1, bt // 2))
+    assert loss.item() == pytest.approx(ref_loss, rel=1e-4)
+    assert rel_close(gx.double().cpu().numpy(), rgx, 1e-4)[0]
+    assert rel_close(gw.double().cpu().numpy(), rgw, 1e-4)[0]
+
+
 @pytest.mark.parametrize("simt", [False, True])
 @pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0, lse_square_scale=1e-4)])
 def test_flce_use_token_scaling(simt, kw):
