@@ -192,3 +192,11 @@ def test_world2_rank_with_only_ignored_tokens(mode):
     """A rank whose token shard is all ignore_index contributes zero loss/dX but still joins
     every collective; the mean denominator is the global valid count."""
     run_world(mode, dict(), prob=dict(ignore_first_half=True))
+
+
+@pytest.mark.parametrize("mode", ["token", "vocab"])
+def test_world4_matches_single_process(mode):
+    """Four ranks (the 8xB200 box's scaling points are 1/2/4/8): ragged token and vocab shards,
+    smoothing + softcap on the vocab path, against the single-process oracle."""
+    kw = dict(label_smoothing=0.1) if mode == "token" else dict(softcap=3.0, label_smoothing=0.1)
+    run_world(mode, kw, world=4, prob=dict(bt=30))
