@@ -70,6 +70,17 @@ def _local_flce_cuda(x, w, t, mean_count, reduction="mean", **kw):
     return loss, gx, gw
 
 
+_COMM_STREAMS: dict = {}
+
+
+def _comm_stream(device: torch.device) -> torch.cuda.Stream:
+    """One side stream per device for the overlapped grad_w all-reduce (created once)."""
+    key = torch.device(device).index
+    if key not in _COMM_STREAMS:
+        _COMM_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _COMM_STREAMS[key]
+
+
 def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw):
     """Local FLCE whose last-chunk grad_w GEMM is split into `dw_slices` vocab-row slices;
     slice s is all-reduced on a side stream as soon as its event fires, so all but the last
@@ -81,7 +92,7 @@ def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw
     v = gw.shape[0]
     step = -(-v // dw_slices)
     rows = -(-step // 256) * 256  # same slice bounds as the library (flce.cu)
-    comm = torch.cuda.Stream(device=gw.device)
+    comm = _comm_stream(gw.device)
     for s, ev in enumerate(events):
         lo, hi = s * rows, min(v, (s + 1) * rows)
         comm.wait_event(ev)
