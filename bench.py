@@ -409,7 +409,7 @@ def run_ours(args):
     xg = (torch.rand(global_bt, h, device=dev, generator=g) * 2 - 1).to(torch.bfloat16)
     w = ((torch.rand(v, h, device=dev, generator=g) * 2 - 1) / 64.0).to(torch.bfloat16)
     tg = torch.randint(0, v, (global_bt,), device=dev, generator=g)
-    tg[torch.rand(global_bt, device=dev, generator=g) < IGNORE_FRAC] = -100
+    tg[torch.rand(global_bt, device=dev, generator=g) < args.ignore_frac] = -100
     x, t = xg[lo:hi].contiguous(), tg[lo:hi].contiguous()
     del xg, tg
     chunk = args.chunk_rows or flce_plan(bt, h, v)[0]
@@ -601,7 +601,7 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform X, W, 10% ignore_index targets; "
                                                           "one seed-0 global batch split by rows across ranks)",
             "config": {
-                "workload": workload, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
+                "workload": workload, "ignore_frac": args.ignore_frac, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
                 "softcap": args.softcap, "label_smoothing": args.label_smoothing,
                 "num_chunks": -(-bt // chunk), "global_tokens": tokens_per_step,
                 "parallelism": (f"vocab-parallel vp{world}" if vocab_mode else
@@ -689,6 +689,8 @@ def main():
                          "head with softcap 30 + smoothing 0.1; cfg5 = 65536 global tokens (strong scaling)")
     ap.add_argument("--softcap", type=float, default=None)
     ap.add_argument("--label-smoothing", type=float, default=0.0)
+    ap.add_argument("--ignore-frac", type=float, default=IGNORE_FRAC,
+                    help="fraction of targets set to ignore_index (the headline config uses 0.1)")
     ap.add_argument("--mode", choices=["token", "vocab"], default="token",
                     help="multi-GPU shard mode: token-sharded (default) or vocab-parallel (strong)")
     ap.add_argument("--cpu-rows", type=int, default=256)
