@@ -291,3 +291,24 @@ def test_ce_unaligned_logits_vs_oracle():
     assert rel_close(loss.item(), rl, 2e-2)[0]
     ok, err = rel_close(x.grad.float().cpu().numpy(), rg, 2e-2)
     assert ok, err
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("spread", [60.0, 1000.0])
+def test_ce_extreme_logit_spread_stable(dtype, spread):
+    """Online softmax with huge logit ranges (one dominant logit per row, the rest spread by
+    `spread`): loss = lse - z_t exactly as Liger (no log(max(p, tiny)) clamp, SURVEY §8(a)
+    edge-case note), gradients finite, against the float64 oracle.  Rows span the ring's
+    multi-piece path (V = 40000)."""
+    rng = np.random.default_rng(7)
+    rows, v = 16, 40000
+    z = rng.uniform(-spread, 0.0, (rows, v)).astype(np.float32)
+    hot = rng.integers(0, v, rows)
+    z[np.arange(rows), hot] = spread  # one dominant logit per row
+    t = np.where(np.arange(rows) % 2 == 0, hot, rng.integers(0, v, rows))  # half hit it, half miss
+    zin = torch.tensor(z, dtype=dtype).float().numpy()
+    ref_loss, ref_rows, _, ref_grad = liger_ref.ce(zin, t, reduction="none")
+    loss, grad = run_ce(z, t, dtype, reduction="none")
+    assert np.all(np.isfinite(loss)) and np.all(np.isfinite(grad))
+    assert rel_close(loss, ref_rows, TOL[dtype])[0]
+    assert rel_close(grad, ref_grad, TOL[dtype])[0]
