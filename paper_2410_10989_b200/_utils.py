@@ -26,12 +26,21 @@ def dtype_code(t: torch.Tensor) -> int:
 
 
 def require_cuda(*tensors: torch.Tensor | None) -> None:
+    """Every operand on CUDA and on the same device (the kernels launch on one device and read
+    their operands through plain device pointers)."""
+    dev = None
     for t in tensors:
-        if t is not None and not t.is_cuda:
+        if t is None:
+            continue
+        if not t.is_cuda:
             raise errors.ExtensionMissing(
                 "paper_2410_10989_b200 runs only on CUDA (sm_100a); got a tensor on "
                 f"{t.device}. There is no CPU fallback."
             )
+        if dev is None:
+            dev = t.device
+        elif t.device != dev:
+            raise errors.ShapeMismatch(f"operands on different devices: {dev} and {t.device}")
 
 
 def require_contiguous(name: str, t: torch.Tensor) -> None:

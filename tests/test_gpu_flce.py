@@ -515,3 +515,12 @@ def test_flce_in_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(eager, out))
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
+def test_operands_on_different_devices_raise():
+    x = torch.randn(8, 64, device="cuda:0", dtype=torch.bfloat16)
+    w = torch.randn(128, 64, device="cuda:1", dtype=torch.bfloat16)
+    t = torch.randint(0, 128, (8,), device="cuda:0")
+    with pytest.raises(errors.ShapeMismatch):
+        flce_fwd(x, w, t)
