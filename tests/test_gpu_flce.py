@@ -524,3 +524,19 @@ def test_operands_on_different_devices_raise():
     t = torch.randint(0, 128, (8,), device="cuda:0")
     with pytest.raises(errors.ShapeMismatch):
         flce_fwd(x, w, t)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_single_cta_gemm_path_matches_pair(path_knob, dtype):
+    """The single-CTA tcgen05 kernel (test knob) with the same operand load modes as the CTA
+    pair -- including the piece-addressed fp32 modes 3-5 -- gives the same FLCE results."""
+    g = torch.Generator(device="cuda").manual_seed(41)
+    x = (torch.rand(300, 264, device="cuda", generator=g) * 2 - 1).to(dtype)
+    w = ((torch.rand(2000, 264, device="cuda", generator=g) * 2 - 1) / 16).to(dtype)
+    t = torch.randint(0, 2000, (300,), device="cuda", generator=g)
+    ref = flce(x, w, t, chunk_rows=128)
+    path_knob(_capi.PATH_CTA_GROUP, 1)
+    one = flce(x, w, t, chunk_rows=128)
+    tol = 1e-5 if dtype == torch.float32 else 1e-2
+    assert abs(one[0].item() - ref[0].item()) <= tol * abs(ref[0].item())
+    assert close(one[2], ref[2], tol) and close(one[3], ref[3], tol)
