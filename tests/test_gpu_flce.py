@@ -540,3 +540,60 @@ def test_single_cta_gemm_path_matches_pair(path_knob, dtype):
     tol = 1e-5 if dtype == torch.float32 else 1e-2
     assert abs(one[0].item() - ref[0].item()) <= tol * abs(ref[0].item())
     assert close(one[2], ref[2], tol) and close(one[3], ref[3], tol)
+
+
+def _random_flce_cases(n=40, seed=2024):
+    """Seeded random FLCE configurations over the option space and the shape edges."""
+    rng = np.random.default_rng(seed)
+    cases = []
+    for i in range(n):
+        dtype = [torch.float32, torch.bfloat16, torch.float16][i % 3]
+        bt = int(rng.choice([1, 7, 64, 130, 333, 700]))
+        h = int(rng.choice([8, 24, 64, 136, 256, 520]))
+        v = int(rng.choice([5, 63, 257, 1000, 4099]))
+        opts = {}
+        if rng.random() < 0.4:
+            opts["label_smoothing"] = float(rng.choice([0.05, 0.1, 0.3]))
+        if rng.random() < 0.3:
+            opts["softcap"] = float(rng.choice([5.0, 30.0]))
+        if rng.random() < 0.2:
+            opts["lse_square_scale"] = 1e-3
+        opts["reduction"] = str(rng.choice(["mean", "sum", "none"]))
+        chunk = int(rng.choice([0, 1, 32, 100, 256]))
+        cases.append((i, dtype, bt, h, v, opts, chunk, bool(rng.random() < 0.25), float(rng.choice([0.0, 0.1, 0.5]))))
+    return cases
+
+
+@pytest.mark.parametrize("case", _random_flce_cases(), ids=lambda c: f"c{c[0]}")
+def test_flce_random_configs_vs_oracle(case):
+    """40 seeded random configurations (fp32 / bf16 / fp16; 1..700 rows; H from 8 (one partial
+    k-block) to 520; V from 5 to 4099; smoothing, softcap, z-loss, bias, all reductions,
+    chunk sizes 1..256 and the default; 0-50% ignored targets) against the float64 oracle at
+    the north-star tolerance of the dtype, with ignored rows exactly zero."""
+    i, dtype, bt, h, v, opts, chunk, use_bias, ign = case
+    rng = np.random.default_rng(1000 + i)
+    x = rng.uniform(-1, 1, (bt, h))
+    w = rng.uniform(-1, 1, (v, h)) / math.sqrt(h) * 3
+    b = rng.normal(size=v) * 0.5 if use_bias else None
+    t = rng.integers(0, v, bt)
+    t[rng.random(bt) < ign] = -100
+    xd = torch.tensor(x, dtype=dtype, device="cuda")
+    wd = torch.tensor(w, dtype=dtype, device="cuda")
+    bd = torch.tensor(b, dtype=dtype, device="cuda") if b is not None else None
+    td = torch.tensor(t, device="cuda")
+    ref = liger_ref.flce(xd.double().cpu().numpy(), wd.double().cpu().numpy(), t,
+                         bias=None if bd is None else bd.double().cpu().numpy(), **opts)
+    loss, _, _, _, gx, gw, gb = flce_fwd(xd, wd, td, bias=bd, compute_grad_input=True, compute_grad_weight=True,
+                                         chunk_rows=chunk or None, **opts)
+    torch.cuda.synchronize()
+    tol = 1e-4 if dtype == torch.float32 else 2e-2
+    if opts["reduction"] == "none":
+        assert rel_close(loss.double().cpu().numpy(), ref[1], tol)[0]
+    else:
+        assert loss.item() == pytest.approx(ref[0], rel=tol, abs=tol * 1e-3)
+    assert rel_close(gx.double().cpu().numpy(), ref[3], tol)[0], "grad_x"
+    assert rel_close(gw.double().cpu().numpy(), ref[4], tol)[0], "grad_w"
+    if bd is not None:
+        assert rel_close(gb.double().cpu().numpy(), ref[5], tol)[0], "grad_bias"
+    ignored = torch.tensor(t == -100, device="cuda")
+    assert torch.all(gx[ignored] == 0)
