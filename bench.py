@@ -427,7 +427,7 @@ def run_ours(args):
                                        check_targets=check, **opts)
         if world > 1:
             return token_sharded_flce(x, w, t, chunk_rows=chunk, accum_dtype=accum_dtype, check_targets=check,
-                                      **opts)
+                                      comm=args.comm, **opts)
         return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True, **opts,
                                                   compute_grad_weight=True, accum_dtype=accum_dtype,
                                                   check_targets=check)
@@ -557,7 +557,7 @@ def run_ours(args):
         if vocab_mode:
             loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, **opts)
         elif world > 1:
-            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk, **opts)
+            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk, comm=args.comm, **opts)
         else:
             loss = loss_fn(wp, xd, td)
             loss.backward()
@@ -610,6 +610,9 @@ def run_ours(args):
                                 "per chunk: all_gather of row statistics + async dX all-reduce (bf16)" if vocab_mode
                                 else "count all-reduce; dW all-reduce (bf16) overlapped with the last chunk's "
                                      "dW GEMM slices; loss all-reduce"),
+                "grad_w_comm": None if (world == 1 or vocab_mode) else
+                ("NCCL all-reduce per slice" if args.comm == "nccl" else
+                 "peer-memory kernel per slice (csrc/peer.cu: fp32 rank-order sum over IPC-mapped buffers)"),
                 "l2": "inputs larger than L2 (W = 1.05 GB bf16 re-streamed every chunk)",
             },
             "roofline": {
@@ -693,6 +696,8 @@ def main():
                     help="fraction of targets set to ignore_index (the headline config uses 0.1)")
     ap.add_argument("--mode", choices=["token", "vocab"], default="token",
                     help="multi-GPU shard mode: token-sharded (default) or vocab-parallel (strong)")
+    ap.add_argument("--comm", choices=["nccl", "peer"], default="nccl",
+                    help="token mode, N>1: grad_w all-reduce by NCCL or by the peer-memory kernel (csrc/peer.cu)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -122,7 +122,7 @@ int lk_cross_entropy_fwd(void* logits, int64_t ld, const int64_t* targets, int64
  * 1.0 if argmax == target else 0.0 (correct_rows) and the argmax (pred_rows); ignored rows
  * -> 0.0 / -1; either may be NULL (LK/ops/cross_entropy.py:131-163, 294-299).  class_weight
  * ([vocab] fp32 or NULL) is Liger's `weight` (LK/ops/cross_entropy.py:122-124, 220-239,
- * 278-288); with label_smoothing > 0 it returns LK_UNSUPPORTED. */
+ * 278-288), also combined with label_smoothing (the smoothing term weighted as Liger does). */
 int lk_cross_entropy_fwd_ex(void* logits, int64_t ld, const int64_t* targets, int64_t rows, int64_t vocab,
                             int dtype, int64_t ignore_index, float label_smoothing, float lse_square_scale,
                             float softcap, int reduction, int compute_grad, float* loss_rows, float* loss_sum,
@@ -291,6 +291,37 @@ int lk_flce_vp_backward2(const void* x, const void* weight_shard, const int64_t*
  * row_stats[rows][4] (max; sumexp rescaled to the global max; sums), folding ranks in rank
  * order so every rank gets bit-identical statistics. */
 int lk_flce_vp_combine_stats(const float* gathered, int64_t world, int64_t rows, float* row_stats, void* stream);
+
+/* ---- peer-memory grad_w all-reduce -------------------- */
+/* The token-sharded dW reduction over NVLink peer memory, replacing the NCCL all-reduce of
+ * distributed.py (the reference's contract: dW is additive over row shards,
+ * /root/reference/pkg/tests/test_flce.py:182-205).  Every rank allocates one symmetric buffer
+ * (a control page of LK_PEER_CTL_BYTES, then the data) and maps every peer's buffer through
+ * CUDA IPC.  lk_peer_alloc is the one entry point that allocates device memory: IPC needs a
+ * cudaMalloc base.  Buffers start zeroed (the control page must be). */
+#define LK_PEER_MAX 16
+#define LK_PEER_CTL_BYTES 4096
+#define LK_PEER_HANDLE_BYTES 64
+int lk_peer_alloc(int device, size_t data_bytes, void** base, void* ipc_handle);
+/* Maps a peer's buffer from its handle (not the caller's own: use its base directly). */
+int lk_peer_open(int device, const void* ipc_handle, void** base);
+int lk_peer_close(int device, void* peer_base);
+int lk_peer_free(int device, void* base);
+/* In-place sum over ranks of n elements (dtype) at byte offset `offset` (from each base; a
+ * multiple of the element size) of every rank's buffer.  One kernel: rank r owns the r-th
+ * 16-byte-aligned part of the range, loads it from every peer, adds in fp32 in rank order
+ * (bit-identical on every rank and every run), rounds once, and stores the sum into every
+ * peer.  Flags in the control pages order it: a rank's part is read only after that rank
+ * signalled `epoch` (its data final, stream order), and the kernel ends only after every owner
+ * signalled its stores done.  Every rank must issue the same calls in the same order with
+ * epochs 1, 2, 3, ... per buffer, on one stream per buffer.  A wait longer than timeout_ns
+ * (0 = 120 s) abandons the call and sets the buffer's error flag (lk_peer_status) instead of
+ * hanging the GPU. */
+int lk_peer_allreduce(void* const* bases, int world, int rank, int64_t offset, int64_t n, int dtype,
+                      uint64_t epoch, int64_t timeout_ns, void* stream);
+/* Synchronous read of the caller's own buffer error flag (1 = a call timed out); clear != 0
+ * resets it. */
+int lk_peer_status(int device, void* base, int clear, int* error);
 
 /* ---- RMSNorm ----------------------------------------------------------- */
 /* rowfuse/ops.py:190-241 and LK/ops/rms_norm.py (forward 58-112, backward 115-210).

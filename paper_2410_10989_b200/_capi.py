@@ -123,6 +123,13 @@ SIGNATURES: dict[str, tuple] = {
          c_void],
     ),
     "lk_flce_vp_combine_stats": (c_int, [c_void, c_i64, c_i64, c_void, c_void]),
+    "lk_peer_alloc": (c_int, [c_int, c_size, C.POINTER(C.c_void_p), c_void]),
+    "lk_peer_open": (c_int, [c_int, c_void, C.POINTER(C.c_void_p)]),
+    "lk_peer_close": (c_int, [c_int, c_void]),
+    "lk_peer_free": (c_int, [c_int, c_void]),
+    "lk_peer_allreduce": (c_int, [C.POINTER(C.c_void_p), c_int, c_int, c_i64, c_i64, c_int, C.c_uint64, c_i64,
+                                  c_void]),
+    "lk_peer_status": (c_int, [c_int, c_void, c_int, C.POINTER(c_int)]),
     "lk_rmsnorm_fwd": (
         c_int, [c_void, c_void, c_void, c_void, c_i64, c_i64, c_float, c_float, c_int, c_int, c_void]
     ),

@@ -81,15 +81,19 @@ def _comm_stream(device: torch.device) -> torch.cuda.Stream:
     return _COMM_STREAMS[key]
 
 
-def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw):
+def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw, peer=None):
     """Local FLCE whose last-chunk grad_w GEMM is split into `dw_slices` vocab-row slices;
     slice s is all-reduced on a side stream as soon as its event fires, so all but the last
     slice's all-reduce hide under the remaining dW GEMM launches.  The library records every
     event on every path (include/liger_b200.h, grad_w_slice_events), so a slice is never
-    all-reduced before it is final -- also on the SIMT path or for a rank with no rows."""
+    all-reduced before it is final -- also on the SIMT path or for a rank with no rows.
+    With `peer` (a PeerBuffer) grad_w lives in the symmetric buffer and each slice is summed by
+    the peer-memory kernel (lk_peer_allreduce) instead of NCCL."""
     events = [torch.cuda.Event() for _ in range(dw_slices)]
+    if peer is not None:
+        kw = dict(kw, grad_w_out=peer.tensor(w.shape, w.dtype))
     loss, gx, gw = local_fn(x, w, t, counts, grad_w_slice_events=events, **kw)
-    v = gw.shape[0]
+    v, h = gw.shape
     step = -(-v // dw_slices)
     rows = -(-step // 256) * 256  # same slice bounds as the library (flce.cu)
     comm = _comm_stream(gw.device)
@@ -97,10 +101,14 @@ def _allreduce_grad_w_overlapped(x, w, t, counts, group, dw_slices, local_fn, kw
         lo, hi = s * rows, min(v, (s + 1) * rows)
         comm.wait_event(ev)
         if lo < hi:
-            with torch.cuda.stream(comm):
-                dist.all_reduce(gw[lo:hi], op=dist.ReduceOp.SUM, group=group)
+            if peer is not None:
+                peer.all_reduce_(gw, lo * h, hi * h, stream=comm)
+            else:
+                with torch.cuda.stream(comm):
+                    dist.all_reduce(gw[lo:hi], op=dist.ReduceOp.SUM, group=group)
     torch.cuda.current_stream(gw.device).wait_stream(comm)
-    gw.record_stream(comm)
+    if peer is None:
+        gw.record_stream(comm)
     return loss, gx, gw
 
 
@@ -116,6 +124,7 @@ def token_sharded_flce(
     reduce_grad_weight: bool = True,
     dw_slices: int = 4,
     check_targets: bool = True,
+    comm: str = "nccl",
     **kw,
 ):
     """Returns (loss, local grad_x, all-reduced grad_w).
@@ -127,9 +136,14 @@ def token_sharded_flce(
     call enqueues every kernel and collective without a host sync, and only then (with
     `check_targets`) reads the globally all-reduced out-of-range target count, so every rank
     raises TargetOutOfRange together instead of one rank leaving the others in a collective.
+    `comm="peer"` sums grad_w with the peer-memory kernel over a symmetric buffer
+    (peer.grad_w_buffer, csrc/peer.cu) instead of NCCL; the returned grad_w is then a view of
+    that buffer, overwritten by the next call for the same weight shape.
     """
     if reduction not in ("mean", "sum", "none"):
         raise ValueError(f"reduction must be 'mean' or 'sum' or 'none'. Got: {reduction}")
+    if comm not in ("nccl", "peer"):
+        raise ValueError(f"comm must be 'nccl' or 'peer'. Got: {comm}")
     t = as_targets(target_local) if target_local.is_cuda else target_local.reshape(-1).to(torch.int64)
     count_fn = count_fn or (lambda tt: _count_cuda(tt, weight.shape[0], ignore_index))
     dw_slices = max(1, min(int(dw_slices), MAX_DW_SLICES))
@@ -148,8 +162,14 @@ def token_sharded_flce(
         wsum = (wsum * valid).sum(dtype=torch.float32).reshape(1)
         dist.all_reduce(wsum, op=dist.ReduceOp.SUM, group=group)
         kw["mean_weight_sum"] = wsum
-    if overlap:
-        loss, gx, gw = _allreduce_grad_w_overlapped(x_local, weight, t, counts, group, dw_slices, local_fn, kw)
+    peer = None
+    if comm == "peer" and reduce_grad_weight and cuda_local and x_local.is_cuda:
+        from .peer import grad_w_buffer
+
+        peer = grad_w_buffer(weight, group)
+    if overlap or peer is not None:
+        loss, gx, gw = _allreduce_grad_w_overlapped(x_local, weight, t, counts, group, dw_slices, local_fn, kw,
+                                                    peer=peer)
     else:
         loss, gx, gw = local_fn(x_local, weight, t, counts, **kw)
         if reduce_grad_weight and gw is not None:
@@ -159,6 +179,8 @@ def token_sharded_flce(
         dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
     if check_targets and cuda_local:
         raise_if_out_of_range(counts, weight.shape[0])
+        if peer is not None:
+            peer.check()
     return loss, gx, gw
 
 

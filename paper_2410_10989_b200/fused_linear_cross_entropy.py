@@ -74,6 +74,7 @@ def fused_linear_cross_entropy_forward(
     mean_weight_sum: Optional[torch.Tensor] = None,
     check_targets: bool = True,
     fp32_pieces: int = 0,
+    grad_w_out: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -93,6 +94,8 @@ def fused_linear_cross_entropy_forward(
     `check_targets=False` skips the host read of the device-side out-of-range count (the one
     host sync of the call); the caller then owns the check (token_sharded_flce does it on the
     all-reduced count after enqueueing its collectives).
+    `grad_w_out` (contiguous, weight's shape / dtype / device) receives grad_weight instead of a
+    new tensor: the token-sharded peer all-reduce passes a view of its symmetric buffer.
     """
     if not (0.0 <= label_smoothing <= 1.0):
         raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
@@ -122,7 +125,11 @@ def fused_linear_cross_entropy_forward(
     need_gw = (need_gx and weight.requires_grad) if compute_grad_weight is None else compute_grad_weight
     dev = x.device
     grad_x = torch.empty_like(x) if need_gx else None
-    grad_w = torch.empty_like(w) if need_gw else None
+    if need_gw and grad_w_out is not None:
+        if grad_w_out.shape != w.shape or grad_w_out.dtype != w.dtype or grad_w_out.device != w.device:
+            raise errors.ShapeMismatch("grad_w_out must match weight's shape, dtype and device")
+        require_contiguous("grad_w_out", grad_w_out)
+    grad_w = (grad_w_out if grad_w_out is not None else torch.empty_like(w)) if need_gw else None
     grad_b = torch.empty_like(b) if (b is not None and need_gx) else None
     loss_rows = torch.empty(bt, dtype=torch.float32, device=dev)
     loss_sum = torch.empty((), dtype=torch.float32, device=dev)

@@ -214,3 +214,36 @@ def test_benchrecord_csv_reads_with_the_reference_reader(tmp_path):
     recs = read_records(p)
     assert recs[0].op == "rmsnorm" and recs[0].median_s == 2e-5
     assert summarize(recs)[0]["fused_median_s"] == 2e-5
+
+
+def test_peer_allreduce_validates_before_touching_the_device():
+    """lk_peer_allreduce rejects bad arguments with LK_INVALID_ARGUMENT before any CUDA call
+    (so this runs without a GPU), and the constants agree with the Python mirror."""
+    from paper_2410_10989_b200 import peer
+
+    text = HEADER.read_text()
+    for name, val in (("LK_PEER_MAX", peer.MAX_PEERS), ("LK_PEER_CTL_BYTES", peer.CTL_BYTES),
+                      ("LK_PEER_HANDLE_BYTES", peer.HANDLE_BYTES)):
+        assert re.search(rf"#define {name} {val}\b", text), name
+    lib = _capi.load()
+    bases = (C.c_void_p * 2)(4096 * 16, 4096 * 32)
+    ok = dict(bases=bases, world=2, rank=0, offset=4096, n=100, dtype=_capi.LK_BF16, epoch=1, timeout=0)
+
+    def call(**over):
+        a = dict(ok, **over)
+        return lib.lk_peer_allreduce(a["bases"], a["world"], a["rank"], a["offset"], a["n"], a["dtype"], a["epoch"],
+                                     a["timeout"], None)
+
+    for bad in (dict(world=0), dict(world=peer.MAX_PEERS + 1), dict(rank=2), dict(rank=-1), dict(dtype=7),
+                dict(n=-1), dict(epoch=0), dict(offset=100), dict(offset=4097),
+                dict(bases=(C.c_void_p * 2)(4096, None))):
+        assert call(**bad) == 8, bad  # LK_INVALID_ARGUMENT
+    assert lib.lk_peer_alloc(0, 16, None, None) == 8
+    assert lib.lk_peer_status(0, None, 0, None) == 8
+
+
+def test_token_sharded_rejects_unknown_comm():
+    from paper_2410_10989_b200.distributed import token_sharded_flce
+
+    with pytest.raises(ValueError, match="comm must be"):
+        token_sharded_flce(torch.zeros(2, 8), torch.zeros(4, 8), torch.zeros(2, dtype=torch.int64), comm="mpi")

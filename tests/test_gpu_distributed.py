@@ -59,7 +59,7 @@ def _worker(rank, port, mode, kw, out):
         xb = torch.tensor(x, dtype=dtype, device=dev)
         wb = torch.tensor(w, dtype=dtype, device=dev)
         tb = torch.tensor(t, device=dev)
-        ref_kw = {k: v for k, v in kw.items() if k not in ("dw_slices", "dx_reduce_dtype")}
+        ref_kw = {k: v for k, v in kw.items() if k not in ("dw_slices", "dx_reduce_dtype", "comm")}
         if "ce_weight" in kw:  # numpy class weights: the oracle's `weight`, the library's ce_weight tensor
             ref_kw["weight"] = ref_kw.pop("ce_weight")
             kw["ce_weight"] = torch.tensor(kw["ce_weight"], dtype=torch.float32, device=dev)
@@ -112,7 +112,12 @@ _CW = np.random.default_rng(5).random(3000) + 0.2
                                 # rows (BT == 0 early return) and beyond the slice limit
                                 dict(_dtype=torch.float32), dict(_rank0_no_rows=True),
                                 dict(_rank0_no_rows=True, _dtype=torch.float32), dict(dw_slices=40),
-                                dict(reduction="none"), dict(reduction="sum", dw_slices=7)])
+                                dict(reduction="none"), dict(reduction="sum", dw_slices=7),
+                                # grad_w summed by the peer-memory kernel (csrc/peer.cu) instead of
+                                # the collective: sliced, unsliced, fp32, a rank with no rows
+                                dict(comm="peer"), dict(comm="peer", dw_slices=1),
+                                dict(comm="peer", dw_slices=7, label_smoothing=0.1),
+                                dict(comm="peer", _dtype=torch.float32), dict(comm="peer", _rank0_no_rows=True)])
 def test_token_sharded_cuda_world2(kw):
     _run("token", kw)
 
