@@ -642,8 +642,9 @@ def run_ours(args):
                     "h2d_pipeline": "each step's X/targets copied from pinned host memory on a side stream, "
                                     "double-buffered one step ahead; every step's loss copied device->host "
                                     "(pinned, on the compute stream, inside the timed region) and read on the "
-                                    "host one step later; the forward's target-range check is a host sync "
-                                    "every step (as Liger's n_non_ignore .item())"},
+                                    "host one step later; the forward's target-range check reads a count "
+                                    "staged to pinned memory before the GEMMs every step, so the host waits "
+                                    "for the count kernel only (Liger's n_non_ignore .item() waits for it too)"},
             "gpu_launches": launches * args.steps,
             "gpu_launches_per_step": launches,
             "clocks": clk.summary(),

@@ -103,12 +103,35 @@ def as_targets(target: torch.Tensor) -> torch.Tensor:
     return t.contiguous()
 
 
-def raise_if_out_of_range(stats: torch.Tensor, vocab: int) -> None:
-    # Under CUDA-graph capture the host read is not allowed: the check is skipped (the kernels
-    # never index outside the row for such targets; the device-side count stays in `stats`).
-    if not CHECK_TARGETS or torch.cuda.is_current_stream_capturing():
+def stage_target_stats(stats: torch.Tensor):
+    """Copy the device (n_valid, n_out_of_range) counts to pinned host memory right after the
+    kernel that produced them, and record an event.  The range check at the end of the call
+    (`raise_if_staged_out_of_range`) then waits for that small kernel only, not for the whole op
+    behind it, so the host goes on to launch the next op while the GEMMs run.  None when the
+    check is off or under graph capture."""
+    if not CHECK_TARGETS or not stats.is_cuda or torch.cuda.is_current_stream_capturing():
+        return None
+    host = torch.empty(2, dtype=torch.int64, pin_memory=True)  # torch's caching host allocator
+    host.copy_(stats[:2], non_blocking=True)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(stats.device))
+    return host, ev
+
+
+def count_and_stage_targets(t: torch.Tensor, vocab: int, ignore_index: int):
+    """lk_count_targets into a fresh device pair, staged for the host check (see above)."""
+    if not CHECK_TARGETS or t.numel() == 0 or torch.cuda.is_current_stream_capturing():
+        return None
+    counts = torch.empty(2, dtype=torch.int64, device=t.device)
+    check(lib().lk_count_targets(t.data_ptr(), t.numel(), vocab, ignore_index, counts.data_ptr(), stream_of(t)))
+    return stage_target_stats(counts)
+
+
+def raise_if_staged_out_of_range(staged, vocab: int) -> None:
+    if staged is None:
         return
-    if int(stats[1].item()) > 0:
-        raise errors.TargetOutOfRange(
-            f"{int(stats[1].item())} target(s) outside [0, {vocab}) that are not ignore_index"
-        )
+    host, ev = staged
+    ev.synchronize()
+    n = int(host[1])
+    if n > 0:
+        raise errors.TargetOutOfRange(f"{n} target(s) outside [0, {vocab}) that are not ignore_index")

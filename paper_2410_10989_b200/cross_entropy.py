@@ -23,7 +23,8 @@ from ._utils import (
     dtype_code,
     lib,
     ptr,
-    raise_if_out_of_range,
+    count_and_stage_targets,
+    raise_if_staged_out_of_range,
     require_cuda,
     stream_of,
     workspace,
@@ -88,6 +89,7 @@ def cross_entropy_forward(
     pred = torch.empty(bt, dtype=torch.int64, device=dev) if return_predicted_tokens else None
     L = lib()
     ws = workspace(L.lk_cross_entropy_workspace_bytes(bt), dev)
+    staged = count_and_stage_targets(t, v, int(ignore_index))  # host check waits for this count only
     check(
         L.lk_cross_entropy_fwd_ex(
             _input.data_ptr(), _input.stride(0) if bt > 0 else v, ptr(t), bt, v, dtype_code(_input),
@@ -97,8 +99,8 @@ def cross_entropy_forward(
             ws.data_ptr(), ws.numel(), stream_of(_input),
         )
     )
-    counts = ws[:16].view(torch.int64)
-    raise_if_out_of_range(counts, v)
+    counts = ws[:16].view(torch.int64)  # (n_valid, n_out_of_range) written by the kernel
+    raise_if_staged_out_of_range(staged, v)
     if reduction == "none":
         loss = loss_rows.to(_input.dtype)
         z_loss = z_rows.to(_input.dtype) if return_z_loss else None

@@ -35,7 +35,8 @@ from ._utils import (
     dtype_code,
     lib,
     ptr,
-    raise_if_out_of_range,
+    raise_if_staged_out_of_range,
+    stage_target_stats,
     stream_of,
     workspace,
 )
@@ -153,6 +154,7 @@ def token_sharded_flce(
     counts = count_fn(t)
     # (n_valid, n_out_of_range) summed over ranks: the MEAN denominator and the global range check
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+    staged = stage_target_stats(counts) if (check_targets and cuda_local) else None
     kw = dict(kw, ignore_index=ignore_index, reduction=reduction)
     cw = kw.get("ce_weight")
     if cw is not None and reduction == "mean" and local_fn is _local_flce_cuda:
@@ -178,7 +180,7 @@ def token_sharded_flce(
         loss = loss.clone()
         dist.all_reduce(loss, op=dist.ReduceOp.SUM, group=group)
     if check_targets and cuda_local:
-        raise_if_out_of_range(counts, weight.shape[0])
+        raise_if_staged_out_of_range(staged, weight.shape[0])
         if peer is not None:
             peer.check()
     return loss, gx, gw
@@ -283,6 +285,7 @@ def vocab_parallel_flce(
     t = target.reshape(-1).to(torch.int64).contiguous()
     bt, h = x.shape
     n_valid = ops.count(t, shard.total, ignore_index)
+    staged = stage_target_stats(n_valid) if (check_targets and isinstance(ops, CudaVocabOps)) else None
     if w_shard.dtype == torch.float64:
         acc_dtype = torch.float64
     elif accum_dtype is None and w_shard.dtype in (torch.bfloat16, torch.float16) and isinstance(ops, CudaVocabOps):
@@ -311,5 +314,5 @@ def vocab_parallel_flce(
             gx[lo:hi] = gxp.to(x.dtype)
     loss = loss_rows if reduction == "none" else loss_rows.sum()
     if check_targets and isinstance(ops, CudaVocabOps):
-        raise_if_out_of_range(n_valid, shard.total)
+        raise_if_staged_out_of_range(staged, shard.total)
     return loss, gx, gw_acc.to(w_shard.dtype)

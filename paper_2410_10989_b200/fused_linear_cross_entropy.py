@@ -23,7 +23,8 @@ from ._utils import (
     dtype_code,
     lib,
     ptr,
-    raise_if_out_of_range,
+    count_and_stage_targets,
+    raise_if_staged_out_of_range,
     require_contiguous,
     require_cuda,
     stream_of,
@@ -185,10 +186,12 @@ def fused_linear_cross_entropy_forward(
         raise errors.ShapeMismatch("mean_count must be a CUDA int64 tensor")
     if mean_weight_sum is not None and (mean_weight_sum.dtype != torch.float32 or not mean_weight_sum.is_cuda):
         raise errors.ShapeMismatch("mean_weight_sum must be a CUDA float32 tensor")
+    # the range check reads a count staged ahead of the GEMMs: the host waits for that count
+    # kernel only, and runs ahead to the next op while this one computes
+    staged = count_and_stage_targets(t, v, int(ignore_index)) if check_targets else None
     check(L.lk_flce_forward_backward(_capi.C.byref(args)))
     del ws
-    if check_targets:
-        raise_if_out_of_range(stats, v)
+    raise_if_staged_out_of_range(staged, v)
     if reduction == "none":
         loss = loss_rows
         z_loss = z_rows.to(x.dtype) if return_z_loss else None
