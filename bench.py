@@ -24,7 +24,8 @@ makes one checked, untimed call afterwards on the same batch.
 
 Keys beyond the base contract:
   roofline      dominant kernel = the tcgen05 GEMM (logits + backward launches); achieved =
-                algorithmic FLOP / summed CUDA-event durations of those launches in the timed
+                executed FLOP (6 * kept rows * H * V: the ignore_index rows are skipped, see
+                variants.all_rows) / summed CUDA-event durations of those launches in the timed
                 region; peak from MEASURED_PEAKS.json (sustained: launched inside a long step);
                 traffic = ncu DRAM bytes per GEMM launch for THIS config (profiles/r02_traffic.json,
                 scripts/traffic_capture.py), null when no capture exists for the config.
@@ -37,7 +38,8 @@ Keys beyond the base contract:
                 X/targets copied from pinned host memory every step (on a side stream, one
                 step ahead, double-buffered) and every step's loss copied back to pinned host
                 memory inside the timed region, read on the host one step later.
-  variants      accum_dtype=torch.float32 (fp32 dW accumulator) tokens/s and peak memory.
+  variants      accum_dtype=torch.float32 (fp32 dW accumulator) tokens/s and peak memory;
+                all_rows: skip_ignored_rows=False (every row through the GEMMs).
   --impl reference  times the reference's CPU algorithm (oracle port, f32) on the box's host
                 cores; rank 0 only.
 """
@@ -418,7 +420,7 @@ def run_ours(args):
         w = w[shard.offset:shard.offset + shard.size].contiguous()
     workload = {"cfg4": CFG4["workload"], "cfg5": CFG5_WORKLOAD}.get(args.config, WORKLOAD)
 
-    def step(accum_dtype=None, check=False):
+    def step(accum_dtype=None, check=False, skip=None):
         # device-resident loop: the out-of-range target count is computed on the device every
         # step; its host read (a sync that would leave the GPU idle while the next step is
         # launched) is done once, untimed, by the checked call after the loop
@@ -430,7 +432,7 @@ def run_ours(args):
                                       comm=args.comm, **opts)
         return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True, **opts,
                                                   compute_grad_weight=True, accum_dtype=accum_dtype,
-                                                  check_targets=check)
+                                                  check_targets=check, skip_ignored_rows=skip)
 
     def barrier():
         if world > 1:
@@ -463,13 +465,13 @@ def run_ours(args):
     ws_bytes = flce_workspace_bytes(bt, h, v, torch.bfloat16, chunk, True)
     logits_chunk_bytes = chunk * (-(-v // 64) * 64) * 2
 
-    def timed(n, accum_dtype=None):
+    def timed(n, accum_dtype=None, skip=None):
         barrier()
         torch.cuda.synchronize()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record()
         for _ in range(n):
-            step(accum_dtype)
+            step(accum_dtype, skip=skip)
         ev1.record()
         torch.cuda.synchronize()
         barrier()
@@ -494,6 +496,14 @@ def run_ours(args):
     tokens_per_step = bt if vocab_mode else global_bt
     value = tokens_per_step * args.steps / (ms / 1e3)
     flop_step = 6.0 * bt * h * v / (world if vocab_mode else 1)  # per rank
+    # ignored-row skipping (single-GPU path, fused_linear_cross_entropy._forward_kept_rows):
+    # the GEMMs run on the kept rows only, so the roofline counts the FLOPs actually executed
+    n_ignored = int((t == -100).sum().item())
+    from paper_2410_10989_b200 import fused_linear_cross_entropy as flce_mod
+
+    skipping = (world == 1 and not vocab_mode and flce_mod.SKIP_IGNORED_ROWS and n_ignored > 0
+                and n_ignored >= max(flce_mod.COMPACT_MIN_SKIPPED, bt // 64))
+    flop_exec = 6.0 * (bt - n_ignored) * h * v if skipping else flop_step
 
     # ---- variant: fp32 dW accumulator (accum_dtype=torch.float32), untimed peak + timed steps ----
     variants = None
@@ -506,6 +516,12 @@ def run_ours(args):
                                    "peak_extra_minus_outputs": pk32 - out_bytes,
                                    "note": "accum_dtype=torch.float32: grad_w accumulated across chunks in an "
                                            "fp32 workspace (V*H*4 bytes), one final rounding"}}
+        if skipping:
+            ms_full = timed(vsteps, skip=False)
+            variants["all_rows"] = {"value": tokens_per_step * vsteps / (ms_full / 1e3), "unit": "tokens/s",
+                                    "steps": vsteps, "ms_per_step": ms_full / vsteps,
+                                    "note": "skip_ignored_rows=False: the GEMMs also run on the ignore_index rows "
+                                            "(the upstream Liger / reference schedule)"}
         if world == 1 and args.config == "cfg2" and not vocab_mode and args.bt == BT:
             variants["fp32_cfg2"] = gpu_cfg2_fp32(dev)
 
@@ -584,7 +600,7 @@ def run_ours(args):
 
     peaks, peak_src = measured_peaks()
     gemm_ms = (ms4[0] + ms4[2]) / args.steps
-    achieved = flop_step / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
+    achieved = flop_exec / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak_sus = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
     traffic, traffic_step, traffic_src = (None, None, None) if vocab_mode else traffic_for(bt, h, v, args.softcap)
 
@@ -614,6 +630,8 @@ def run_ours(args):
                 ("NCCL all-reduce per slice" if args.comm == "nccl" else
                  "peer-memory kernel per slice (csrc/peer.cu: fp32 rank-order sum over IPC-mapped buffers)"),
                 "l2": "inputs larger than L2 (W = 1.05 GB bf16 re-streamed every chunk)",
+                "ignore_index_rows": ("skipped: the chunk loop runs on the kept rows (outputs of ignored rows "
+                                      "written as the full call leaves them)" if skipping else "computed"),
             },
             "roofline": {
                 "bound": "tensor", "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
@@ -621,10 +639,11 @@ def run_ours(args):
                 "kernel": "tc2::gemm2_kernel<bf16> (CTA-pair tcgen05; logits + backward launches)",
                 "traffic_unit": "DRAM bytes per GEMM launch (avg over one step's launches, ncu, this config)",
                 "traffic_per_step": traffic_step, "traffic_source": traffic_src,
-                "algorithmic_flop_per_step": flop_step,
+                "algorithmic_flop_per_step": flop_step, "executed_flop_per_step": flop_exec,
+                "ignored_rows": n_ignored, "ignored_rows_skipped": skipping,
                 "peak_source": f"{peak_src} bf16_tflops_sustained", "peak_burst": float(peaks["bf16_tflops"]),
                 "frac_of_burst": (achieved / float(peaks["bf16_tflops"])) if achieved else None,
-                "step_tflops": flop_step / (ms / args.steps / 1e3) / 1e12,
+                "step_tflops": flop_exec / (ms / args.steps / 1e3) / 1e12,
                 "stage_ms_per_step": {"logits_gemm": ms4[0] / args.steps, "finalize": ms4[1] / args.steps,
                                       "backward_gemm": ms4[2] / args.steps, "other": ms4[3] / args.steps},
             },

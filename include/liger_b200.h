@@ -292,6 +292,19 @@ int lk_flce_vp_backward2(const void* x, const void* weight_shard, const int64_t*
  * order so every rank gets bit-identical statistics. */
 int lk_flce_vp_combine_stats(const float* gathered, int64_t world, int64_t rows, float* row_stats, void* stream);
 
+/* ---- ignored-row compaction (fused_linear_cross_entropy.py) ------------------ */
+/* Rows whose target is ignore_index contribute nothing to the FLCE (loss 0, gradient row 0, no
+ * dW / db term: rowfuse/ops.py:515-523, rowfuse/flce.py:161-168), so the host wrapper runs the
+ * chunk loop on the other rows only.  lk_compact_rows writes the stable list of kept rows
+ * index[0 .. *count) (index[i] = -1 past the count) and the inverse map pos[rows] (-1 for an
+ * ignored row); *count is on the device.  lk_gather_rows copies dst[i, :] = src[index[i], :]
+ * for i < out_rows, or the fill element (elem_bytes wide, low bytes of `fill`) where
+ * index[i] < 0: with `index` the gather, with `pos` the scatter back. */
+int lk_compact_rows(const int64_t* targets, int64_t rows, int64_t ignore_index, int64_t* index, int64_t* pos,
+                    int64_t* count, void* stream);
+int lk_gather_rows(const void* src, int64_t cols, int elem_bytes, const int64_t* index, int64_t out_rows, void* dst,
+                   uint64_t fill, void* stream);
+
 /* ---- peer-memory grad_w all-reduce -------------------- */
 /* The token-sharded dW reduction over NVLink peer memory, replacing the NCCL all-reduce of
  * distributed.py (the reference's contract: dW is additive over row shards,

@@ -123,6 +123,8 @@ SIGNATURES: dict[str, tuple] = {
          c_void],
     ),
     "lk_flce_vp_combine_stats": (c_int, [c_void, c_i64, c_i64, c_void, c_void]),
+    "lk_compact_rows": (c_int, [c_void, c_i64, c_i64, c_void, c_void, c_void, c_void]),
+    "lk_gather_rows": (c_int, [c_void, c_i64, c_int, c_void, c_i64, c_void, C.c_uint64, c_void]),
     "lk_peer_alloc": (c_int, [c_int, c_size, C.POINTER(C.c_void_p), c_void]),
     "lk_peer_open": (c_int, [c_int, c_void, C.POINTER(C.c_void_p)]),
     "lk_peer_close": (c_int, [c_int, c_void]),

@@ -67,7 +67,8 @@ def _local_flce_cuda(x, w, t, mean_count, reduction="mean", **kw):
     # after every collective is enqueued, so the dW all-reduce can overlap the dW GEMMs
     loss, _, _, _, gx, gw, _ = fused_linear_cross_entropy_forward(
         x, w, t, compute_grad_input=True, compute_grad_weight=True, reduction=reduction,
-        mean_count=mean_count[:1] if reduction == "mean" else None, check_targets=False, **kw)
+        mean_count=mean_count[:1] if reduction == "mean" else None, check_targets=False,
+        skip_ignored_rows=False, **kw)  # no host read of the kept-row count: the call stays sync-free
     return loss, gx, gw
 
 

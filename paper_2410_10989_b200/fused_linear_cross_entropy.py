@@ -49,6 +49,57 @@ def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=Non
                                                 int(accum)))
 
 
+# Ignored-row skipping (lk_compact_rows / lk_gather_rows, csrc/compact.cu).  On by default; a
+# call skips rows only when at least COMPACT_MIN_SKIPPED rows (and 1/64 of the batch) are
+# ignored -- below that the GEMM tiles (256 rows per CTA pair) barely shrink.
+SKIP_IGNORED_ROWS = True
+COMPACT_MIN_SKIPPED = 128
+
+
+def _gather_rows(src: torch.Tensor, index: torch.Tensor, out_rows: int, dst: torch.Tensor, fill_bits: int = 0):
+    cols = src[0].numel() if src.dim() > 1 else 1
+    check(lib().lk_gather_rows(src.data_ptr(), cols, src.element_size(), index.data_ptr(), out_rows, dst.data_ptr(),
+                               fill_bits, stream_of(src)))
+    return dst
+
+
+def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, return_z_loss, return_token_accuracy,
+                       return_predicted_tokens, kw):
+    """The FLCE on the rows whose target is not ignore_index, outputs scattered back to all rows.
+
+    Ignored rows contribute nothing (loss 0, gradient row 0, no dW / db term:
+    rowfuse/ops.py:515-523, rowfuse/flce.py:161-168) and the MEAN denominator counts the kept
+    rows only, so the kept-row problem has the same loss, dW and db, and the same dX rows.
+    The dW sum is grouped into chunks differently (same tolerance, deterministic).  Returns
+    None (caller runs the full problem) when too few rows are ignored."""
+    bt, h = x.shape
+    dev = x.device
+    L = lib()
+    index = torch.empty(bt, dtype=torch.int64, device=dev)
+    pos = torch.empty(bt, dtype=torch.int64, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    check(L.lk_compact_rows(t.data_ptr(), bt, int(ignore_index), index.data_ptr(), pos.data_ptr(), count.data_ptr(),
+                            stream_of(t)))
+    n = int(count.item())  # the one host read: the chunk loop is sized by the kept rows
+    if n == 0 or bt - n < max(COMPACT_MIN_SKIPPED, bt // 64):
+        return None
+    xk = _gather_rows(x, index, n, torch.empty(n, h, dtype=x.dtype, device=dev))
+    tk = _gather_rows(t, index, n, torch.empty(n, dtype=torch.int64, device=dev))
+    loss, z_loss, acc, pred, gxk, gw, gb = fused_linear_cross_entropy_forward(
+        xk, w, tk, compute_grad_input=need_gx, compute_grad_weight=need_gw, skip_ignored_rows=False, **kw)
+    del xk, tk
+    gx = _gather_rows(gxk, pos, bt, torch.empty_like(x)) if gxk is not None else None
+    if reduction == "none":  # per-row outputs back to every row (ignored: 0)
+        loss = _gather_rows(loss, pos, bt, torch.empty(bt, dtype=loss.dtype, device=dev))
+        if z_loss is not None:
+            z_loss = _gather_rows(z_loss, pos, bt, torch.empty(bt, dtype=z_loss.dtype, device=dev))
+        if acc is not None:
+            acc = _gather_rows(acc, pos, bt, torch.empty(bt, dtype=acc.dtype, device=dev))
+    if pred is not None:  # ignored rows predict -1 (LK/ops/cross_entropy.py:294-299)
+        pred = _gather_rows(pred, pos, bt, torch.empty(bt, dtype=torch.int64, device=dev), (1 << 64) - 1)
+    return loss, z_loss, acc, pred, gx, gw, gb
+
+
 @device_guard
 def fused_linear_cross_entropy_forward(
     _input: torch.Tensor,
@@ -76,6 +127,7 @@ def fused_linear_cross_entropy_forward(
     check_targets: bool = True,
     fp32_pieces: int = 0,
     grad_w_out: Optional[torch.Tensor] = None,
+    skip_ignored_rows: Optional[bool] = None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -97,6 +149,10 @@ def fused_linear_cross_entropy_forward(
     all-reduced count after enqueueing its collectives).
     `grad_w_out` (contiguous, weight's shape / dtype / device) receives grad_weight instead of a
     new tensor: the token-sharded peer all-reduce passes a view of its symmetric buffer.
+    `skip_ignored_rows` (default SKIP_IGNORED_ROWS) runs the chunk loop on the rows whose
+    target is not ignore_index only (`_forward_kept_rows`); the outputs are those of the full
+    call (ignored rows: loss 0, gradient 0, predicted token -1).  It costs one host read of the
+    kept-row count, so the token-sharded (sync-free) path turns it off.
     """
     if not (0.0 <= label_smoothing <= 1.0):
         raise ValueError(f"label_smoothing must be between 0.0 and 1.0. Got: {label_smoothing}")
@@ -125,6 +181,20 @@ def fused_linear_cross_entropy_forward(
     need_gx = _input.requires_grad if compute_grad_input is None else compute_grad_input
     need_gw = (need_gx and weight.requires_grad) if compute_grad_weight is None else compute_grad_weight
     dev = x.device
+    if (SKIP_IGNORED_ROWS if skip_ignored_rows is None else skip_ignored_rows) and bt >= COMPACT_MIN_SKIPPED \
+            and not torch.cuda.is_current_stream_capturing():
+        kept = _forward_kept_rows(
+            x, w, t, ignore_index, need_gx, need_gw, reduction, return_z_loss, return_token_accuracy,
+            return_predicted_tokens,
+            dict(ce_weight=ce_weight, bias=b, ignore_index=ignore_index, lse_square_scale=lse_square_scale,
+                 label_smoothing=label_smoothing, reduction=reduction, softcap=softcap, return_z_loss=return_z_loss,
+                 accum_dtype=accum_dtype, use_token_scaling=use_token_scaling,
+                 return_token_accuracy=return_token_accuracy, return_predicted_tokens=return_predicted_tokens,
+                 chunk_rows=chunk_rows, force_simt=force_simt, mean_count=mean_count,
+                 grad_w_slice_events=grad_w_slice_events, mean_weight_sum=mean_weight_sum,
+                 check_targets=check_targets, fp32_pieces=fp32_pieces, grad_w_out=grad_w_out))
+        if kept is not None:
+            return kept
     grad_x = torch.empty_like(x) if need_gx else None
     if need_gw and grad_w_out is not None:
         if grad_w_out.shape != w.shape or grad_w_out.dtype != w.dtype or grad_w_out.device != w.device:

@@ -247,3 +247,13 @@ def test_token_sharded_rejects_unknown_comm():
 
     with pytest.raises(ValueError, match="comm must be"):
         token_sharded_flce(torch.zeros(2, 8), torch.zeros(4, 8), torch.zeros(2, dtype=torch.int64), comm="mpi")
+
+
+def test_compaction_entry_points_validate_arguments():
+    lib = _capi.load()
+    assert lib.lk_compact_rows(None, -1, -100, None, None, None, None) == 8
+    assert lib.lk_compact_rows(None, 10, -100, None, None, None, None) == 8
+    assert lib.lk_gather_rows(None, 4, 3, None, 4, None, 0, None) == 8  # element width 3
+    assert lib.lk_gather_rows(None, -1, 2, None, 4, None, 0, None) == 8
+    assert lib.lk_gather_rows(None, 0, 2, None, 4, None, 0, None) == 0  # nothing to copy
+    assert lib.lk_gather_rows(None, 4, 2, None, 4, None, 0, None) == 8

@@ -485,9 +485,14 @@ def test_fp16_tcgen05_path_vs_oracle(kw):
     assert ok, err
 
 
-def test_flce_in_cuda_graph():
+def test_flce_in_cuda_graph(monkeypatch):
     """No host syncs on the FLCE path: forward + backward capture into a CUDA graph and replay
-    to the same bits as eager (counts and the MEAN scale stay on the device)."""
+    to the same bits as eager (counts and the MEAN scale stay on the device).  Ignored-row
+    skipping needs a host read of the kept-row count, so it is off under capture; the eager
+    reference here runs with it off too (with it on, eager matches to tolerance below)."""
+    import paper_2410_10989_b200.fused_linear_cross_entropy as flce_mod
+
+    monkeypatch.setattr(flce_mod, "SKIP_IGNORED_ROWS", False)
     bt, h, v = 1024, 1024, 16384
     g = torch.Generator(device="cuda").manual_seed(5)
     x = ((torch.rand(bt, h, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
@@ -515,6 +520,11 @@ def test_flce_in_cuda_graph():
     graph.replay()
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(eager, out))
+    monkeypatch.setattr(flce_mod, "SKIP_IGNORED_ROWS", True)
+    skipped = step()  # 147 of 1024 rows ignored: the kept-row path
+    assert abs(skipped[0].item() - eager[0].item()) <= 1e-3 * abs(eager[0].item())
+    assert torch.equal(skipped[1][t == -100], torch.zeros_like(skipped[1][t == -100]))
+    assert close(skipped[1], eager[1], 1e-2) and close(skipped[2], eager[2], 2e-2)
 
 
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs two GPUs")
