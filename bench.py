@@ -282,14 +282,16 @@ def run_reference(args):
 
 
 # -------------------------------------------------------------------- ours
-def traffic_for(bt, h, v, softcap):
-    """ncu DRAM bytes per GEMM launch for this rank's local FLCE shape, captured by
-    scripts/traffic_capture.py into profiles/r02_traffic.json; None when not captured."""
+def traffic_for(bt, h, v, softcap, skipped=False):
+    """ncu DRAM bytes per GEMM launch for this rank's local FLCE shape (and row schedule: the
+    kept-row path or all rows), captured by scripts/traffic_capture.py into
+    profiles/r02_traffic.json; None when not captured."""
     prof = ROOT / "profiles" / "r02_traffic.json"
     if not prof.exists():
         return None, None, None
     try:
-        d = json.loads(prof.read_text()).get(f"bt{bt}_h{h}_v{v}_cap{float(softcap or 0.0):g}")
+        d = json.loads(prof.read_text()).get(f"bt{bt}_h{h}_v{v}_cap{float(softcap or 0.0):g}"
+                                             + ("_kept" if skipped else ""))
     except Exception:
         return None, None, None
     if not d or "error" in d:
@@ -415,6 +417,8 @@ def run_ours(args):
     x, t = xg[lo:hi].contiguous(), tg[lo:hi].contiguous()
     del xg, tg
     chunk = args.chunk_rows or flce_plan(bt, h, v)[0]
+    # one GPU: the library plans its own chunks (on the kept rows when ignored rows are skipped)
+    call_chunk = args.chunk_rows or None
     if vocab_mode:
         shard = vocab_shard(v, rank, world)
         w = w[shard.offset:shard.offset + shard.size].contiguous()
@@ -430,7 +434,7 @@ def run_ours(args):
         if world > 1:
             return token_sharded_flce(x, w, t, chunk_rows=chunk, accum_dtype=accum_dtype, check_targets=check,
                                       comm=args.comm, **opts)
-        return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=chunk, compute_grad_input=True, **opts,
+        return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=call_chunk, compute_grad_input=True, **opts,
                                                   compute_grad_weight=True, accum_dtype=accum_dtype,
                                                   check_targets=check, skip_ignored_rows=skip)
 
@@ -504,6 +508,9 @@ def run_ours(args):
     skipping = (world == 1 and not vocab_mode and flce_mod.SKIP_IGNORED_ROWS and n_ignored > 0
                 and n_ignored >= max(flce_mod.COMPACT_MIN_SKIPPED, bt // 64))
     flop_exec = 6.0 * (bt - n_ignored) * h * v if skipping else flop_step
+    if skipping and not args.chunk_rows:
+        chunk = flce_plan(bt - n_ignored, h, v)[0]  # the plan the kept-row call runs
+    n_chunks = -(-(bt - n_ignored if skipping else bt) // chunk)
 
     # ---- variant: fp32 dW accumulator (accum_dtype=torch.float32), untimed peak + timed steps ----
     variants = None
@@ -529,7 +536,7 @@ def run_ours(args):
     xh = x.cpu().pin_memory()
     th = t.cpu().pin_memory()
     wp = torch.nn.Parameter(w.clone())
-    loss_fn = lk.LigerFusedLinearCrossEntropyLoss(chunk_rows=chunk, **opts)
+    loss_fn = lk.LigerFusedLinearCrossEntropyLoss(chunk_rows=call_chunk, **opts)
 
     # Inputs of step i+1 are copied host->device on a side stream while step i computes
     # (double-buffered), as a training input pipeline does; every step still moves its own
@@ -602,7 +609,7 @@ def run_ours(args):
     gemm_ms = (ms4[0] + ms4[2]) / args.steps
     achieved = flop_exec / (gemm_ms / 1e3) / 1e12 if gemm_ms > 0 else None
     peak_sus = float(peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"]))
-    traffic, traffic_step, traffic_src = (None, None, None) if vocab_mode else traffic_for(bt, h, v, args.softcap)
+    traffic, traffic_step, traffic_src = (None, None, None) if vocab_mode else traffic_for(bt, h, v, args.softcap, skipping)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -619,7 +626,7 @@ def run_ours(args):
             "config": {
                 "workload": workload, "ignore_frac": args.ignore_frac, "bt_per_gpu": bt, "hidden": h, "vocab": v, "chunk_rows": chunk,
                 "softcap": args.softcap, "label_smoothing": args.label_smoothing,
-                "num_chunks": -(-bt // chunk), "global_tokens": tokens_per_step,
+                "num_chunks": n_chunks, "global_tokens": tokens_per_step,
                 "parallelism": (f"vocab-parallel vp{world}" if vocab_mode else
                                 (f"token-sharded dp{world}" if world > 1 else "single GPU")),
                 "collectives": (None if world == 1 else

@@ -93,12 +93,15 @@ int64_t lk_launch_count(void);
  *                              1 = separate cast kernel after the loop
  *   LK_PATH_CE_IMPL            0 = TMA-ring CE, 1 = one CTA per row
  *   LK_PATH_NORM_IMPL          0 = CTA-per-row RMSNorm, 1 = warp per row, 2 = generic, 3 = TMA ring
+ *   LK_PATH_DW_ACCUM16         0 = 16-bit grad_w accumulation by TMA reduce-add in L2,
+ *                              1 = read-add-round in the epilogue registers
  * Returns the previous value, or -1 for an unknown knob / value. */
 #define LK_PATH_CTA_GROUP 0
 #define LK_PATH_FLCE_FINALIZE 1
 #define LK_PATH_FLCE_SEPARATE_CAST 2
 #define LK_PATH_CE_IMPL 3
 #define LK_PATH_NORM_IMPL 4
+#define LK_PATH_DW_ACCUM16 5
 int lk_test_select_path(int knob, int value);
 
 /* ---- cross entropy (standalone) ---------------------------------------- */

@@ -208,7 +208,7 @@ def check(rc: int) -> None:
 
 
 # Test-only path knobs (include/liger_b200.h lk_test_select_path): 0 = the product path.
-PATH_CTA_GROUP, PATH_FLCE_FINALIZE, PATH_FLCE_SEPARATE_CAST, PATH_CE_IMPL, PATH_NORM_IMPL = range(5)
+PATH_CTA_GROUP, PATH_FLCE_FINALIZE, PATH_FLCE_SEPARATE_CAST, PATH_CE_IMPL, PATH_NORM_IMPL, PATH_DW_ACCUM16 = range(6)
 
 
 class select_path:

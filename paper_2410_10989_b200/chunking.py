@@ -4,7 +4,7 @@
 PAPER.md:272): chunk_rows = 2^ceil(log2(ceil(BT / ceil(V / H)))), validated the
 same way (power of two, <= next_pow2(BT), consistent chunk count).  The B200
 library uses a larger default (`b200_plan`) because
-every chunk pays one fp32 read-modify-write of dW; any plan can be passed
+every chunk is one more pass of the dW GEMM over all of grad_w; any plan can be passed
 explicitly, which is the reference's sanctioned override (ChunkPlan.with_chunk_rows,
 rowfuse/flce.py:58-66; "plan_chunks is advisory", SPEC.md:342).
 """
@@ -53,15 +53,36 @@ def plan_chunks(total_rows: int, vocab_size: int, hidden_size: int) -> ChunkPlan
     return ChunkPlan.with_chunk_rows(total_rows, next_pow2(raw))
 
 
-def b200_plan(total_rows: int, vocab_size: int, hidden_size: int, elem_bytes: int = 2) -> ChunkPlan:
-    """Host restatement of the library's default (flce.cu b200_chunk_rows): at least
-    min(next_pow2(BT), 2048) rows -- 4096 when BT > 16384 (more than 8 chunks of 2048) --
-    at most a 1 GiB chunk buffer."""
+@dataclass(frozen=True)
+class B200Plan:
+    """The library's chunk plan: chunk_rows need not be a power of two (whole 256-row tiles,
+    or the whole batch), num_chunks = ceil(total_rows / chunk_rows)."""
+
+    chunk_rows: int
+    num_chunks: int
+    total_rows: int
+
+    def __post_init__(self) -> None:
+        if self.total_rows < 1 or self.chunk_rows < 1 or self.chunk_rows > self.total_rows:
+            raise ValueError(f"bad plan: {self.chunk_rows} rows per chunk for {self.total_rows} rows")
+        if self.num_chunks != -(-self.total_rows // self.chunk_rows):
+            raise ValueError(f"num_chunks {self.num_chunks} inconsistent with {self.chunk_rows} / {self.total_rows}")
+
+
+def b200_plan(total_rows: int, vocab_size: int, hidden_size: int, elem_bytes: int = 2) -> B200Plan:
+    """Host restatement of the library's default (flce.cu b200_chunk_rows): the fewest chunks
+    of at most 3072 rows (4096 when BT > 16384) and a 1 GiB logits buffer, split evenly in
+    256-row tiles; never below the reference's rule (capped by the buffer)."""
     ref = plan_chunks(total_rows, vocab_size, hidden_size).chunk_rows
-    c_min = 4096 if total_rows > 2048 * 8 else 2048
-    c = max(ref, min(next_pow2(total_rows), c_min))
     ldz = -(-vocab_size // 64) * 64
-    while c > 128 and c * ldz * elem_bytes > (1 << 30):
-        c >>= 1
-    c = min(c, next_pow2(total_rows))
-    return ChunkPlan.with_chunk_rows(total_rows, c)
+    cap_rows = max(256, (1 << 30) // (ldz * elem_bytes) // 256 * 256)
+    c_max = min(4096 if total_rows > 2048 * 8 else 3072, cap_rows)
+    if total_rows <= c_max:
+        c = total_rows
+    else:
+        nch = -(-total_rows // c_max)
+        tiles = -(-total_rows // 256)
+        c = -(-tiles // nch) * 256
+    c = max(c, min(ref, cap_rows))
+    c = max(1, min(c, max(total_rows, 1)))
+    return B200Plan(chunk_rows=c, num_chunks=-(-total_rows // c), total_rows=total_rows)

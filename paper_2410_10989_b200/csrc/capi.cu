@@ -26,10 +26,11 @@ int check_launch(const char* what) {
 }
 
 // ------------------------------------------------ test-only path knobs ----
-static std::atomic<int> g_knobs[5];
-static const int kKnobMax[5] = {1, 1, 1, 1, 3};
+static constexpr int kKnobs = 6;
+static std::atomic<int> g_knobs[kKnobs];
+static const int kKnobMax[kKnobs] = {1, 1, 1, 1, 3, 1};
 
-int path_knob(int knob) { return (knob >= 0 && knob < 5) ? g_knobs[knob].load(std::memory_order_relaxed) : 0; }
+int path_knob(int knob) { return (knob >= 0 && knob < kKnobs) ? g_knobs[knob].load(std::memory_order_relaxed) : 0; }
 
 // ---------------------------------------------------------- profiling ----
 struct ProfRec {
@@ -121,6 +122,6 @@ extern "C" int lk_has_tcgen05(void) {
 }
 
 extern "C" int lk_test_select_path(int knob, int value) {
-  if (knob < 0 || knob >= 5 || value < 0 || value > lk::kKnobMax[knob]) return -1;
+  if (knob < 0 || knob >= lk::kKnobs || value < 0 || value > lk::kKnobMax[knob]) return -1;
   return lk::g_knobs[knob].exchange(value);
 }

@@ -162,7 +162,10 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     if (rc) return rc;
     rc = encode_operand(&maps[2 * p + 1], b[p], dtype, b_rows_in_box, &P.b_mode);
     if (rc) return rc;
-    P.tma_out = register_epilogue ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
+    // LK_PATH_DW_ACCUM16 = 1: the 16-bit grad_w accumulation (later chunks) reads, adds and rounds
+    // in the epilogue registers instead of a TMA reduce-add in L2
+    const bool reg16 = P.epi.kind == EPI_ACCUM && !P.epi.acc && P.epi.beta && path_knob(LK_PATH_DW_ACCUM16) == 1;
+    P.tma_out = (register_epilogue || reg16) ? 0 : encode_out(&maps[4 + p], P.epi, dtype);
     // segmented accumulation needs the fp32 TMA store / reduce-add epilogue
     if (P.seg_kb > 0 && (!P.tma_out || P.epi.kind != EPI_F32 || P.seg_kb >= P.k_blocks)) P.seg_kb = 0;
     args.prob[p] = P;
@@ -232,13 +235,26 @@ static int64_t ld_logits(int64_t vocab) { return (vocab + 63) / 64 * 64; }
 // BT = 65536 (cfg5 at N = 1) and +0.8% at BT = 8192, for which the smaller buffer is kept
 // (profiles/r02/chunk_sweep.log).  The chunk buffer is capped at 1 GiB.
 static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dtype) {
-  int64_t ratio = (vocab + hidden - 1) / hidden;
-  int64_t c_ref = next_pow2((bt + ratio - 1) / ratio);
-  const int64_t c_min = bt > 2048 * LK_ACCUM_AUTO_MAX_CHUNKS ? 4096 : 2048;
-  int64_t c = std::max<int64_t>(c_ref, std::min<int64_t>(next_pow2(bt), c_min));
+  // Fewest chunks under a row cap, split evenly in 256-row CTA-pair tiles.  Every chunk is one
+  // pass of the dW GEMM over all of grad_w, and a pass costs ~0.35 ms at the Llama-3 head
+  // beyond its FLOPs (measured: 4 -> 3 chunks of 8192 rows is +2.4%, 3 -> 2 is flat;
+  // profiles/r02/chunk_count_probe.log), while the logits buffer grows with the chunk.
+  // Cap: 3072 rows (12 tiles) up to 16384 rows, 4096 beyond, and a logits buffer <= 1 GiB.
+  const int64_t ratio = (vocab + hidden - 1) / hidden;
+  const int64_t c_ref = next_pow2((bt + ratio - 1) / ratio);  // the reference's rule
   const int64_t cap_bytes = (int64_t)1 << 30;
-  while (c > 128 && c * ld_logits(vocab) * elt_size(dtype) > cap_bytes) c >>= 1;
-  return std::max<int64_t>(1, c);
+  const int64_t row_bytes = ld_logits(vocab) * elt_size(dtype);
+  const int64_t cap_rows = std::max<int64_t>(256, cap_bytes / row_bytes / 256 * 256);
+  const int64_t c_max = std::min<int64_t>(bt > 2048 * LK_ACCUM_AUTO_MAX_CHUNKS ? 4096 : 3072, cap_rows);
+  int64_t c;
+  if (bt <= c_max) {
+    c = bt;
+  } else {
+    const int64_t nch = (bt + c_max - 1) / c_max, tiles = (bt + 255) / 256;
+    c = (tiles + nch - 1) / nch * 256;
+  }
+  c = std::max<int64_t>(c, std::min<int64_t>(c_ref, cap_rows));
+  return std::max<int64_t>(1, std::min<int64_t>(c, std::max<int64_t>(bt, 1)));
 }
 
 struct FlceLayout {

@@ -362,15 +362,37 @@ __device__ __forceinline__ void epi_store(const EpiArgs& e, int64_t grow, int64_
 template <typename T>
 __device__ __forceinline__ void epi_accum(const EpiArgs& e, int64_t grow, int64_t n0, uint32_t taddr) {
   const bool row_ok = grow < e.M;
-  if (!e.acc) {  // weight-dtype accumulation directly in `out` (register fallback of the TMA reduce-add)
+  if (!e.acc) {  // weight-dtype accumulation directly in `out`: read, add in fp32, round once
     T* orow = static_cast<T*>(e.out) + grow * e.ldo;
+    const bool vec16 = (e.ldo % 8) == 0 && (reinterpret_cast<uintptr_t>(e.out) % 16) == 0;
+    uint4 nxt[4];  // the next 32 columns of this row, loaded while TMEM drains the current ones
+    auto fetch = [&](int c, uint4 (&dst)[4]) {
+      const int64_t col0 = n0 + c * 32;
+      if (row_ok && e.beta && vec16 && col0 + 32 <= e.N) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = reinterpret_cast<const uint4*>(orow + col0)[q];
+      }
+    };
+    fetch(0, nxt);
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
+      uint4 cur[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
       uint32_t r[32];
       tmem_ld32(taddr + c * 32, r);
+      if (c + 1 < BN / 32) fetch(c + 1, nxt);
       tmem_wait_ld();
       if (!row_ok) continue;
       const int64_t col0 = n0 + c * 32;
+      if (vec16 && col0 + 32 <= e.N) {
+        const T* old = reinterpret_cast<const T*>(cur);
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (e.beta ? to_f<T>(old[j]) : 0.f) + e.alpha * __uint_as_float(r[j]);
+        store32<T>(orow + col0, v);
+        continue;
+      }
       for (int j = 0; j < 32 && col0 + j < e.N; ++j) {
         const float a = e.beta ? to_f<T>(orow[col0 + j]) : 0.f;
         orow[col0 + j] = from_f<T>(a + e.alpha * __uint_as_float(r[j]));

@@ -49,13 +49,13 @@ def test_plan_and_workspace_queries():
     lib = _capi.load()
     c, n = C.c_int64(), C.c_int64()
     assert lib.lk_flce_plan(8192, 4096, 128256, 1, C.byref(c), C.byref(n)) == 0
-    assert (c.value, n.value) == (2048, 4)
+    assert (c.value, n.value) == (2816, 3)
     assert lib.lk_flce_plan(1024, 512, 4096, 0, C.byref(c), C.byref(n)) == 0
     assert (c.value, n.value) == (1024, 1)
     assert lib.lk_flce_plan(0, 4096, 128256, 1, C.byref(c), C.byref(n)) == 3  # SIZE_MISMATCH
-    chunk = 2048 * 128256 * 2
+    chunk = 2816 * 128256 * 2
     dw_acc = 128256 * 4096 * 4
-    # default (LK_ACCUM_AUTO, 4 chunks): grad_w accumulates in bf16 -> workspace ~ one logits chunk
+    # default (LK_ACCUM_AUTO, 3 chunks): grad_w accumulates in bf16 -> workspace ~ one logits chunk
     ws = lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 0, 1)
     assert chunk < ws < chunk + 64 * 2**20
     assert lib.lk_flce_workspace_bytes_ex(8192, 4096, 128256, 1, 0, 1, _capi.LK_ACCUM_AUTO) == ws
@@ -64,7 +64,7 @@ def test_plan_and_workspace_queries():
     assert chunk + dw_acc < ws32 < chunk + dw_acc + 64 * 2**20
     # more than 8 chunks: auto falls back to the fp32 accumulator
     assert lib.lk_flce_workspace_bytes(8192, 4096, 128256, 1, 512, 1) > dw_acc
-    assert lk.flce_plan(8192, 4096, 128256) == (2048, 4)
+    assert lk.flce_plan(8192, 4096, 128256) == (2816, 3)
     # the legacy size queries cover the exact-call query for the default options, fp32 included
     # (fp32 runs on split operands with 3 pieces by default: 6 terms along K)
     for dt, (bt, h, v) in ((0, (1024, 512, 4096)), (0, (300, 264, 5003)), (1, (8192, 4096, 128256))):
@@ -72,7 +72,7 @@ def test_plan_and_workspace_queries():
         exact = lib.lk_flce_workspace_bytes_for(C.byref(a))
         assert lib.lk_flce_workspace_bytes(bt, h, v, dt, 0, 1) >= exact
         assert lib.lk_flce_workspace_bytes_ex(bt, h, v, dt, 0, 1, _capi.LK_ACCUM_AUTO) >= exact
-    for bt in (16384, 65536, 32768 + 5):  # the host restatement agrees with the library
+    for bt in (1, 3000, 7373, 8192, 16384, 65536, 32768 + 5):  # the host restatement agrees with the library
         for h, v in ((4096, 128256), (3584, 256000), (512, 4096)):
             p = b200_plan(bt, v, h)
             assert lk.flce_plan(bt, h, v) == (p.chunk_rows, p.num_chunks), (bt, h, v)

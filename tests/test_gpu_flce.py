@@ -607,3 +607,16 @@ def test_flce_random_configs_vs_oracle(case):
         assert rel_close(gb.double().cpu().numpy(), ref[5], tol)[0], "grad_bias"
     ignored = torch.tensor(t == -100, device="cuda")
     assert torch.all(gx[ignored] == 0)
+
+
+@pytest.mark.parametrize("reg", [0, 1])
+def test_weight_dtype_accumulation_paths_vs_oracle(reg, path_knob):
+    """16-bit grad_w accumulated across 4 chunks: TMA reduce-add in L2 (default) or the
+    register read-add-round epilogue (LK_PATH_DW_ACCUM16 = 1), both against the f64 oracle."""
+    path_knob(_capi.PATH_DW_ACCUM16, reg)
+    xb, wb, tb, x, w, t = bf16_problem(1000, 256, 3000, seed=41)
+    loss, _, gx, gw, _ = flce(xb, wb, tb, chunk_rows=256, accum_dtype=torch.bfloat16)
+    rl, _, _, rgx, rgw, _ = liger_ref.flce(x, w, t)
+    assert rel_close(loss.item(), rl, 2e-2)[0]
+    assert rel_close(gx.double().cpu().numpy(), rgx, 2e-2)[0]
+    assert rel_close(gw.double().cpu().numpy(), rgw, 2e-2)[0]

@@ -217,12 +217,19 @@ def test_chunk_plan_validation():
         ChunkPlan(chunk_rows=8, num_chunks=1, total_rows=3, scale_ratio=1.0)
     with pytest.raises(ValueError):
         ChunkPlan(chunk_rows=2, num_chunks=1, total_rows=3, scale_ratio=1.0)
-    p = b200_plan(8192, 128256, 4096)
-    assert p.chunk_rows == 2048 and p.num_chunks == 4
+    p = b200_plan(8192, 128256, 4096)  # cfg2: 3 chunks of 11 / 11 / 10 CTA-pair tiles
+    assert p.chunk_rows == 2816 and p.num_chunks == 3
+    assert b200_plan(7373, 128256, 4096).chunk_rows == 2560  # cfg2's kept rows: 10 / 10 / 9 tiles
     assert b200_plan(1024, 4096, 512).num_chunks == 1
-    assert b200_plan(16384, 128256, 4096).chunk_rows == 2048  # 8 chunks: weight-dtype dW accumulation
+    assert b200_plan(3000, 128256, 4096).num_chunks == 1  # <= 3072 rows: one chunk
+    assert (b200_plan(16384, 128256, 4096).chunk_rows, b200_plan(16384, 128256, 4096).num_chunks) == (2816, 6)
     assert b200_plan(65536, 128256, 4096).chunk_rows == 4096  # cfg5 at N = 1: 16 chunks
-    assert b200_plan(65536, 256000, 3584).chunk_rows == 2048  # 1 GiB buffer cap at V = 256000
+    assert b200_plan(8192, 256000, 3584).chunk_rows == 2048  # cfg4: the 1 GiB buffer caps at 2048 rows
+    assert b200_plan(65536, 256000, 3584).chunk_rows == 2048
+    assert b200_plan(8192, 128256, 4096, elem_bytes=4).chunk_rows == 2048  # fp32 logits: 1 GiB cap
+    for bt in (1, 255, 3073, 9000, 20000, 100000):
+        q = b200_plan(bt, 128256, 4096)
+        assert q.num_chunks == -(-bt // q.chunk_rows) and (q.chunk_rows % 256 == 0 or q.chunk_rows == bt)
 
 
 def test_flce_properties_f64():
