@@ -269,9 +269,10 @@ def fused_linear_cross_entropy_forward(
     else:
         loss = loss_sum
         z_loss = z_sum.to(x.dtype) if return_z_loss else None
-        # mean over non-ignored tokens (LK/ops/fused_linear_cross_entropy.py:234-236)
-        denom = (mean_count[:1] if mean_count is not None else stats[:1]).clamp(min=1)
-        acc = correct.sum() / denom[0] if return_token_accuracy else None
+        acc = None
+        if return_token_accuracy:  # mean over non-ignored tokens (LK/ops/fused_linear_cross_entropy.py:234-236)
+            denom = (mean_count[:1] if mean_count is not None else stats[:1]).clamp(min=1)
+            acc = correct.sum() / denom[0]
     return loss, z_loss, acc, pred, grad_x, grad_w, grad_b
 
 

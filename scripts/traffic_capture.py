@@ -61,13 +61,14 @@ def inner(bt, h, v, softcap, smoothing, skip):
     torch.cuda.profiler.stop()
 
 
-def capture(shape, outdir):
+def capture(shape, outdir, parse_only=False):
     bt, h, v, cap, ls, skip = shape
     log = outdir / f"traffic_{key(bt, h, v, cap, skip)}.csv"
     cmd = ["ncu", "--metrics", METRICS, "--clock-control", "none", "--profile-from-start", "off", "--csv",
            "--log-file", str(log), sys.executable, __file__, "--inner", str(bt), str(h), str(v), str(cap), str(ls),
            str(skip)]
-    subprocess.run(cmd, cwd=ROOT, check=True)
+    if not parse_only:
+        subprocess.run(cmd, cwd=ROOT, check=True)
     rows = list(csv.reader(io.StringIO(log.read_text())))
     hdr_i = next(i for i, r in enumerate(rows) if "Metric Name" in r)
     hdr = rows[hdr_i]
@@ -101,6 +102,7 @@ def main():
     ap.add_argument("--inner", nargs=6, default=None)
     ap.add_argument("--out", default=str(ROOT / "profiles" / "r02_traffic.json"))
     ap.add_argument("--logdir", default=str(ROOT / "gpurun_out"))
+    ap.add_argument("--parse-only", action="store_true", help="rebuild --out from the CSVs already in --logdir")
     a = ap.parse_args()
     if a.inner:
         bt, h, v = (int(s) for s in a.inner[:3])
@@ -112,7 +114,7 @@ def main():
     for shape in SHAPES:
         k = key(*shape[:4], shape[5])
         try:
-            res[k] = capture(shape, outdir)
+            res[k] = capture(shape, outdir, a.parse_only)
         except Exception as e:  # keep the other shapes
             res[k] = {"error": repr(e)[:300]}
         print(k, json.dumps(res[k])[:300], flush=True)
