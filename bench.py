@@ -510,6 +510,9 @@ def run_ours(args):
     flop_exec = 6.0 * (bt - n_ignored) * h * v if skipping else flop_step
     if skipping and not args.chunk_rows:
         chunk = flce_plan(bt - n_ignored, h, v)[0]  # the plan the kept-row call runs
+    if skipping:
+        ws_bytes = flce_workspace_bytes(bt - n_ignored, h, v, torch.bfloat16, chunk, True)
+        logits_chunk_bytes = chunk * (-(-v // 64) * 64) * 2
     n_chunks = -(-(bt - n_ignored if skipping else bt) // chunk)
 
     # ---- variant: fp32 dW accumulator (accum_dtype=torch.float32), untimed peak + timed steps ----
