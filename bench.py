@@ -430,10 +430,10 @@ def run_ours(args):
         # launched) is done once, untimed, by the checked call after the loop
         if vocab_mode:
             return vocab_parallel_flce(x, w, t, shard, chunk_rows=chunk, accum_dtype=accum_dtype,
-                                       check_targets=check, **opts)
+                                       check_targets=check, skip_ignored_rows=skip, **opts)
         if world > 1:
-            return token_sharded_flce(x, w, t, chunk_rows=chunk, accum_dtype=accum_dtype, check_targets=check,
-                                      comm=args.comm, **opts)
+            return token_sharded_flce(x, w, t, chunk_rows=call_chunk, accum_dtype=accum_dtype,
+                                      check_targets=check, comm=args.comm, skip_ignored_rows=skip, **opts)
         return fused_linear_cross_entropy_forward(x, w, t, chunk_rows=call_chunk, compute_grad_input=True, **opts,
                                                   compute_grad_weight=True, accum_dtype=accum_dtype,
                                                   check_targets=check, skip_ignored_rows=skip)
@@ -505,10 +505,10 @@ def run_ours(args):
     n_ignored = int((t == -100).sum().item())
     from paper_2410_10989_b200 import fused_linear_cross_entropy as flce_mod
 
-    skipping = (world == 1 and not vocab_mode and flce_mod.SKIP_IGNORED_ROWS and n_ignored > 0
+    skipping = (flce_mod.SKIP_IGNORED_ROWS and n_ignored > 0
                 and n_ignored >= max(flce_mod.COMPACT_MIN_SKIPPED, bt // 64))
-    flop_exec = 6.0 * (bt - n_ignored) * h * v if skipping else flop_step
-    if skipping and not args.chunk_rows:
+    flop_exec = 6.0 * (bt - n_ignored) * h * v / (world if vocab_mode else 1) if skipping else flop_step
+    if skipping and not args.chunk_rows and not vocab_mode:
         chunk = flce_plan(bt - n_ignored, h, v)[0]  # the plan the kept-row call runs
     if skipping:
         ws_bytes = flce_workspace_bytes(bt - n_ignored, h, v, torch.bfloat16, chunk, True)
@@ -583,7 +583,7 @@ def run_ours(args):
         if vocab_mode:
             loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, **opts)
         elif world > 1:
-            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=chunk, comm=args.comm, **opts)
+            loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=call_chunk, comm=args.comm, **opts)
         else:
             loss = loss_fn(wp, xd, td)
             loss.backward()

@@ -67,8 +67,7 @@ def _local_flce_cuda(x, w, t, mean_count, reduction="mean", **kw):
     # after every collective is enqueued, so the dW all-reduce can overlap the dW GEMMs
     loss, _, _, _, gx, gw, _ = fused_linear_cross_entropy_forward(
         x, w, t, compute_grad_input=True, compute_grad_weight=True, reduction=reduction,
-        mean_count=mean_count[:1] if reduction == "mean" else None, check_targets=False,
-        skip_ignored_rows=False, **kw)  # no host read of the kept-row count: the call stays sync-free
+        mean_count=mean_count[:1] if reduction == "mean" else None, check_targets=False, **kw)
     return loss, gx, gw
 
 
@@ -127,6 +126,7 @@ def token_sharded_flce(
     dw_slices: int = 4,
     check_targets: bool = True,
     comm: str = "nccl",
+    skip_ignored_rows: Optional[bool] = None,
     **kw,
 ):
     """Returns (loss, local grad_x, all-reduced grad_w).
@@ -135,9 +135,14 @@ def token_sharded_flce(
     per-row loss vector (rows of different ranks are not summed element-wise).
     With the CUDA kernels (default `local_fn`) and 2 <= `dw_slices` <= 16, the grad_w
     all-reduce overlaps the last chunk's grad_w GEMM (`_allreduce_grad_w_overlapped`): the
-    call enqueues every kernel and collective without a host sync, and only then (with
+    call enqueues every kernel and collective without a host sync (see skip_ignored_rows below),
+    and only then (with
     `check_targets`) reads the globally all-reduced out-of-range target count, so every rank
     raises TargetOutOfRange together instead of one rank leaving the others in a collective.
+    The local FLCE skips this rank's ignore_index rows (`skip_ignored_rows`, default
+    SKIP_IGNORED_ROWS: fused_linear_cross_entropy._forward_kept_rows).  That costs one host read
+    of the kept-row count at the start of the local call, before its GEMMs, so the dW overlap
+    is unaffected; `skip_ignored_rows=False` keeps the call entirely free of host reads.
     `comm="peer"` sums grad_w with the peer-memory kernel over a symmetric buffer
     (peer.grad_w_buffer, csrc/peer.cu) instead of NCCL; the returned grad_w is then a view of
     that buffer, overwritten by the next call for the same weight shape.
@@ -157,6 +162,8 @@ def token_sharded_flce(
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     staged = stage_target_stats(counts) if (check_targets and cuda_local) else None
     kw = dict(kw, ignore_index=ignore_index, reduction=reduction)
+    if cuda_local:
+        kw["skip_ignored_rows"] = skip_ignored_rows
     cw = kw.get("ce_weight")
     if cw is not None and reduction == "mean" and local_fn is _local_flce_cuda:
         # weighted MEAN: the denominator is the GLOBAL sum of the valid targets' weights
@@ -271,6 +278,7 @@ def vocab_parallel_flce(
     accum_dtype: Optional[torch.dtype] = None,
     dx_reduce_dtype: Optional[torch.dtype] = None,
     check_targets: bool = True,
+    skip_ignored_rows: Optional[bool] = None,
 ):
     """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
 
@@ -281,7 +289,31 @@ def vocab_parallel_flce(
     computes; by default it is written by the backward GEMM straight into grad_x in the x
     dtype and reduced there in place (`dx_reduce_dtype=torch.float32` reduces fp32 partials
     and casts after the last wait).  The only wait is on the outstanding reductions at the end.
+    With the CUDA ops the ignore_index rows are skipped (`skip_ignored_rows`, default
+    SKIP_IGNORED_ROWS): every rank holds the same targets, so every rank compacts the same rows
+    and the collectives stay matched; one host read of the kept-row count.
     """
+    from . import fused_linear_cross_entropy as flce_mod
+
+    skip = flce_mod.SKIP_IGNORED_ROWS if skip_ignored_rows is None else skip_ignored_rows
+    if ops is None and skip and x.is_cuda:
+        t_all = target.reshape(-1).to(torch.int64).contiguous()
+        kr = flce_mod.kept_rows(t_all, ignore_index)
+        if kr is not None:
+            index, pos, n = kr
+            bt_all, h = x.shape
+            xk = flce_mod._gather_rows(x.contiguous(), index, n, torch.empty(n, h, dtype=x.dtype, device=x.device))
+            tk = flce_mod._gather_rows(t_all, index, n, torch.empty(n, dtype=torch.int64, device=x.device))
+            loss, gxk, gw = vocab_parallel_flce(
+                xk, w_shard, tk, shard, group=group, ignore_index=ignore_index, label_smoothing=label_smoothing,
+                lse_square_scale=lse_square_scale, softcap=softcap, reduction=reduction, chunk_rows=chunk_rows,
+                accum_dtype=accum_dtype, dx_reduce_dtype=dx_reduce_dtype, check_targets=check_targets,
+                skip_ignored_rows=False)
+            gx = flce_mod._gather_rows(gxk, pos, bt_all, torch.empty(bt_all, h, dtype=x.dtype, device=x.device))
+            if reduction == "none":
+                loss = flce_mod._gather_rows(loss, pos, bt_all,
+                                             torch.empty(bt_all, dtype=loss.dtype, device=x.device))
+            return loss, gx, gw
     ops = ops or CudaVocabOps(x.dtype, x.device)
     t = target.reshape(-1).to(torch.int64).contiguous()
     bt, h = x.shape

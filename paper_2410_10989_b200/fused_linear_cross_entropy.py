@@ -63,6 +63,26 @@ def _gather_rows(src: torch.Tensor, index: torch.Tensor, out_rows: int, dst: tor
     return dst
 
 
+def kept_rows(t: torch.Tensor, ignore_index: int):
+    """(index, pos, n) for the rows whose target is not ignore_index: the stable list of kept
+    rows, the inverse map (-1 for ignored rows) and their count (lk_compact_rows), or None
+    when skipping does not pay (fewer than COMPACT_MIN_SKIPPED or 1/64 of the rows ignored,
+    nothing kept) or cannot run (graph capture: the count is a host read)."""
+    bt = t.numel()
+    if bt < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
+        return None
+    dev = t.device
+    index = torch.empty(bt, dtype=torch.int64, device=dev)
+    pos = torch.empty(bt, dtype=torch.int64, device=dev)
+    count = torch.empty(1, dtype=torch.int64, device=dev)
+    check(lib().lk_compact_rows(t.data_ptr(), bt, int(ignore_index), index.data_ptr(), pos.data_ptr(),
+                                count.data_ptr(), stream_of(t)))
+    n = int(count.item())  # the one host read: the chunk loop is sized by the kept rows
+    if n == 0 or bt - n < max(COMPACT_MIN_SKIPPED, bt // 64):
+        return None
+    return index, pos, n
+
+
 def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, return_z_loss, return_token_accuracy,
                        return_predicted_tokens, kw):
     """The FLCE on the rows whose target is not ignore_index, outputs scattered back to all rows.
@@ -74,15 +94,10 @@ def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, retur
     None (caller runs the full problem) when too few rows are ignored."""
     bt, h = x.shape
     dev = x.device
-    L = lib()
-    index = torch.empty(bt, dtype=torch.int64, device=dev)
-    pos = torch.empty(bt, dtype=torch.int64, device=dev)
-    count = torch.empty(1, dtype=torch.int64, device=dev)
-    check(L.lk_compact_rows(t.data_ptr(), bt, int(ignore_index), index.data_ptr(), pos.data_ptr(), count.data_ptr(),
-                            stream_of(t)))
-    n = int(count.item())  # the one host read: the chunk loop is sized by the kept rows
-    if n == 0 or bt - n < max(COMPACT_MIN_SKIPPED, bt // 64):
+    kr = kept_rows(t, ignore_index)
+    if kr is None:
         return None
+    index, pos, n = kr
     xk = _gather_rows(x, index, n, torch.empty(n, h, dtype=x.dtype, device=dev))
     tk = _gather_rows(t, index, n, torch.empty(n, dtype=torch.int64, device=dev))
     loss, z_loss, acc, pred, gxk, gw, gb = fused_linear_cross_entropy_forward(

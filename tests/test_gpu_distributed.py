@@ -55,6 +55,10 @@ def _worker(rank, port, mode, kw, out):
             t[: len(t) // 2] = -100  # rank 0's whole token shard is ignore_index
         dtype = kw.pop("_dtype", torch.bfloat16)
         zero_rows = kw.pop("_rank0_no_rows", False)
+        if "_min_skipped" in kw:  # exercise the kept-row path at test sizes
+            import paper_2410_10989_b200.fused_linear_cross_entropy as flce_mod
+
+            flce_mod.COMPACT_MIN_SKIPPED = kw.pop("_min_skipped")
         tol = 1e-4 if dtype == torch.float32 else 2e-2
         xb = torch.tensor(x, dtype=dtype, device=dev)
         wb = torch.tensor(w, dtype=dtype, device=dev)
@@ -117,14 +121,18 @@ _CW = np.random.default_rng(5).random(3000) + 0.2
                                 # the collective: sliced, unsliced, fp32, a rank with no rows
                                 dict(comm="peer"), dict(comm="peer", dw_slices=1),
                                 dict(comm="peer", dw_slices=7, label_smoothing=0.1),
-                                dict(comm="peer", _dtype=torch.float32), dict(comm="peer", _rank0_no_rows=True)])
+                                dict(comm="peer", _dtype=torch.float32), dict(comm="peer", _rank0_no_rows=True),
+                                # each rank's ignore_index rows skipped (kept-row path)
+                                dict(_min_skipped=1), dict(_min_skipped=1, comm="peer"),
+                                dict(_min_skipped=1, reduction="none"), dict(_min_skipped=1, _ignore_first_half=True)])
 def test_token_sharded_cuda_world2(kw):
     _run("token", kw)
 
 
 @pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(lse_square_scale=1e-4),
                                 dict(_ignore_first_half=True), dict(dx_reduce_dtype=torch.float32),
-                                dict(_dtype=torch.float32)])
+                                dict(_dtype=torch.float32), dict(_min_skipped=1),
+                                dict(_min_skipped=1, _ignore_first_half=True, label_smoothing=0.1)])
 def test_vocab_parallel_cuda_world2(kw):
     _run("vocab", kw)
 
@@ -148,8 +156,8 @@ def _sync_free_worker(rank, port, mode, out):
 
         def call():
             if mode == "token":
-                return token_sharded_flce(xb, wb, tb, chunk_rows=256, check_targets=False)
-            return vocab_parallel_flce(xb, wb, tb, sh, chunk_rows=256, check_targets=False)
+                return token_sharded_flce(xb, wb, tb, chunk_rows=256, check_targets=False, skip_ignored_rows=False)
+            return vocab_parallel_flce(xb, wb, tb, sh, chunk_rows=256, check_targets=False, skip_ignored_rows=False)
 
         ref = call()  # warm (workspace allocation, tensor-map encode, NCCL communicator)
         torch.cuda.synchronize()
