@@ -567,6 +567,9 @@ def run_ours(args):
         with torch.cuda.stream(copy_stream):
             xb.copy_(xh, non_blocking=True)
             tb.copy_(th, non_blocking=True)
+            # the input pipeline also enqueues the kept-row compaction of the targets it just
+            # landed (lk.prepare_kept_rows), so the step's FLCE call does not wait on the GPU
+            lk.prepare_kept_rows(tb, stream=copy_stream)
             ready[i % 2].record(copy_stream)
 
     def e2e_step():
@@ -671,7 +674,9 @@ def run_ours(args):
                     "h2d_pipeline": "each step's X/targets copied from pinned host memory on a side stream, "
                                     "double-buffered one step ahead; every step's loss copied device->host "
                                     "(pinned, on the compute stream, inside the timed region) and read on the "
-                                    "host one step later; the forward's target-range check reads a count "
+                                    "host one step later; the side stream also enqueues the targets' kept-row "
+                                    "compaction (lk.prepare_kept_rows) after their copy; the forward's "
+                                    "target-range check reads a count "
                                     "staged to pinned memory before the GEMMs every step, so the host waits "
                                     "for the count kernel only (Liger's n_non_ignore .item() waits for it too)"},
             "gpu_launches": launches * args.steps,

@@ -12,8 +12,10 @@ from .cross_entropy import CrossEntropyOutput, LigerCrossEntropyFunction, LigerC
 from .fused_linear_cross_entropy import (
     LigerFusedLinearCrossEntropyFunction,
     LigerFusedLinearCrossEntropyLoss,
+    KeptRows,
     flce_plan,
     fused_linear_cross_entropy_forward,
+    prepare_kept_rows,
 )
 from .layer_norm import LigerLayerNorm, LigerLayerNormFunction, liger_layer_norm
 from .rms_norm import LigerRMSNorm, LigerRMSNormFunction
@@ -72,7 +74,7 @@ __all__ = [
     "errors", "ChunkPlan", "plan_chunks", "b200_plan", "flce_plan",
     "CrossEntropyOutput", "LigerCrossEntropyFunction", "LigerCrossEntropyLoss",
     "LigerFusedLinearCrossEntropyFunction", "LigerFusedLinearCrossEntropyLoss",
-    "fused_linear_cross_entropy_forward",
+    "fused_linear_cross_entropy_forward", "prepare_kept_rows", "KeptRows",
     "LigerRMSNorm", "LigerRMSNormFunction", "LigerLayerNorm", "LigerLayerNormFunction", "liger_layer_norm", "LigerRopeFunction", "liger_rotary_pos_emb",
     "LigerSiLUMulFunction", "LigerGELUMulFunction", "LigerSwiGLUMLP", "LigerGEGLUMLP",
     "liger_swiglu", "liger_geglu", "liger_cross_entropy", "liger_fused_linear_cross_entropy", "liger_rms_norm",

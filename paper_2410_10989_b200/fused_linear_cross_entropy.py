@@ -63,21 +63,77 @@ def _gather_rows(src: torch.Tensor, index: torch.Tensor, out_rows: int, dst: tor
     return dst
 
 
-def kept_rows(t: torch.Tensor, ignore_index: int):
-    """(index, pos, n) for the rows whose target is not ignore_index: the stable list of kept
-    rows, the inverse map (-1 for ignored rows) and their count (lk_compact_rows), or None
-    when skipping does not pay (fewer than COMPACT_MIN_SKIPPED or 1/64 of the rows ignored,
-    nothing kept) or cannot run (graph capture: the count is a host read)."""
+class KeptRows:
+    """A compaction of one target vector enqueued ahead of the FLCE call that consumes it
+    (`prepare_kept_rows`): the kept-row list, the inverse map, and the kept count copied to
+    pinned host memory behind an event."""
+
+    def __init__(self, index, pos, count_host, event, rows):
+        self.index, self.pos, self.count_host, self.event, self.rows = index, pos, count_host, event, rows
+
+    @property
+    def n(self) -> int:
+        self.event.synchronize()  # done long ago when prepared early: no wait
+        return int(self.count_host[0])
+
+
+_PREPARED: dict = {}  # (data_ptr, numel, ignore_index, device) -> (version, KeptRows)
+_PREPARED_MAX = 8
+
+
+def _compact(t: torch.Tensor, ignore_index: int):
     bt = t.numel()
-    if bt < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
-        return None
     dev = t.device
     index = torch.empty(bt, dtype=torch.int64, device=dev)
     pos = torch.empty(bt, dtype=torch.int64, device=dev)
     count = torch.empty(1, dtype=torch.int64, device=dev)
     check(lib().lk_compact_rows(t.data_ptr(), bt, int(ignore_index), index.data_ptr(), pos.data_ptr(),
                                 count.data_ptr(), stream_of(t)))
-    n = int(count.item())  # the one host read: the chunk loop is sized by the kept rows
+    return index, pos, count
+
+
+def prepare_kept_rows(target: torch.Tensor, ignore_index: int = -100,
+                      stream: Optional[torch.cuda.Stream] = None) -> Optional[KeptRows]:
+    """Enqueue the kept-row compaction of `target` now (e.g. as soon as the labels exist, before
+    the model's forward), on `stream` (default: the current stream), which must be ordered
+    before the stream of the FLCE call.  A later FLCE call on the same, unmodified target
+    tensor (same storage, same version) then sizes its chunk loop from a count the GPU
+    produced long before, instead of waiting for all work queued ahead of it."""
+    t = as_targets(target)
+    if not t.is_cuda or t.numel() < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
+        return None
+    with torch.cuda.stream(stream or torch.cuda.current_stream(t.device)):
+        index, pos, count = _compact(t, ignore_index)
+        host = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        host.copy_(count, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+    kr = KeptRows(index, pos, host, ev, t.numel())
+    while len(_PREPARED) >= _PREPARED_MAX:
+        _PREPARED.pop(next(iter(_PREPARED)))
+    _PREPARED[(t.data_ptr(), t.numel(), int(ignore_index), t.device)] = (t._version, kr)
+    return kr
+
+
+def kept_rows(t: torch.Tensor, ignore_index: int):
+    """(index, pos, n) for the rows whose target is not ignore_index: the stable list of kept
+    rows, the inverse map (-1 for ignored rows) and their count (lk_compact_rows), or None
+    when skipping does not pay (fewer than COMPACT_MIN_SKIPPED or 1/64 of the rows ignored,
+    nothing kept) or cannot run (graph capture: the count is a host read).  Uses the
+    compaction `prepare_kept_rows` enqueued for this tensor, if any."""
+    bt = t.numel()
+    if bt < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
+        return None
+    entry = _PREPARED.pop((t.data_ptr(), bt, int(ignore_index), t.device), None)
+    if entry is not None and entry[0] == t._version and entry[1].rows == bt:
+        kr = entry[1]
+        cur = torch.cuda.current_stream(t.device)
+        kr.index.record_stream(cur)
+        kr.pos.record_stream(cur)
+        index, pos, n = kr.index, kr.pos, kr.n
+    else:
+        index, pos, count = _compact(t, ignore_index)
+        n = int(count.item())  # the host read: the chunk loop is sized by the kept rows
     if n == 0 or bt - n < max(COMPACT_MIN_SKIPPED, bt // 64):
         return None
     return index, pos, n

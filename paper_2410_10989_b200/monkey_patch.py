@@ -114,6 +114,19 @@ def lce_forward(self, input_ids=None, attention_mask=None, position_ids=None, pa
     if getattr(self.config, "pretraining_tp", 1) > 1:
         raise NotImplementedError("pretraining_tp > 1 is not supported")
     shift_labels = kwargs.pop("shift_labels", None)
+    head_loss = skip_logits if skip_logits is not None else (
+        self.training and (labels is not None or shift_labels is not None))
+    if head_loss and (labels is not None or shift_labels is not None):
+        # the fused head skips ignore_index rows; its row compaction is enqueued here, before
+        # the decoder runs, so the head later sizes its chunk loop from a count the GPU produced
+        # long before instead of waiting for the whole forward (prepare_kept_rows)
+        if shift_labels is None:
+            shift_labels = nn.functional.pad(labels, (0, 1), value=kwargs.get("ignore_index", -100))[..., 1:]
+            shift_labels = shift_labels.contiguous()
+        if shift_labels.is_cuda:
+            from .fused_linear_cross_entropy import prepare_kept_rows
+
+            prepare_kept_rows(shift_labels.reshape(-1), ignore_index=kwargs.get("ignore_index", -100))
     outputs = self.model(input_ids=input_ids, attention_mask=attention_mask, position_ids=position_ids,
                          past_key_values=past_key_values, inputs_embeds=inputs_embeds, use_cache=use_cache, **kwargs)
     hidden_states = outputs[0]

@@ -142,3 +142,33 @@ def test_skip_ignored_rows_is_bitwise_repeatable():
     for _ in range(3):
         b = flce_mod.fused_linear_cross_entropy_forward(x, w, t, compute_grad_input=True, compute_grad_weight=True)
         assert a[0].item() == b[0].item() and torch.equal(a[4], b[4]) and torch.equal(a[5], b[5])
+
+
+def test_prepared_kept_rows_match_and_are_consumed():
+    """lk.prepare_kept_rows on a side stream ahead of the call: the same result bit for bit as
+    the call that compacts by itself; the entry is consumed; an in-place change to the targets
+    after preparing (a new tensor version) falls back to a fresh compaction."""
+    import paper_2410_10989_b200 as lk
+
+    flce_mod._PREPARED.clear()
+    x, w, t = _problem(4096, 256, 5000, 0.25, torch.bfloat16, seed=9)
+    kw = dict(compute_grad_input=True, compute_grad_weight=True)
+    ref = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    kr = lk.prepare_kept_rows(t, stream=side)
+    assert kr is not None and len(flce_mod._PREPARED) == 1
+    torch.cuda.current_stream().wait_stream(side)
+    got = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    assert len(flce_mod._PREPARED) == 0
+    assert ref[0].item() == got[0].item() and torch.equal(ref[4], got[4]) and torch.equal(ref[5], got[5])
+    assert kr.n == int((t != -100).sum())
+    # stale: the targets change after preparing -> recompacted, matches a fresh call
+    lk.prepare_kept_rows(t)
+    t2 = t.clone()
+    t[:100] = -100
+    t2[:100] = -100
+    a = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    b = flce_mod.fused_linear_cross_entropy_forward(x, w, t2, **kw)
+    assert a[0].item() == b[0].item() and torch.equal(a[4], b[4]) and torch.equal(a[5], b[5])
+    flce_mod._PREPARED.clear()
