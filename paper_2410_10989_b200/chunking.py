@@ -71,11 +71,12 @@ class B200Plan:
 
 def b200_plan(total_rows: int, vocab_size: int, hidden_size: int, elem_bytes: int = 2) -> B200Plan:
     """Host restatement of the library's default (flce.cu b200_chunk_rows): the fewest chunks
-    of at most 3072 rows (4096 when BT > 16384) and a 1 GiB logits buffer, split evenly in
-    256-row tiles; never below the reference's rule (capped by the buffer)."""
+    of at most 3072 rows (4096 when BT > 16384) and a 1.5 GiB logits buffer (1 GiB for fp32),
+    split evenly in 256-row tiles; never below the reference's rule (capped by the buffer)."""
     ref = plan_chunks(total_rows, vocab_size, hidden_size).chunk_rows
     ldz = -(-vocab_size // 64) * 64
-    cap_rows = max(256, (1 << 30) // (ldz * elem_bytes) // 256 * 256)
+    cap_bytes = (1 << 30) if elem_bytes == 4 else (3 << 29)  # 1.5 GiB (1 GiB for fp32 logits)
+    cap_rows = max(256, cap_bytes // (ldz * elem_bytes) // 256 * 256)
     c_max = min(4096 if total_rows > 2048 * 8 else 3072, cap_rows)
     if total_rows <= c_max:
         c = total_rows

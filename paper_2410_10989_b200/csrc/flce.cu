@@ -239,10 +239,13 @@ static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dt
   // pass of the dW GEMM over all of grad_w, and a pass costs ~0.35 ms at the Llama-3 head
   // beyond its FLOPs (measured: 4 -> 3 chunks of 8192 rows is +2.4%, 3 -> 2 is flat;
   // profiles/r02/chunk_count_probe.log), while the logits buffer grows with the chunk.
-  // Cap: 3072 rows (12 tiles) up to 16384 rows, 4096 beyond, and a logits buffer <= 1 GiB.
+  // Cap: 3072 rows (12 tiles) up to 16384 rows, 4096 beyond, and a logits buffer <= 1.5 GiB
+  // (1 GiB for fp32 inputs, whose chunk also carries three bf16 piece copies).  At the Gemma-2
+  // head (V = 256000) the 1.5 GiB cap allows 3 chunks instead of 4: +1.6%
+  // (profiles/r02/cfg4_chunk_ab.log).
   const int64_t ratio = (vocab + hidden - 1) / hidden;
   const int64_t c_ref = next_pow2((bt + ratio - 1) / ratio);  // the reference's rule
-  const int64_t cap_bytes = (int64_t)1 << 30;
+  const int64_t cap_bytes = dtype == LK_F32 ? (int64_t)1 << 30 : (int64_t)3 << 29;
   const int64_t row_bytes = ld_logits(vocab) * elt_size(dtype);
   const int64_t cap_rows = std::max<int64_t>(256, cap_bytes / row_bytes / 256 * 256);
   const int64_t c_max = std::min<int64_t>(bt > 2048 * LK_ACCUM_AUTO_MAX_CHUNKS ? 4096 : 3072, cap_rows);

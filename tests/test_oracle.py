@@ -224,8 +224,9 @@ def test_chunk_plan_validation():
     assert b200_plan(3000, 128256, 4096).num_chunks == 1  # <= 3072 rows: one chunk
     assert (b200_plan(16384, 128256, 4096).chunk_rows, b200_plan(16384, 128256, 4096).num_chunks) == (2816, 6)
     assert b200_plan(65536, 128256, 4096).chunk_rows == 4096  # cfg5 at N = 1: 16 chunks
-    assert b200_plan(8192, 256000, 3584).chunk_rows == 2048  # cfg4: the 1 GiB buffer caps at 2048 rows
-    assert b200_plan(65536, 256000, 3584).chunk_rows == 2048
+    assert b200_plan(8192, 256000, 3584).num_chunks == 3  # cfg4: 2816-row chunks, a 1.44 GB buffer
+    assert b200_plan(7373, 256000, 3584).chunk_rows == 2560  # cfg4's kept rows
+    assert b200_plan(65536, 256000, 3584).chunk_rows == 3072  # the 1.5 GiB buffer caps V = 256000
     assert b200_plan(8192, 128256, 4096, elem_bytes=4).chunk_rows == 2048  # fp32 logits: 1 GiB cap
     for bt in (1, 255, 3073, 9000, 20000, 100000):
         q = b200_plan(bt, 128256, 4096)
