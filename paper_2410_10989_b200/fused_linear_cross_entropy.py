@@ -95,10 +95,12 @@ def _compact(t: torch.Tensor, ignore_index: int):
 def prepare_kept_rows(target: torch.Tensor, ignore_index: int = -100,
                       stream: Optional[torch.cuda.Stream] = None) -> Optional[KeptRows]:
     """Enqueue the kept-row compaction of `target` now (e.g. as soon as the labels exist, before
-    the model's forward), on `stream` (default: the current stream), which must be ordered
-    before the stream of the FLCE call.  A later FLCE call on the same, unmodified target
-    tensor (same storage, same version) then sizes its chunk loop from a count the GPU
-    produced long before, instead of waiting for all work queued ahead of it."""
+    the model's forward), on `stream` (default: the current stream; the target's producer
+    must be ordered before it).  A later FLCE call on the same, unmodified target tensor (same
+    storage, same version) then sizes its chunk loop from a count the GPU produced long
+    before, instead of waiting for all work queued ahead of it.  That call waits on the
+    compaction's event before enqueuing anything that reads its output, so `stream` need not
+    be ordered with the call's stream."""
     t = as_targets(target)
     if not t.is_cuda or t.numel() < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
         return None
