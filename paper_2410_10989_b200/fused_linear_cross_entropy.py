@@ -68,8 +68,11 @@ class KeptRows:
     (`prepare_kept_rows`): the kept-row list, the inverse map, and the kept count copied to
     pinned host memory behind an event."""
 
-    def __init__(self, index, pos, count_host, event, rows):
-        self.index, self.pos, self.count_host, self.event, self.rows = index, pos, count_host, event, rows
+    def __init__(self, target, index, pos, count_host, event):
+        # the target tensor itself is held: while the entry exists no other tensor can occupy
+        # its memory, so (data pointer, version) identifies it
+        self.target, self.index, self.pos, self.count_host, self.event = target, index, pos, count_host, event
+        self.rows = target.numel()
 
     @property
     def n(self) -> int:
@@ -110,7 +113,7 @@ def prepare_kept_rows(target: torch.Tensor, ignore_index: int = -100,
         host.copy_(count, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-    kr = KeptRows(index, pos, host, ev, t.numel())
+    kr = KeptRows(t, index, pos, host, ev)
     while len(_PREPARED) >= _PREPARED_MAX:
         _PREPARED.pop(next(iter(_PREPARED)))
     _PREPARED[(t.data_ptr(), t.numel(), int(ignore_index), t.device)] = (t._version, kr)
@@ -127,7 +130,7 @@ def kept_rows(t: torch.Tensor, ignore_index: int):
     if bt < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
         return None
     entry = _PREPARED.pop((t.data_ptr(), bt, int(ignore_index), t.device), None)
-    if entry is not None and entry[0] == t._version and entry[1].rows == bt:
+    if entry is not None and entry[0] == t._version and entry[1].rows == bt and entry[1].target.data_ptr() == t.data_ptr():
         kr = entry[1]
         cur = torch.cuda.current_stream(t.device)
         kr.index.record_stream(cur)
