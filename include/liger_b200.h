@@ -227,11 +227,17 @@ typedef struct {
    * segments added in fp32 (the tensor core's own accumulator truncates).  Ignored for
    * 16-bit dtypes and with force_simt. */
   int fp32_pieces;
+  /* Kept-row gather (the ignored-row skipping of fused_linear_cross_entropy.py): NULL, or
+   * x_row_index[bt] = the x row of each of the call's bt rows (lk_compact_rows' list).  The
+   * chunk loop then gathers each chunk's X rows into a chunk-sized workspace buffer
+   * (lk_gather_rows) instead of reading x[lo : lo + r]; everything else -- targets, grad_x,
+   * the per-row outputs -- is indexed by the call's rows.  x may hold more rows than bt. */
+  const int64_t* x_row_index;
 } lk_flce_args;
 
 /* Workspace bytes for exactly this call (every field that sizes the workspace is read:
  * bt, hidden, vocab, dtype, chunk_rows, grad_w, grad_bias, grad_w_accum, force_simt,
- * fp32_pieces; pointers may be NULL). */
+ * fp32_pieces, x_row_index; other pointers may be NULL). */
 size_t lk_flce_workspace_bytes_for(const lk_flce_args* args);
 
 enum { LK_ACCUM_AUTO = 0, LK_ACCUM_FP32 = 1, LK_ACCUM_WEIGHT_DTYPE = 2 };

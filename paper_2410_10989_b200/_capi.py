@@ -71,6 +71,7 @@ class FlceArgs(C.Structure):
         ("ce_weight", c_void),
         ("mean_weight_sum", c_void),
         ("fp32_pieces", c_int),
+        ("x_row_index", c_void),
     ]
 
 

@@ -136,14 +136,12 @@ extern "C" int lk_compact_rows(const int64_t* targets, int64_t rows, int64_t ign
   return check_launch("compact_rows_kernel");
 }
 
-extern "C" int lk_gather_rows(const void* src, int64_t cols, int elem_bytes, const int64_t* index, int64_t out_rows,
-                              void* dst, uint64_t fill, void* stream) {
-  LK_REQUIRE(cols >= 0 && out_rows >= 0, LK_INVALID_ARGUMENT, "lk_gather_rows: negative size");
-  LK_REQUIRE(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8, LK_INVALID_ARGUMENT,
-             "lk_gather_rows: elem_bytes must be 1, 2, 4 or 8");
-  if (cols == 0 || out_rows == 0) return LK_OK;
-  LK_REQUIRE(src && dst && index, LK_INVALID_ARGUMENT, "lk_gather_rows: null pointer");
-  cudaStream_t st = as_stream(stream);
+namespace lk {
+// dst[i, :] = index[i] >= 0 ? src[index[i], :] : fill, for i < out_rows (also used by the FLCE
+// chunk loop to gather a chunk's kept X rows: lk_flce_args.x_row_index).
+int launch_gather_rows(const void* src, int64_t cols, int elem_bytes, const int64_t* index, int64_t out_rows,
+                       void* dst, uint64_t fill, cudaStream_t st) {
+  using namespace compact;
   const int64_t row_bytes = cols * elem_bytes;
   const bool vec = row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(src) % 16 == 0 &&
                    reinterpret_cast<uintptr_t>(dst) % 16 == 0;
@@ -151,8 +149,7 @@ extern "C" int lk_gather_rows(const void* src, int64_t cols, int elem_bytes, con
     uint4 f;  // the fill element repeated over 16 bytes
     unsigned char* fb = reinterpret_cast<unsigned char*>(&f);
     for (int i = 0; i < 16; ++i) fb[i] = reinterpret_cast<const unsigned char*>(&fill)[i % elem_bytes];
-    const int64_t warps_needed = out_rows;
-    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((warps_needed + 7) / 8, 16 * sm_count()));
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((out_rows + 7) / 8, 16 * sm_count()));
     gather_rows_vec_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4*>(src), row_bytes / 16, index, out_rows,
                                                    static_cast<uint4*>(dst), f);
     return check_launch("gather_rows_vec_kernel");
@@ -163,4 +160,15 @@ extern "C" int lk_gather_rows(const void* src, int64_t cols, int elem_bytes, con
     case 4: return launch_elem<uint32_t>(src, cols, index, out_rows, dst, fill, st);
     default: return launch_elem<uint64_t>(src, cols, index, out_rows, dst, fill, st);
   }
+}
+}  // namespace lk
+
+extern "C" int lk_gather_rows(const void* src, int64_t cols, int elem_bytes, const int64_t* index, int64_t out_rows,
+                              void* dst, uint64_t fill, void* stream) {
+  LK_REQUIRE(cols >= 0 && out_rows >= 0, LK_INVALID_ARGUMENT, "lk_gather_rows: negative size");
+  LK_REQUIRE(elem_bytes == 1 || elem_bytes == 2 || elem_bytes == 4 || elem_bytes == 8, LK_INVALID_ARGUMENT,
+             "lk_gather_rows: elem_bytes must be 1, 2, 4 or 8");
+  if (cols == 0 || out_rows == 0) return LK_OK;
+  LK_REQUIRE(src && dst && index, LK_INVALID_ARGUMENT, "lk_gather_rows: null pointer");
+  return launch_gather_rows(src, cols, elem_bytes, index, out_rows, dst, fill, as_stream(stream));
 }

@@ -234,6 +234,9 @@ static int64_t ld_logits(int64_t vocab) { return (vocab + 63) / 64 * 64; }
 // (BT > 16384) take 4096-row chunks: half the W re-streams and dW RMWs, +3.2% at
 // BT = 65536 (cfg5 at N = 1) and +0.8% at BT = 8192, for which the smaller buffer is kept
 // (profiles/r02/chunk_sweep.log).  The chunk buffer is capped at 1 GiB.
+int launch_gather_rows(const void* src, int64_t cols, int elem_bytes, const int64_t* index, int64_t out_rows,
+                       void* dst, uint64_t fill, cudaStream_t st);  // compact.cu
+
 static int64_t b200_chunk_rows(int64_t bt, int64_t hidden, int64_t vocab, int dtype) {
   // Fewest chunks under a row cap, split evenly in 256-row CTA-pair tiles.  Every chunk is one
   // pass of the dW GEMM over all of grad_w, and a pass costs ~0.35 ms at the Llama-3 head
@@ -268,6 +271,7 @@ struct FlceLayout {
   int pieces, nT;
   size_t off_counts, off_sched, off_z, off_parts, off_tgt, off_acc, off_bias;
   size_t off_wp, off_xp, off_dzp;  // bf16 pieces: W [P][V][H], X_c [P][C][H], dZ [P][C][ldz]
+  size_t off_xg;                    // gathered X chunk [C][H] (lk_flce_args.x_row_index)
   size_t total;
 };
 
@@ -312,7 +316,7 @@ static bool wdtype_accum(int mode, int dtype, int64_t nchunks, bool tc) {
 
 static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dtype, int64_t chunk_rows,
                               bool has_grad_w, bool has_bias_grad, bool tc, int accum_mode, bool tc32 = false,
-                              int pieces = 2, bool has_grad_x = true) {
+                              int pieces = 2, bool has_grad_x = true, bool gather_x = false) {
   FlceLayout L{};
   L.tc32 = tc32;
   L.pieces = pieces == 2 ? 2 : 3;  // default 3: products exact to fp32's 2^-24
@@ -339,6 +343,7 @@ static FlceLayout flce_layout(int64_t bt, int64_t hidden, int64_t vocab, int dty
   L.off_wp = take(tc32 ? P * (size_t)vocab * hidden * 2 : 0);
   L.off_xp = take(tc32 ? P * (size_t)L.C * hidden * 2 : 0);
   L.off_dzp = take(tc32 ? P * (size_t)L.C * L.ldz * 2 : 0);
+  L.off_xg = take(gather_x ? (size_t)L.C * hidden * elt_size(dtype) : 0);
   L.total = align_up(off, 1024);
   return L;
 }
@@ -375,7 +380,8 @@ static FlceLayout layout_for(const lk_flce_args* a) {
   const bool tc = use_tc_path(a->dtype, a->hidden, a->x, a->weight, a->force_simt);
   const bool tc32 = use_tc32_path(a->dtype, a->hidden, a->force_simt);
   return flce_layout(a->bt, a->hidden, a->vocab, a->dtype, a->chunk_rows, a->grad_w != nullptr,
-                     a->grad_bias != nullptr, tc, a->grad_w_accum, tc32, a->fp32_pieces, a->grad_x != nullptr);
+                     a->grad_bias != nullptr, tc, a->grad_w_accum, tc32, a->fp32_pieces, a->grad_x != nullptr,
+                     a->x_row_index != nullptr);
 }
 
 extern "C" size_t lk_flce_workspace_bytes_for(const lk_flce_args* a) {
@@ -477,6 +483,13 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
     const int64_t lo = ci * L.C;
     const int64_t r = std::min(L.C, BT - lo);
     const char* xc = static_cast<const char*>(a->x) + lo * H * es;
+    if (a->x_row_index) {  // kept-row gather: this chunk's X rows into the chunk-sized buffer
+      ProfScope ps(3, st);
+      char* xg = ws + L.off_xg;
+      rc = launch_gather_rows(a->x, H, (int)es, a->x_row_index + lo, r, xg, 0, st);
+      if (rc) return rc;
+      xc = xg;
+    }
     const bool first = ci == 0, last = ci == L.nchunks - 1;
     if (tc32) {
       ProfScope ps(3, st);

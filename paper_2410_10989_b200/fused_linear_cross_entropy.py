@@ -159,11 +159,14 @@ def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, retur
     if kr is None:
         return None
     index, pos, n = kr
-    xk = _gather_rows(x, index, n, torch.empty(n, h, dtype=x.dtype, device=dev))
+    # the kept targets are gathered here (8 bytes a row); the kept X rows are gathered by the
+    # library one chunk at a time into its workspace (lk_flce_args.x_row_index), so no
+    # n x H copy of X is ever held
     tk = _gather_rows(t, index, n, torch.empty(n, dtype=torch.int64, device=dev))
     loss, z_loss, acc, pred, gxk, gw, gb = fused_linear_cross_entropy_forward(
-        xk, w, tk, compute_grad_input=need_gx, compute_grad_weight=need_gw, skip_ignored_rows=False, **kw)
-    del xk, tk
+        x, w, tk, compute_grad_input=need_gx, compute_grad_weight=need_gw, skip_ignored_rows=False,
+        _x_row_index=index, **kw)
+    del tk
     gx = _gather_rows(gxk, pos, bt, torch.empty_like(x)) if gxk is not None else None
     if reduction == "none":  # per-row outputs back to every row (ignored: 0)
         loss = _gather_rows(loss, pos, bt, torch.empty(bt, dtype=loss.dtype, device=dev))
@@ -204,6 +207,7 @@ def fused_linear_cross_entropy_forward(
     fp32_pieces: int = 0,
     grad_w_out: Optional[torch.Tensor] = None,
     skip_ignored_rows: Optional[bool] = None,
+    _x_row_index: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -240,6 +244,8 @@ def fused_linear_cross_entropy_forward(
     if _input.dim() != 2 or weight.dim() != 2:
         raise errors.ShapeMismatch("expected _input (BT, H) and weight (V, H)")
     bt, h = _input.shape
+    if _x_row_index is not None:  # internal (_forward_kept_rows): the call's rows are x[_x_row_index[:n]]
+        bt = target.numel()
     v, hw = weight.shape
     if hw != h:
         raise errors.ShapeMismatch(f"hidden width {h} != weight input width {hw}")
@@ -271,7 +277,7 @@ def fused_linear_cross_entropy_forward(
                  check_targets=check_targets, fp32_pieces=fp32_pieces, grad_w_out=grad_w_out))
         if kept is not None:
             return kept
-    grad_x = torch.empty_like(x) if need_gx else None
+    grad_x = torch.empty(bt, h, dtype=x.dtype, device=dev) if need_gx else None
     if need_gw and grad_w_out is not None:
         if grad_w_out.shape != w.shape or grad_w_out.dtype != w.dtype or grad_w_out.device != w.device:
             raise errors.ShapeMismatch("grad_w_out must match weight's shape, dtype and device")
@@ -307,6 +313,7 @@ def fused_linear_cross_entropy_forward(
         raise errors.UnsupportedOption(f"accum_dtype {accum_dtype}: use None, torch.float32 or the weight dtype")
     args = _capi.FlceArgs(
         x=ptr(x), weight=ptr(w), target=ptr(t), bias=ptr(b), bt=bt, hidden=h, vocab=v, dtype=dt,
+        x_row_index=ptr(_x_row_index),
         ignore_index=int(ignore_index), label_smoothing=float(label_smoothing),
         lse_square_scale=float(lse_square_scale), softcap=float(softcap) if softcap is not None else 0.0,
         reduction=_capi.REDUCTIONS[reduction], chunk_rows=cr, loss_rows=ptr(loss_rows), loss_sum=ptr(loss_sum),
