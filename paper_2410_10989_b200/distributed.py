@@ -279,6 +279,7 @@ def vocab_parallel_flce(
     dx_reduce_dtype: Optional[torch.dtype] = None,
     check_targets: bool = True,
     skip_ignored_rows: Optional[bool] = None,
+    _x_row_index: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
 
@@ -302,13 +303,13 @@ def vocab_parallel_flce(
         if kr is not None:
             index, pos, n = kr
             bt_all, h = x.shape
-            xk = flce_mod._gather_rows(x.contiguous(), index, n, torch.empty(n, h, dtype=x.dtype, device=x.device))
             tk = flce_mod._gather_rows(t_all, index, n, torch.empty(n, dtype=torch.int64, device=x.device))
+            # X rows are gathered chunk by chunk inside the loop (_x_row_index): no n x H copy
             loss, gxk, gw = vocab_parallel_flce(
-                xk, w_shard, tk, shard, group=group, ignore_index=ignore_index, label_smoothing=label_smoothing,
-                lse_square_scale=lse_square_scale, softcap=softcap, reduction=reduction, chunk_rows=chunk_rows,
-                accum_dtype=accum_dtype, dx_reduce_dtype=dx_reduce_dtype, check_targets=check_targets,
-                skip_ignored_rows=False)
+                x.contiguous(), w_shard, tk, shard, group=group, ignore_index=ignore_index,
+                label_smoothing=label_smoothing, lse_square_scale=lse_square_scale, softcap=softcap,
+                reduction=reduction, chunk_rows=chunk_rows, accum_dtype=accum_dtype, dx_reduce_dtype=dx_reduce_dtype,
+                check_targets=check_targets, skip_ignored_rows=False, _x_row_index=index)
             gx = flce_mod._gather_rows(gxk, pos, bt_all, torch.empty(bt_all, h, dtype=x.dtype, device=x.device))
             if reduction == "none":
                 loss = flce_mod._gather_rows(loss, pos, bt_all,
@@ -317,6 +318,8 @@ def vocab_parallel_flce(
     ops = ops or CudaVocabOps(x.dtype, x.device)
     t = target.reshape(-1).to(torch.int64).contiguous()
     bt, h = x.shape
+    if _x_row_index is not None:  # internal (kept rows): the call's rows are x[_x_row_index[:len(t)]]
+        bt = t.numel()
     n_valid = ops.count(t, shard.total, ignore_index)
     staged = stage_target_stats(n_valid) if (check_targets and isinstance(ops, CudaVocabOps)) else None
     if w_shard.dtype == torch.float64:
@@ -334,7 +337,12 @@ def vocab_parallel_flce(
     pending = []  # (work, lo, hi, partial) of in-flight dX reductions
     for ci, lo in enumerate(range(0, bt, chunk_rows)):
         hi = min(lo + chunk_rows, bt)
-        xc, tc = x[lo:hi].contiguous(), t[lo:hi]
+        if _x_row_index is not None:
+            xc = flce_mod._gather_rows(x, _x_row_index[lo:hi], hi - lo,
+                                       torch.empty(hi - lo, h, dtype=x.dtype, device=x.device))
+        else:
+            xc = x[lo:hi].contiguous()
+        tc = t[lo:hi]
         stats, buf = ops.logits_stats(xc, w_shard, tc, shard, softcap, ignore_index)
         stats_g = combine_row_stats(stats, ops, group)
         gx_out = gx[lo:hi] if dx_dt == x.dtype else torch.empty(hi - lo, h, dtype=dx_dt, device=x.device)
