@@ -69,7 +69,8 @@ class PeerBuffer:
         check(L.lk_peer_alloc(self.dev_index, self.nbytes, C.byref(base), handle))
         self.base = int(base.value)
         handles: list = [None] * self.world
-        dist.all_gather_object(handles, bytes(handle), group=group)
+        with torch.cuda.device(self.dev_index):  # NCCL's object gather stages on the current device
+            dist.all_gather_object(handles, bytes(handle), group=group)
         self._opened = []
         ptrs = []
         try:
