@@ -4,7 +4,7 @@
  * This is the drop-in boundary for the reference's fused-kernel layer
  * (/root/reference/pkg/src/rowfuse/ops.py and flce.py, surveyed in SURVEY.md
  * §8(a)/(b)) and for the third-party Liger operator surface those kernels stand
- * for (liger_kernel 0.8.0, ops/*.py).  The reference is pure Python, so there is
+ * for (liger_kernel 0.8.0, the ops package).  The reference is pure Python, so there is
  * no FFI to replace; each entry point below is what a ctypes/cffi binding of the
  * reference's operator would call (see INTEGRATION.md for the binding stubs).
  *
