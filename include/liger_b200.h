@@ -233,6 +233,12 @@ typedef struct {
    * (lk_gather_rows) instead of reading x[lo : lo + r]; everything else -- targets, grad_x,
    * the per-row outputs -- is indexed by the call's rows.  x may hold more rows than bt. */
   const int64_t* x_row_index;
+  /* Device-side row count (with x_row_index: the kept-row FLCE without a host read of the
+   * count, e.g. under CUDA graph capture): NULL, or a device int64 n <= bt.  The caller
+   * guarantees that rows >= n are ignore_index rows whose X rows are zero (x_row_index = -1).
+   * The CTA-pair GEMMs then skip the M tiles past row n of each chunk and stop the dW K loop at
+   * row max(n, 1).  The outputs are unchanged: a limit only removes work. */
+  const int64_t* row_limit;
 } lk_flce_args;
 
 /* Workspace bytes for exactly this call (every field that sizes the workspace is read:

@@ -72,6 +72,7 @@ class FlceArgs(C.Structure):
         ("mean_weight_sum", c_void),
         ("fp32_pieces", c_int),
         ("x_row_index", c_void),
+        ("row_limit", c_void),
     ]
 
 

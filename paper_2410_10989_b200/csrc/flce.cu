@@ -175,6 +175,8 @@ int launch_tc_gemm(const TmaOperand* a, const TmaOperand* b, Problem* probs, int
     total += P.tiles_m * P.tiles_n;
   }
   if (n_problems == 1) { maps[2] = maps[0]; maps[3] = maps[1]; maps[5] = maps[4]; }
+  if (cta_group == 1)  // the single-CTA kernel runs every row (a limit only removes work)
+    for (int p = 0; p < n_problems; ++p) { args.prob[p].m_limit = nullptr; args.prob[p].k_limit = nullptr; }
   args.total_tiles = total;
   args.counter = counter;
   if (total == 0) return LK_OK;
@@ -512,11 +514,13 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         // m-fastest raster: the 8 pairs working on one W tile run together (W read once from HBM;
         // n-fastest measured 15% slower, profiles/README.md)
         P.M = r; P.N = V; P.K = H; P.n_fast = 0; P.epi = le;
+        P.m_limit = a->row_limit; P.m_base = lo;
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, dt, sched + 2 * ci, st);
       } else if (tc32) {  // fp32 logits = sum over the terms of X piece ordA[t] . W piece ordC[t]
         tc::TmaOperand A{xp, H, r, H, 0, (int)NP, L.C * H}, B{wp, H, V, H, 0, (int)NP, V * H};
         tc::Problem P{};
         P.M = r; P.N = V; P.n_fast = 0; P.epi = le;
+        P.m_limit = a->row_limit; P.m_base = lo;
         set_terms(P, H);
         rc = tc::launch_tc_gemm(&A, &B, &P, 1, LK_BF16, sched + 2 * ci, st);
       } else {
@@ -596,6 +600,10 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
       const tc::TmaOperand dxA = tc32 ? tc::TmaOperand{dzp, L.ldz, r, L.ldz, 0, npc, L.C * L.ldz}
                                       : tc::TmaOperand{zbuf, V, r, L.ldz, 0};
       const tc::TmaOperand dxB = tc32 ? tc::TmaOperand{wp, H, V, H, 1, npc, V * H} : tc::TmaOperand{a->weight, H, V, H, 1};
+      // dW K loop stops at the device row limit, except on the split-operand path (K is runs of
+      // pieces) and in a last chunk that must write grad_w from the fp32 accumulator (a pass
+      // limited to zero rows would skip that write)
+      const bool dw_k_limit = a->row_limit && !tc32 && !(last && L.need_acc);
       const void* dwA_base = tc32 ? dzp : zbuf;
       const void* dwB_base = tc32 ? xp : xc;
       auto dw_ops = [&](int64_t v0, int64_t v1, tc::TmaOperand& A, tc::TmaOperand& B) {
@@ -611,6 +619,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Bs[np] = dxB;
         Ps[np] = tc::Problem{};
         Ps[np].M = r; Ps[np].N = H; Ps[np].K = V; Ps[np].n_fast = 0; Ps[np].epi = xe;
+        Ps[np].m_limit = a->row_limit; Ps[np].m_base = lo;
         if (tc32) {
           set_terms(Ps[np], L.ldz);
           // fp32 dX (K = nT x ldz): restart the truncating tensor-core accumulation every
@@ -626,6 +635,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
         Ps[np] = tc::Problem{};
         Ps[np].M = V; Ps[np].N = H; Ps[np].K = r; Ps[np].n_fast = 1; Ps[np].epi = we;
         if (tc32) set_terms(Ps[np], r);
+        if (dw_k_limit) { Ps[np].k_limit = a->row_limit; Ps[np].k_base = lo; }
         ++np;
       }
       if (np) rc = tc::launch_tc_gemm(As, Bs, Ps, np, gdt, sched + 2 * ci + 1, st);
@@ -644,6 +654,7 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
           tc::Problem P1{};
           P1.M = v1 - v0; P1.N = H; P1.K = r; P1.n_fast = 1; P1.epi = ws;
           if (tc32) set_terms(P1, r);
+          if (dw_k_limit) { P1.k_limit = a->row_limit; P1.k_base = lo; }
           rc = tc::launch_tc_gemm(&As1, &Bs1, &P1, 1, gdt, sched + 2 * L.nchunks + 2 + sl, st);
         }
         if (!rc) {

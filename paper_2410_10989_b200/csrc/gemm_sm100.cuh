@@ -60,6 +60,15 @@ struct Problem {
   int kb_term;
   unsigned char pa[8], pb[8];
   EpiArgs epi;
+  // Device-side row limit (the kept-row FLCE without a host read; CTA-pair kernel only):
+  // m_limit != NULL -> only the first max(*m_limit - m_base, 0) rows of M are computed (M tiles
+  // past them are skipped); k_limit != NULL -> the K loop stops after max(*k_limit, 1) - k_base
+  // rows (K is the row dimension of the dW GEMM).  Rows past the limit hold zeros in the
+  // operands, so a limit only removes work.
+  const int64_t* m_limit;
+  int64_t m_base;
+  const int64_t* k_limit;
+  int64_t k_base;
 };
 
 struct Args {

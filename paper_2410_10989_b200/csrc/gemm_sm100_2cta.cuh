@@ -130,11 +130,45 @@ __device__ __forceinline__ void umma2_commit_mc(uint32_t bar, uint16_t mask) {
 struct PairTile {
   int p, m_blk, n_blk;
 };
-__device__ __forceinline__ PairTile decode_pair(const Args& a, int t) {
+// The launch's effective tile counts and K lengths: Problem::m_limit / k_limit read once per
+// thread at kernel start (every role computes the same values).
+struct Eff {
+  int tiles0, total;
+  int tm[2], kb[2];
+};
+__device__ __forceinline__ Eff effective(const Args& a) {
+  Eff e;
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const Problem& P = a.prob[p];
+    int tm = P.tiles_m, kb = P.k_blocks;
+    if (p < a.n_problems) {
+      if (P.m_limit) {
+        int64_t lim = *P.m_limit - P.m_base;
+        lim = lim < 0 ? 0 : (lim > P.M ? P.M : lim);
+        tm = (int)((lim + PBM - 1) / PBM);
+      }
+      if (P.k_limit) {
+        int64_t lim = *P.k_limit;
+        lim = (lim < 1 ? 1 : lim) - P.k_base;
+        lim = lim < 0 ? 0 : (lim > P.K ? P.K : lim);
+        kb = (int)((lim + BK - 1) / BK);
+        if (kb == 0) tm = 0;  // nothing to add (the host never limits a storing pass to zero)
+      }
+    }
+    e.tm[p] = tm;
+    e.kb[p] = kb;
+  }
+  e.tiles0 = e.tm[0] * a.prob[0].tiles_n;
+  e.total = e.tiles0 + (a.n_problems > 1 ? e.tm[1] * a.prob[1].tiles_n : 0);
+  return e;
+}
+
+__device__ __forceinline__ PairTile decode_pair(const Args& a, const Eff& e, int t) {
   PairTile c;
-  c.p = (t >= a.tiles0) ? 1 : 0;
-  const int lt = c.p ? t - a.tiles0 : t;
-  const int tm = c.p ? a.prob[1].tiles_m : a.prob[0].tiles_m;
+  c.p = (t >= e.tiles0) ? 1 : 0;
+  const int lt = c.p ? t - e.tiles0 : t;
+  const int tm = e.tm[c.p];
   const int tn = c.p ? a.prob[1].tiles_n : a.prob[0].tiles_n;
   const int nf = c.p ? a.prob[1].n_fast : a.prob[0].n_fast;
   if (nf) { c.n_blk = lt % tn; c.m_blk = lt / tn; }
@@ -164,6 +198,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
   uint64_t* sempty = sfull + SCHED;
   int* stile = reinterpret_cast<int*>(sempty + SCHED);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(stile + SCHED);
+  const Eff eff = effective(args);  // device row limits (Problem::m_limit / k_limit)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -207,7 +242,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
         if (leader) {
           mbar_wait(&sempty[slot], sp ^ 1);
           tile = atomicAdd(args.counter, 1);
-          if (tile >= args.total_tiles) tile = -1;
+          if (tile >= eff.total) tile = -1;
           stile[slot] = tile;
           st_cluster_u32(peer_stile0 + 4 * slot, (uint32_t)tile);
           mbar_arrive(&sfull[slot]);
@@ -220,11 +255,11 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
       }
       tile = __shfl_sync(0xffffffffu, tile, 0);
       if (tile < 0) break;
-      const PairTile pt = decode_pair(args, tile);
+      const PairTile pt = decode_pair(args, eff, tile);
       const int p = pt.p;
       const int a_mode = p ? args.prob[1].a_mode : args.prob[0].a_mode;
       const int b_mode = p ? args.prob[1].b_mode : args.prob[0].b_mode;
-      const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
+      const int kblocks = eff.kb[p];
       const uint64_t ma = reinterpret_cast<uint64_t>(p ? &ma1 : &ma0);
       const uint64_t mb = reinterpret_cast<uint64_t>(p ? &mb1 : &mb0);
       const int m0 = pt.m_blk * PBM + (int)rank * HALF;
@@ -295,11 +330,11 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
         __syncwarp();
         if (lane == 0) mbar_arrive(&sempty[slot]);
         if (tile < 0) break;
-        const int p = tile >= args.tiles0 ? 1 : 0;
+        const int p = tile >= eff.tiles0 ? 1 : 0;
         const int a_mn = tc::mode_mn(p ? args.prob[1].a_mode : args.prob[0].a_mode);
         const int b_mn = tc::mode_mn(p ? args.prob[1].b_mode : args.prob[0].b_mode);
-        const int kblocks = p ? args.prob[1].k_blocks : args.prob[0].k_blocks;
-        const int seg_kb = tc::seg_len(args.prob[p]);
+        const int kblocks = eff.kb[p];
+        const int seg_kb = args.prob[p].seg_kb > 0 ? args.prob[p].seg_kb : kblocks;
         const uint32_t idesc = p ? args.idesc[1] : args.idesc[0];
         const uint64_t a_desc0 = tc::make_desc(sA0, a_mn ? 8192u : 16u, 1024u);
         const uint64_t b_desc0 = tc::make_desc(sB0, b_mn ? 8192u : 16u, 1024u);
@@ -352,7 +387,7 @@ gemm2_kernel(const __grid_constant__ CUtensorMap ma0, const __grid_constant__ CU
         else mbar_arrive_cluster(leader_sempty0 + 8 * slot);
       }
       if (tile < 0) break;
-      const PairTile pt = decode_pair(args, tile);
+      const PairTile pt = decode_pair(args, eff, tile);
       const Problem& P = args.prob[pt.p];
       const uint64_t omap = reinterpret_cast<uint64_t>(pt.p ? &mc1 : &mc0);
       const int row0 = pt.m_blk * PBM + (int)rank * HALF + q * 32;

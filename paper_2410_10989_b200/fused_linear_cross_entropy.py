@@ -54,6 +54,10 @@ def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=Non
 # ignored -- below that the GEMM tiles (256 rows per CTA pair) barely shrink.
 SKIP_IGNORED_ROWS = True
 COMPACT_MIN_SKIPPED = 128
+# Kept-row count without a host read: the FLCE runs on all bt row slots, the kept rows first,
+# and the CTA-pair GEMMs read the count on the device (lk_flce_args.row_limit) to skip the M
+# tiles and dW K blocks past it.  Always used under CUDA graph capture; in eager mode when True.
+KEPT_ROWS_DEVICE_COUNT = False
 
 
 def _gather_rows(src: torch.Tensor, index: torch.Tensor, out_rows: int, dst: torch.Tensor, fill_bits: int = 0):
@@ -155,17 +159,24 @@ def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, retur
     None (caller runs the full problem) when too few rows are ignored."""
     bt, h = x.shape
     dev = x.device
-    kr = kept_rows(t, ignore_index)
-    if kr is None:
-        return None
-    index, pos, n = kr
+    limit = None
+    if KEPT_ROWS_DEVICE_COUNT or torch.cuda.is_current_stream_capturing():
+        # no host read: all bt row slots, kept rows first, ignored slots after (X rows 0,
+        # targets ignore_index); the GEMMs skip the work past the device count
+        index, pos, limit = _compact(t, ignore_index)
+        n = bt
+    else:
+        kr = kept_rows(t, ignore_index)
+        if kr is None:
+            return None
+        index, pos, n = kr
     # the kept targets are gathered here (8 bytes a row); the kept X rows are gathered by the
     # library one chunk at a time into its workspace (lk_flce_args.x_row_index), so no
     # n x H copy of X is ever held
-    tk = _gather_rows(t, index, n, torch.empty(n, dtype=torch.int64, device=dev))
+    tk = _gather_rows(t, index, n, torch.empty(n, dtype=torch.int64, device=dev), int(ignore_index) & ((1 << 64) - 1))
     loss, z_loss, acc, pred, gxk, gw, gb = fused_linear_cross_entropy_forward(
         x, w, tk, compute_grad_input=need_gx, compute_grad_weight=need_gw, skip_ignored_rows=False,
-        _x_row_index=index, **kw)
+        _x_row_index=index, _row_limit=limit, **kw)
     del tk
     gx = _gather_rows(gxk, pos, bt, torch.empty_like(x)) if gxk is not None else None
     if reduction == "none":  # per-row outputs back to every row (ignored: 0)
@@ -208,6 +219,7 @@ def fused_linear_cross_entropy_forward(
     grad_w_out: Optional[torch.Tensor] = None,
     skip_ignored_rows: Optional[bool] = None,
     _x_row_index: Optional[torch.Tensor] = None,
+    _row_limit: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, z_loss, token_accuracy, predicted_tokens, grad_input, grad_weight, grad_bias).
 
@@ -263,8 +275,7 @@ def fused_linear_cross_entropy_forward(
     need_gx = _input.requires_grad if compute_grad_input is None else compute_grad_input
     need_gw = (need_gx and weight.requires_grad) if compute_grad_weight is None else compute_grad_weight
     dev = x.device
-    if (SKIP_IGNORED_ROWS if skip_ignored_rows is None else skip_ignored_rows) and bt >= COMPACT_MIN_SKIPPED \
-            and not torch.cuda.is_current_stream_capturing():
+    if (SKIP_IGNORED_ROWS if skip_ignored_rows is None else skip_ignored_rows) and bt >= COMPACT_MIN_SKIPPED:
         kept = _forward_kept_rows(
             x, w, t, ignore_index, need_gx, need_gw, reduction, return_z_loss, return_token_accuracy,
             return_predicted_tokens,
@@ -313,7 +324,7 @@ def fused_linear_cross_entropy_forward(
         raise errors.UnsupportedOption(f"accum_dtype {accum_dtype}: use None, torch.float32 or the weight dtype")
     args = _capi.FlceArgs(
         x=ptr(x), weight=ptr(w), target=ptr(t), bias=ptr(b), bt=bt, hidden=h, vocab=v, dtype=dt,
-        x_row_index=ptr(_x_row_index),
+        x_row_index=ptr(_x_row_index), row_limit=ptr(_row_limit),
         ignore_index=int(ignore_index), label_smoothing=float(label_smoothing),
         lse_square_scale=float(lse_square_scale), softcap=float(softcap) if softcap is not None else 0.0,
         reduction=_capi.REDUCTIONS[reduction], chunk_rows=cr, loss_rows=ptr(loss_rows), loss_sum=ptr(loss_sum),

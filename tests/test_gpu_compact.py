@@ -86,9 +86,13 @@ CASES = [dict(), dict(reduction="sum"), dict(reduction="none"), dict(lse_square_
          dict(_no_grad_x=True), dict(_no_grad_x=True, _bias=True)]
 
 
+@pytest.mark.parametrize("device_count", [False, True], ids=["host_count", "device_count"])
 @pytest.mark.parametrize("kw", CASES, ids=lambda k: "-".join(f"{a}" for a in k) or "default")
-def test_flce_skip_ignored_rows_vs_full_call_and_oracle(kw, monkeypatch):
+def test_flce_skip_ignored_rows_vs_full_call_and_oracle(kw, device_count, monkeypatch):
+    """device_count: the kept-row count stays on the device (KEPT_ROWS_DEVICE_COUNT, the CUDA
+    graph path): all row slots run, and the CTA-pair GEMMs skip the work past the count."""
     monkeypatch.setattr(flce_mod, "COMPACT_MIN_SKIPPED", 1)
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", device_count)
     kw = dict(kw)
     dtype = kw.pop("_dtype", torch.bfloat16)
     frac = kw.pop("_frac", 0.3)
@@ -177,3 +181,22 @@ def test_prepared_kept_rows_match_and_are_consumed():
     b = flce_mod.fused_linear_cross_entropy_forward(x, w, t2, **kw)
     assert a[0].item() == b[0].item() and torch.equal(a[4], b[4]) and torch.equal(a[5], b[5])
     flce_mod._PREPARED.clear()
+
+
+@pytest.mark.parametrize("shape", [(8192, 512, 8192, 0.1), (3000, 256, 5000, 0.6), (700, 256, 3000, 1.0)])
+def test_device_count_matches_host_count(shape, monkeypatch):
+    """The device-count kept-row FLCE against the host-count one: loss and gradients within the
+    bf16 tolerance (chunk grouping differs), ignored rows exact, bitwise repeatable."""
+    bt, h, v, frac = shape
+    x, w, t = _problem(bt, h, v, frac, torch.bfloat16, seed=bt)
+    kw = dict(compute_grad_input=True, compute_grad_weight=True, chunk_rows=1024)
+    monkeypatch.setattr(flce_mod, "COMPACT_MIN_SKIPPED", 1)
+    host = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", True)
+    dev = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    dev2 = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    assert dev[0].item() == dev2[0].item() and torch.equal(dev[4], dev2[4]) and torch.equal(dev[5], dev2[5])
+    ign = t == -100
+    assert torch.all(dev[4][ign] == 0)
+    for a, b in ((dev[0], host[0]), (dev[4], host[4]), (dev[5], host[5])):
+        assert rel_close(a.double().cpu().numpy(), b.double().cpu().numpy(), 2e-2)[0]

@@ -487,12 +487,13 @@ def test_fp16_tcgen05_path_vs_oracle(kw):
 
 def test_flce_in_cuda_graph(monkeypatch):
     """No host syncs on the FLCE path: forward + backward capture into a CUDA graph and replay
-    to the same bits as eager (counts and the MEAN scale stay on the device).  Ignored-row
-    skipping needs a host read of the kept-row count, so it is off under capture; the eager
-    reference here runs with it off too (with it on, eager matches to tolerance below)."""
+    to the same bits as eager (counts and the MEAN scale stay on the device).  Under capture
+    the ignored rows are skipped with the kept-row count kept on the device
+    (KEPT_ROWS_DEVICE_COUNT), so the eager reference runs that mode too; the host-count mode
+    matches it to tolerance below."""
     import paper_2410_10989_b200.fused_linear_cross_entropy as flce_mod
 
-    monkeypatch.setattr(flce_mod, "SKIP_IGNORED_ROWS", False)
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", True)
     bt, h, v = 1024, 1024, 16384
     g = torch.Generator(device="cuda").manual_seed(5)
     x = ((torch.rand(bt, h, device="cuda", generator=g) * 2 - 1)).to(torch.bfloat16)
@@ -520,8 +521,8 @@ def test_flce_in_cuda_graph(monkeypatch):
     graph.replay()
     torch.cuda.synchronize()
     assert all(torch.equal(a, b) for a, b in zip(eager, out))
-    monkeypatch.setattr(flce_mod, "SKIP_IGNORED_ROWS", True)
-    skipped = step()  # 147 of 1024 rows ignored: the kept-row path
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", False)
+    skipped = step()  # 147 of 1024 rows ignored: the host-count kept-row path
     assert abs(skipped[0].item() - eager[0].item()) <= 1e-3 * abs(eager[0].item())
     assert torch.equal(skipped[1][t == -100], torch.zeros_like(skipped[1][t == -100]))
     assert close(skipped[1], eager[1], 1e-2) and close(skipped[2], eager[2], 2e-2)
