@@ -1,13 +1,14 @@
 // Row compaction around the FLCE: the rows whose target is ignore_index contribute nothing
 // (loss 0, gradient row 0, no dW/db term -- rowfuse/ops.py:515-523, flce.py:161-168), so the
-// host wrapper (fused_linear_cross_entropy.py) gathers the other rows to the front, runs the
-// chunk loop on them alone, and scatters the per-row outputs back.  10% ignored targets
-// (BASELINE cfg2) is 10% of the step's GEMM work not done.
+// host wrapper (fused_linear_cross_entropy.py) runs the chunk loop on the other rows alone and
+// scatters the per-row outputs back.  10% ignored targets is 10% of the
+// step's GEMM work not done.
 //
 //   lk_compact_rows : stable compaction map of one target vector (one CTA, block scans);
-//   lk_gather_rows  : dst[i, :] = index[i] >= 0 ? src[index[i], :] : fill -- both the gather
-//                     (index = compacted row list) and the scatter back (index = inverse map,
-//                     -1 for ignored rows), 16-byte vectors, one warp per wide row.
+//   lk_gather_rows  : dst[i, :] = index[i] >= 0 ? src[index[i], :] : fill -- the targets'
+//                     gather, the per-chunk X gather inside the FLCE (launch_gather_rows,
+//                     lk_flce_args.x_row_index), and the scatter back (index = inverse map, -1
+//                     for ignored rows); 16-byte vectors, one warp per wide row.
 #include "common.cuh"
 
 namespace lk {
