@@ -517,12 +517,15 @@ def run_ours(args):
     skipping = (flce_mod.SKIP_IGNORED_ROWS and n_ignored > 0
                 and n_ignored >= max(flce_mod.COMPACT_MIN_SKIPPED, bt // 64))
     flop_exec = 6.0 * (bt - n_ignored) * h * v / (world if vocab_mode else 1) if skipping else flop_step
+    # the rows the kept-row call plans its chunks for: all row slots with the device count (the
+    # default), the kept rows with the host count
+    plan_rows = bt - n_ignored if (skipping and not flce_mod.KEPT_ROWS_DEVICE_COUNT) else bt
     if skipping and not args.chunk_rows and not vocab_mode:
-        chunk = flce_plan(bt - n_ignored, h, v)[0]  # the plan the kept-row call runs
+        chunk = flce_plan(plan_rows, h, v)[0]
     if skipping:
-        ws_bytes = flce_workspace_bytes(bt - n_ignored, h, v, torch.bfloat16, chunk, True)
+        ws_bytes = flce_workspace_bytes(plan_rows, h, v, torch.bfloat16, chunk, True)
         logits_chunk_bytes = chunk * (-(-v // 64) * 64) * 2
-    n_chunks = -(-(bt - n_ignored if skipping else bt) // chunk)
+    n_chunks = -(-plan_rows // chunk)
 
     # ---- variant: fp32 dW accumulator (accum_dtype=torch.float32), untimed peak + timed steps ----
     variants = None

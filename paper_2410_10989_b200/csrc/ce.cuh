@@ -57,6 +57,11 @@ struct CeRowArgs {
   // smooth term eps sum_c w_c (lse - z_c); the statistics pass then sums z_c w_c, and the
   // gradient gains a per-column -eps w_c term (ce_rows_kernel only).
   const float* weight_total;      // device scalar sum_c w[c]
+  // Device row limit of the kept-row FLCE (lk_flce_args.row_limit): the gradient rows of ignored
+  // rows at or past round_up(max(*zero_limit, 1), 256) - zero_base are never read (the GEMMs
+  // stop at that tile), so the ring kernel skips their zero writes.  null = write every row.
+  const int64_t* zero_limit;
+  int64_t zero_base;
 };
 
 // Per-row loss and gradient coefficients: grad = p * pc + ceps - [col == y] * chit (then the

@@ -121,6 +121,11 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
   const int npc32 = (int)npc;
   const int tail_nvec = (int)((row_bytes - (npc - 1) * (int64_t)PIECE) / 16);
   const int v0 = warp * VPW + lane;
+  int64_t zero_end = INT64_MAX;  // local rows at or past it: ignored-row zero writes skipped
+  if (a.zero_limit) {
+    const int64_t lim = *a.zero_limit < 1 ? 1 : *a.zero_limit;
+    zero_end = (lim + 255) / 256 * 256 - a.zero_base;
+  }
   // class weights with label smoothing: the smoothing sum is sum_c w_c z_c and the gradient
   // gains -eps w_c per column (weights by global column; runtime-uniform branch)
   const float* wcol = W ? a.class_weight + a.col_offset : nullptr;
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(THREADS, 1) ce_ring_kernel(CeRowArgs a, int st
     T* xr = static_cast<T*>(a.x) + row * a.ld;
     const int64_t y = a.target[row];
     if (y == a.ignore_index) {
-      if (a.compute_grad)
+      if (a.compute_grad && row < zero_end)
         for (int64_t v = tid; v < n / NV; v += NC * 32) ring::stg128(xr + v * NV, make_uint4(0, 0, 0, 0));
       if (tid == 0) {
         if (a.loss_rows) a.loss_rows[row] = 0.f;

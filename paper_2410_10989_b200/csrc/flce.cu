@@ -545,6 +545,14 @@ extern "C" int lk_flce_forward_backward(const lk_flce_args* a) {
                           : a->mean_weight_sum ? a->mean_weight_sum : reinterpret_cast<const float*>(counts + 2);
     ce.weight_total = wls ? reinterpret_cast<const float*>(counts + 3) : nullptr;
     ce.pred_rows = a->predicted_tokens ? a->predicted_tokens + lo : nullptr;
+    // unread rows only when every reader stops at the limit: the tcgen05 dX GEMM (M tiles), the
+    // dW GEMM (K loop: not in a last chunk that folds the fp32 accumulator, which reads every
+    // row) and no bias column sum (reads every row)
+    // (and only on the CTA-pair GEMM: the single-CTA test path ignores limits)
+    if (a->row_limit && tc && tc::default_cta_group() == 2 && !a->grad_bias && !(a->grad_w && last && L.need_acc)) {
+      ce.zero_limit = a->row_limit;
+      ce.zero_base = lo;
+    }
     if (tc || tc32) { ce.partials = parts; ce.n_parts = L.nparts; ce.tgt_logit = tgt; }
     {
       ProfScope ps(1, st);

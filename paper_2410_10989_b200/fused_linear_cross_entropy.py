@@ -56,8 +56,11 @@ SKIP_IGNORED_ROWS = True
 COMPACT_MIN_SKIPPED = 128
 # Kept-row count without a host read: the FLCE runs on all bt row slots, the kept rows first,
 # and the CTA-pair GEMMs read the count on the device (lk_flce_args.row_limit) to skip the M
-# tiles and dW K blocks past it.  Always used under CUDA graph capture; in eager mode when True.
-KEPT_ROWS_DEVICE_COUNT = False
+# tiles and dW K blocks past it -- no host synchronisation anywhere on the call.  Always used
+# under CUDA graph capture.  False: the count is read on the host (the chunk plan is then
+# sized for the kept rows, and nothing runs when too few rows are ignored); measured equal
+# speed at cfg2 (profiles/r02/kept_count_probe*.log).
+KEPT_ROWS_DEVICE_COUNT = True
 
 
 def _gather_rows(src: torch.Tensor, index: torch.Tensor, out_rows: int, dst: torch.Tensor, fill_bits: int = 0):
@@ -72,10 +75,11 @@ class KeptRows:
     (`prepare_kept_rows`): the kept-row list, the inverse map, and the kept count copied to
     pinned host memory behind an event."""
 
-    def __init__(self, target, index, pos, count_host, event):
+    def __init__(self, target, index, pos, count, count_host, event):
         # the target tensor itself is held: while the entry exists no other tensor can occupy
         # its memory, so (data pointer, version) identifies it
-        self.target, self.index, self.pos, self.count_host, self.event = target, index, pos, count_host, event
+        self.target, self.index, self.pos, self.count = target, index, pos, count
+        self.count_host, self.event = count_host, event
         self.rows = target.numel()
 
     @property
@@ -106,8 +110,9 @@ def prepare_kept_rows(target: torch.Tensor, ignore_index: int = -100,
     must be ordered before it).  A later FLCE call on the same, unmodified target tensor (same
     storage, same version) then sizes its chunk loop from a count the GPU produced long
     before, instead of waiting for all work queued ahead of it.  That call waits on the
-    compaction's event before enqueuing anything that reads its output, so `stream` need not
-    be ordered with the call's stream."""
+    compaction's event before enqueuing anything that reads its output (host count: on the
+    host; device count, the default: on its stream), so `stream` need not be ordered with the
+    call's stream, and the call skips its own compaction."""
     t = as_targets(target)
     if not t.is_cuda or t.numel() < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
         return None
@@ -117,10 +122,23 @@ def prepare_kept_rows(target: torch.Tensor, ignore_index: int = -100,
         host.copy_(count, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record()
-    kr = KeptRows(t, index, pos, host, ev)
+    kr = KeptRows(t, index, pos, count, host, ev)
     while len(_PREPARED) >= _PREPARED_MAX:
         _PREPARED.pop(next(iter(_PREPARED)))
     _PREPARED[(t.data_ptr(), t.numel(), int(ignore_index), t.device)] = (t._version, kr)
+    return kr
+
+
+def _take_prepared(t: torch.Tensor, ignore_index: int) -> Optional[KeptRows]:
+    """The prepare_kept_rows entry for this exact target tensor (consumed), or None."""
+    entry = _PREPARED.pop((t.data_ptr(), t.numel(), int(ignore_index), t.device), None)
+    if entry is None or entry[0] != t._version or entry[1].rows != t.numel() \
+            or entry[1].target.data_ptr() != t.data_ptr():
+        return None
+    kr = entry[1]
+    cur = torch.cuda.current_stream(t.device)
+    for buf in (kr.index, kr.pos, kr.count):  # made on the preparing stream, read on this one
+        buf.record_stream(cur)
     return kr
 
 
@@ -133,12 +151,8 @@ def kept_rows(t: torch.Tensor, ignore_index: int):
     bt = t.numel()
     if bt < COMPACT_MIN_SKIPPED or torch.cuda.is_current_stream_capturing():
         return None
-    entry = _PREPARED.pop((t.data_ptr(), bt, int(ignore_index), t.device), None)
-    if entry is not None and entry[0] == t._version and entry[1].rows == bt and entry[1].target.data_ptr() == t.data_ptr():
-        kr = entry[1]
-        cur = torch.cuda.current_stream(t.device)
-        kr.index.record_stream(cur)
-        kr.pos.record_stream(cur)
+    kr = _take_prepared(t, ignore_index)
+    if kr is not None:
         index, pos, n = kr.index, kr.pos, kr.n
     else:
         index, pos, count = _compact(t, ignore_index)
@@ -163,7 +177,13 @@ def _forward_kept_rows(x, w, t, ignore_index, need_gx, need_gw, reduction, retur
     if KEPT_ROWS_DEVICE_COUNT or torch.cuda.is_current_stream_capturing():
         # no host read: all bt row slots, kept rows first, ignored slots after (X rows 0,
         # targets ignore_index); the GEMMs skip the work past the device count
-        index, pos, limit = _compact(t, ignore_index)
+        kr = _take_prepared(t, ignore_index) if not torch.cuda.is_current_stream_capturing() else None
+        if kr is not None:
+            # the prepared compaction ran on another stream: order it before this one's readers
+            kr.event.wait(torch.cuda.current_stream(dev))
+            index, pos, limit = kr.index, kr.pos, kr.count
+        else:
+            index, pos, limit = _compact(t, ignore_index)
         n = bt
     else:
         kr = kept_rows(t, ignore_index)

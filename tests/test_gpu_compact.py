@@ -153,12 +153,14 @@ def test_skip_ignored_rows_is_bitwise_repeatable():
         assert a[0].item() == b[0].item() and torch.equal(a[4], b[4]) and torch.equal(a[5], b[5])
 
 
-def test_prepared_kept_rows_match_and_are_consumed():
+@pytest.mark.parametrize("device_count", [True, False], ids=["device_count", "host_count"])
+def test_prepared_kept_rows_match_and_are_consumed(device_count, monkeypatch):
     """lk.prepare_kept_rows on a side stream ahead of the call: the same result bit for bit as
     the call that compacts by itself; the entry is consumed; an in-place change to the targets
     after preparing (a new tensor version) falls back to a fresh compaction."""
     import paper_2410_10989_b200 as lk
 
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", device_count)
     flce_mod._PREPARED.clear()
     x, w, t = _problem(4096, 256, 5000, 0.25, torch.bfloat16, seed=9)
     kw = dict(compute_grad_input=True, compute_grad_weight=True)
@@ -191,6 +193,7 @@ def test_device_count_matches_host_count(shape, monkeypatch):
     x, w, t = _problem(bt, h, v, frac, torch.bfloat16, seed=bt)
     kw = dict(compute_grad_input=True, compute_grad_weight=True, chunk_rows=1024)
     monkeypatch.setattr(flce_mod, "COMPACT_MIN_SKIPPED", 1)
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", False)
     host = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
     monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", True)
     dev = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
@@ -200,3 +203,36 @@ def test_device_count_matches_host_count(shape, monkeypatch):
     assert torch.all(dev[4][ign] == 0)
     for a, b in ((dev[0], host[0]), (dev[4], host[4]), (dev[5], host[5])):
         assert rel_close(a.double().cpu().numpy(), b.double().cpu().numpy(), 2e-2)[0]
+
+
+@pytest.mark.parametrize("case", ["cta1", "fp32_accumulator_fold", "grad_w_slices", "bias"])
+def test_device_count_special_paths_vs_oracle(case, path_knob, monkeypatch):
+    """Device-count kept rows where the unread-row shortcuts must stay off or stay safe: the
+    single-CTA GEMM (ignores limits), a last chunk that folds the fp32 dW accumulator (reads every
+    row), grad_w in vocab-row slices with events, and a bias gradient (column sum over all rows)."""
+    monkeypatch.setattr(flce_mod, "KEPT_ROWS_DEVICE_COUNT", True)
+    monkeypatch.setattr(flce_mod, "COMPACT_MIN_SKIPPED", 1)
+    bt, h, v = 3000, 256, 4000
+    x, w, t = _problem(bt, h, v, 0.35, torch.bfloat16, seed=77)
+    kw = dict(compute_grad_input=True, compute_grad_weight=True, chunk_rows=1024)
+    b = None
+    if case == "cta1":
+        path_knob(_capi.PATH_CTA_GROUP, 1)
+    elif case == "fp32_accumulator_fold":
+        kw["chunk_rows"] = 256  # 12 chunks > 8: fp32 accumulator, last chunk folds it into grad_w
+    elif case == "grad_w_slices":
+        kw["grad_w_slice_events"] = [torch.cuda.Event() for _ in range(4)]
+    else:
+        b = (torch.rand(v, device="cuda") * 0.2).to(torch.bfloat16)
+        kw["bias"] = b
+    out = flce_mod.fused_linear_cross_entropy_forward(x, w, t, **kw)
+    torch.cuda.synchronize()
+    rl, _, _, rgx, rgw, rgb = liger_ref.flce(x.double().cpu().numpy(), w.double().cpu().numpy(), t.cpu().numpy(),
+                                             bias=None if b is None else b.double().cpu().numpy())
+    assert rel_close(float(out[0].item()), rl, 2e-2)[0]
+    assert rel_close(out[4].double().cpu().numpy(), rgx, 2e-2)[0]
+    assert rel_close(out[5].double().cpu().numpy(), rgw, 2e-2)[0]
+    assert torch.all(out[4][t == -100] == 0)
+    assert torch.isfinite(out[5]).all()
+    if b is not None:
+        assert rel_close(out[6].double().cpu().numpy(), rgb, 2e-2)[0]

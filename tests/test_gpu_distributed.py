@@ -137,7 +137,7 @@ def test_vocab_parallel_cuda_world2(kw):
     _run("vocab", kw)
 
 
-def _sync_free_worker(rank, port, mode, out):
+def _sync_free_worker(rank, port, mode, out, skip=False):
     """One-rank NCCL group: the sharded call must enqueue every kernel and collective without a
     device->host sync (the dW all-reduce overlap was defeated by an .item())."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -156,7 +156,8 @@ def _sync_free_worker(rank, port, mode, out):
 
         def call():
             if mode == "token":
-                return token_sharded_flce(xb, wb, tb, chunk_rows=256, check_targets=False, skip_ignored_rows=False)
+                # skip=True: the kept-row path with the count on the device (the default mode)
+                return token_sharded_flce(xb, wb, tb, chunk_rows=256, check_targets=False, skip_ignored_rows=skip)
             return vocab_parallel_flce(xb, wb, tb, sh, chunk_rows=256, check_targets=False, skip_ignored_rows=False)
 
         ref = call()  # warm (workspace allocation, tensor-map encode, NCCL communicator)
@@ -175,9 +176,9 @@ def _sync_free_worker(rank, port, mode, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["token", "vocab"])
-def test_sharded_calls_have_no_host_sync(mode):
+@pytest.mark.parametrize("mode,skip", [("token", False), ("vocab", False), ("token", True)])
+def test_sharded_calls_have_no_host_sync(mode, skip):
     ctx = mp.get_context("spawn")
     out = ctx.Manager().dict()
-    mp.spawn(_sync_free_worker, args=(_port(), mode, out), nprocs=1, join=True)
+    mp.spawn(_sync_free_worker, args=(_port(), mode, out, skip), nprocs=1, join=True)
     assert dict(out) == {0: "ok"}, dict(out)
