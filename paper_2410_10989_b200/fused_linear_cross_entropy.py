@@ -49,9 +49,10 @@ def flce_workspace_bytes(bt, hidden, vocab, dtype=torch.bfloat16, chunk_rows=Non
                                                 int(accum)))
 
 
-# Ignored-row skipping (lk_compact_rows / lk_gather_rows, csrc/compact.cu).  On by default; a
-# call skips rows only when at least COMPACT_MIN_SKIPPED rows (and 1/64 of the batch) are
-# ignored -- below that the GEMM tiles (256 rows per CTA pair) barely shrink.
+# Ignored-row skipping (lk_compact_rows / lk_gather_rows, csrc/compact.cu).  On by default for
+# calls of at least COMPACT_MIN_SKIPPED rows.  With the host count (KEPT_ROWS_DEVICE_COUNT =
+# False) a call skips rows only when at least COMPACT_MIN_SKIPPED rows (and 1/64 of the batch)
+# are ignored -- below that the GEMM tiles (256 rows per CTA pair) barely shrink.
 SKIP_IGNORED_ROWS = True
 COMPACT_MIN_SKIPPED = 128
 # Kept-row count without a host read: the FLCE runs on all bt row slots, the kept rows first,
