@@ -432,7 +432,7 @@ def run_ours(args):
         # launched) is done once, untimed, by the checked call after the loop
         if vocab_mode:
             out = vocab_parallel_flce(x, w, t, shard, chunk_rows=chunk, accum_dtype=accum_dtype,
-                                      check_targets=check, skip_ignored_rows=skip, **opts)
+                                      check_targets=check, skip_ignored_rows=skip, comm=args.comm, **opts)
         elif world > 1:
             out = token_sharded_flce(x, w, t, chunk_rows=call_chunk, accum_dtype=accum_dtype,
                                      check_targets=check, comm=args.comm, skip_ignored_rows=skip, **opts)
@@ -596,7 +596,8 @@ def run_ours(args):
         xd = xd.detach().requires_grad_(True)
         state["i"] = i + 1
         if vocab_mode:
-            loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, **opts)
+            loss, gx, gw = vocab_parallel_flce(xd.detach(), wp.detach(), td, shard, chunk_rows=chunk, comm=args.comm,
+                                               **opts)
         elif world > 1:
             loss, gx, gw = token_sharded_flce(xd, wp, td, chunk_rows=call_chunk, comm=args.comm, **opts)
         else:
@@ -651,9 +652,9 @@ def run_ours(args):
                                 "per chunk: all_gather of row statistics + async dX all-reduce (bf16)" if vocab_mode
                                 else "count all-reduce; dW all-reduce (bf16) overlapped with the last chunk's "
                                      "dW GEMM slices; loss all-reduce"),
-                "grad_w_comm": None if (world == 1 or vocab_mode) else
-                ("NCCL all-reduce per slice" if args.comm == "nccl" else
-                 "peer-memory kernel per slice (csrc/peer.cu: fp32 rank-order sum over IPC-mapped buffers)"),
+                "grad_w_comm": None if world == 1 else
+                (("NCCL" if args.comm == "nccl" else "peer-memory kernel (csrc/peer.cu: fp32 rank-order sum over "
+                  "IPC-mapped buffers)") + (" per chunk, dX partials" if vocab_mode else " per dW slice")),
                 "l2": "inputs larger than L2 (W = 1.05 GB bf16 re-streamed every chunk)",
                 "ignore_index_rows": ("skipped: the chunk loop runs on the kept rows (outputs of ignored rows "
                                       "written as the full call leaves them); each step's kept-row compaction "
@@ -746,7 +747,8 @@ def main():
     ap.add_argument("--mode", choices=["token", "vocab"], default="token",
                     help="multi-GPU shard mode: token-sharded (default) or vocab-parallel (strong)")
     ap.add_argument("--comm", choices=["nccl", "peer"], default="nccl",
-                    help="token mode, N>1: grad_w all-reduce by NCCL or by the peer-memory kernel (csrc/peer.cu)")
+                    help="N>1: the dW (token mode) or dX (vocab mode) all-reduce by NCCL or by the peer-memory "
+                         "kernel (csrc/peer.cu)")
     ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--ref-rows", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -279,6 +279,7 @@ def vocab_parallel_flce(
     dx_reduce_dtype: Optional[torch.dtype] = None,
     check_targets: bool = True,
     skip_ignored_rows: Optional[bool] = None,
+    comm: str = "nccl",
     _x_row_index: Optional[torch.Tensor] = None,
 ):
     """Returns (loss, grad_x (all-reduced, x dtype), local grad_w shard (w dtype)).
@@ -293,7 +294,12 @@ def vocab_parallel_flce(
     With the CUDA ops the ignore_index rows are skipped (`skip_ignored_rows`, default
     SKIP_IGNORED_ROWS): every rank holds the same targets, so every rank compacts the same rows
     and the collectives stay matched; one host read of the kept-row count.
+    `comm="peer"` sums each chunk's dX partial with the peer-memory kernel (csrc/peer.cu) over
+    a symmetric grad_x buffer instead of NCCL (x-dtype reduction only); the returned grad_x is
+    then a view of that buffer, overwritten by the next call of the same shape.
     """
+    if comm not in ("nccl", "peer"):
+        raise ValueError(f"comm must be 'nccl' or 'peer'. Got: {comm}")
     from . import fused_linear_cross_entropy as flce_mod
 
     skip = flce_mod.SKIP_IGNORED_ROWS if skip_ignored_rows is None else skip_ignored_rows
@@ -309,7 +315,7 @@ def vocab_parallel_flce(
                 x.contiguous(), w_shard, tk, shard, group=group, ignore_index=ignore_index,
                 label_smoothing=label_smoothing, lse_square_scale=lse_square_scale, softcap=softcap,
                 reduction=reduction, chunk_rows=chunk_rows, accum_dtype=accum_dtype, dx_reduce_dtype=dx_reduce_dtype,
-                check_targets=check_targets, skip_ignored_rows=False, _x_row_index=index)
+                check_targets=check_targets, skip_ignored_rows=False, comm=comm, _x_row_index=index)
             gx = flce_mod._gather_rows(gxk, pos, bt_all, torch.empty(bt_all, h, dtype=x.dtype, device=x.device))
             if reduction == "none":
                 loss = flce_mod._gather_rows(loss, pos, bt_all,
@@ -329,11 +335,20 @@ def vocab_parallel_flce(
     else:
         acc_dtype = torch.float32
     gw_acc = torch.zeros(shard.size, h, dtype=acc_dtype, device=x.device)
-    gx = torch.empty(bt, h, dtype=x.dtype, device=x.device)
+    dx_dt = dx_reduce_dtype or x.dtype
+    peer = None
+    if comm == "peer" and isinstance(ops, CudaVocabOps) and dx_dt == x.dtype:
+        from .peer import buffer_for
+
+        # sized for all of x's rows (the kept-row call uses a prefix): one buffer per batch shape
+        peer = buffer_for(x.shape[0] * h * x.element_size(), x.device, group, "vp_grad_x")
+        gx = peer.tensor((bt, h), x.dtype)
+        comm_stream = _comm_stream(x.device)
+    else:
+        gx = torch.empty(bt, h, dtype=x.dtype, device=x.device)
     loss_rows = torch.empty(bt, dtype=torch.float32, device=x.device)
     kw = dict(ignore_index=ignore_index, label_smoothing=label_smoothing, lse_square_scale=lse_square_scale,
               softcap=softcap, reduction=reduction)
-    dx_dt = dx_reduce_dtype or x.dtype
     pending = []  # (work, lo, hi, partial) of in-flight dX reductions
     for ci, lo in enumerate(range(0, bt, chunk_rows)):
         hi = min(lo + chunk_rows, bt)
@@ -347,8 +362,14 @@ def vocab_parallel_flce(
         stats_g = combine_row_stats(stats, ops, group)
         gx_out = gx[lo:hi] if dx_dt == x.dtype else torch.empty(hi - lo, h, dtype=dx_dt, device=x.device)
         lr, gxp = ops.backward(xc, w_shard, tc, shard, stats_g, buf, n_valid, gw_acc, ci > 0, gx_out=gx_out, **kw)
-        pending.append((dist.all_reduce(gxp, op=dist.ReduceOp.SUM, group=group, async_op=True), lo, hi, gxp))
+        if peer is not None:  # this chunk's dX rows summed over peer memory on the side stream
+            comm_stream.wait_stream(torch.cuda.current_stream(x.device))
+            peer.all_reduce_(gx, lo * h, hi * h, stream=comm_stream)
+        else:
+            pending.append((dist.all_reduce(gxp, op=dist.ReduceOp.SUM, group=group, async_op=True), lo, hi, gxp))
         loss_rows[lo:hi] = lr
+    if peer is not None:
+        torch.cuda.current_stream(x.device).wait_stream(comm_stream)
     for work, lo, hi, gxp in pending:
         work.wait()
         if gxp.data_ptr() != gx[lo:hi].data_ptr():
@@ -356,4 +377,6 @@ def vocab_parallel_flce(
     loss = loss_rows if reduction == "none" else loss_rows.sum()
     if check_targets and isinstance(ops, CudaVocabOps):
         raise_if_staged_out_of_range(staged, shard.total)
+        if peer is not None:
+            peer.check()
     return loss, gx, gw_acc.to(w_shard.dtype)

@@ -143,16 +143,20 @@ class PeerBuffer:
 _BUFFERS: dict = {}
 
 
-def grad_w_buffer(weight: torch.Tensor, group=None) -> PeerBuffer:
-    """The cached symmetric buffer that holds grad_w for `weight`'s shape on this device/group
-    (created collectively on first use: every rank must reach the first call)."""
-    nbytes = weight.numel() * weight.element_size()
-    key = (id(group), weight.device.index, nbytes)
+def buffer_for(nbytes: int, device: torch.device, group=None, tag: str = "") -> PeerBuffer:
+    """The cached symmetric buffer of `nbytes` for (`tag`, group, device), created collectively on
+    first use: every rank must reach the first call with the same arguments."""
+    key = (tag, id(group), torch.device(device).index, int(nbytes))
     buf = _BUFFERS.get(key)
     if buf is None or buf.poisoned:
-        buf = PeerBuffer(nbytes, group=group, device=weight.device)
+        buf = PeerBuffer(nbytes, group=group, device=device)
         _BUFFERS[key] = buf
     return buf
 
 
-__all__ = ["PeerBuffer", "PeerTimeout", "grad_w_buffer", "CTL_BYTES", "MAX_PEERS"]
+def grad_w_buffer(weight: torch.Tensor, group=None) -> PeerBuffer:
+    """The cached symmetric buffer that holds grad_w for `weight`'s shape (token-sharded mode)."""
+    return buffer_for(weight.numel() * weight.element_size(), weight.device, group, "grad_w")
+
+
+__all__ = ["PeerBuffer", "PeerTimeout", "buffer_for", "grad_w_buffer", "CTL_BYTES", "MAX_PEERS"]

@@ -132,7 +132,10 @@ def test_token_sharded_cuda_world2(kw):
 @pytest.mark.parametrize("kw", [dict(), dict(label_smoothing=0.1, softcap=30.0), dict(lse_square_scale=1e-4),
                                 dict(_ignore_first_half=True), dict(dx_reduce_dtype=torch.float32),
                                 dict(_dtype=torch.float32), dict(_min_skipped=1),
-                                dict(_min_skipped=1, _ignore_first_half=True, label_smoothing=0.1)])
+                                dict(_min_skipped=1, _ignore_first_half=True, label_smoothing=0.1),
+                                # dX partials summed by the peer-memory kernel (csrc/peer.cu)
+                                dict(comm="peer"), dict(comm="peer", _min_skipped=1),
+                                dict(comm="peer", dx_reduce_dtype=torch.float32)])
 def test_vocab_parallel_cuda_world2(kw):
     _run("vocab", kw)
 
